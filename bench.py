@@ -1,0 +1,474 @@
+#!/usr/bin/env python3
+"""Benchmark of the north-star path: HM-LSTM cell-update mixed-mode gradient
+(fused dual-number forward K1 + adjoint-reduction pullback K2, plus the NCCL
+allreduce of batch-broadcast adjoints when sharded), BASELINE.json metric
+"HM-LSTM cell-update grad elements/s & ms/step at 1/2/4/8 B200; % HBM roofline".
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config cfg2] [--impl native|reference]
+  python -m torch.distributed.run --nproc-per-node N --master-addr 127.0.0.1 bench.py --gpus N
+
+One step = one pass of the hot path over one batch: bcad_cu_forward (primal +
+M*N partials) then bcad_cu_pullback (all input adjoints) — what the
+reference's run_cell_once("mixed-cache") times (proj/src/bench.cpp:112-128).
+`value` = grad elements (output cells) per second over all ranks, inputs
+resident in HBM, L2 flushed between steps (a 1 GiB write, outside the timed
+events). `e2e` = the same step through the C-ABI with HOST buffers: pinned
+H2D of the step's inputs and seed, forward, pullback, D2H of the gradients.
+
+--impl reference times the reference's own CPU implementation (the
+unmodified /root/reference code compiled into oracle/_ref) on the host cores.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from paper_1810_08297_b200.workloads import WORKLOADS, Workload, shard_rows  # noqa: E402
+
+PEAKS_PATH = os.path.join(ROOT, "MEASURED_PEAKS.json")
+FALLBACK_HBM_GBS = 6650.0  # /opt/skills/guides/B200_PROFILING.md fallback
+NCU_SUMMARY = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+
+
+def hbm_peak():
+    try:
+        with open(PEAKS_PATH) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)"
+
+
+# ----------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region
+    (B200_PROFILING.md 'clocks' line)."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.idx = gpu_index
+        self.proc = None
+        self.path = None
+
+    def start(self):
+        try:
+            fd, self.path = tempfile.mkstemp(suffix=".csv")
+            os.close(fd)
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.idx), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+        time.sleep(0.25)
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        with open(self.path) as f:
+            for line in f:
+                parts = [p.strip() for p in line.split(",")]
+                if len(parts) < 9:
+                    continue
+                try:
+                    sm.append(float(parts[1]))
+                    mx = float(parts[2])
+                except ValueError:
+                    continue
+                for nm, v in zip(names, parts[5:9]):
+                    if v.lower() == "active":
+                        reasons.add(nm)
+        os.unlink(self.path)
+        busy = [s for s in sm if mx and s > 0.5 * mx] or sm
+        return {"sm_mhz": statistics.median(busy) if busy else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# -------------------------------------------------------------- reference
+def cpu_reference_rate(w: Workload, budget_s: float, min_reps: int = 1, threads: int = 0):
+    """Time the unmodified reference (oracle/_ref) on host cores: Tape +
+    mixed_broadcast(CacheForward) + backward(ones), bench.cpp:112-128.
+    Bounded sample: full rows up to a row cap sized to the budget."""
+    import numpy as np
+    import oracle as O
+    ref = O.Reference() if O.reference_available() else None
+    kind = "reference" if ref else "port"
+    lib = ref or O.Oracle()
+    # cells the reference processes per second is ~5e6 on 8 cores; cap rows
+    # so one rep stays well inside the budget.
+    rows = w.B
+    while rows > 1 and rows * w.H > 4e6 * max(1.0, budget_s / 4):
+        rows //= 2
+    sample = Workload(w.key, rows, w.H, w.dtype, w.variant, w.describe)
+    dtype = np.float32 if w.dtype == "f32" else np.float64
+    s = O.Oracle().mix_seed(42, w.B * 1000003 + w.H)
+    ins = lib.gen(s, dtype, list(zip(sample.shapes(), sample.kinds())))
+    ns = []
+    t_end = time.time() + budget_s
+    if ref:
+        ref.time_mixed(w.kernel, ins, threads=threads, warmup=1, reps=1)
+        while len(ns) < min_reps or time.time() < t_end:
+            ns += ref.time_mixed(w.kernel, ins, threads=threads, warmup=0, reps=1)
+        cores = ref.max_threads() if threads == 0 else threads
+    else:
+        while len(ns) < min_reps or time.time() < t_end:
+            t0 = time.perf_counter_ns()
+            lib.mixed_step(w.kernel, ins)
+            ns.append(time.perf_counter_ns() - t0)
+        cores = 1
+    med = statistics.median(ns)
+    cells = rows * w.H
+    return {"value": cells / (med * 1e-9), "unit": "grad elements/s", "cores": cores, "kind": kind,
+            "sample": f"{rows}x{w.H} rows of {w.B}x{w.H} {w.dtype} {w.variant}, {len(ns)} reps, median "
+                      f"{med / 1e6:.2f} ms/rep",
+            "ms_per_rep": med / 1e6, "reps": len(ns)}
+
+
+def run_reference_arm(args, w: Workload, rank: int, world: int):
+    if rank != 0:
+        return
+    import numpy as np  # noqa: F401
+    import oracle as O
+    ref = O.Reference() if O.reference_available() else None
+    kind = "reference" if ref else "port"
+    lib = ref or O.Oracle()
+    rows = w.B
+    while rows > 1 and rows * w.H > 2.1e6:  # a bounded sample per step (~0.2-0.5 s on 8 cores)
+        rows //= 2
+    sample = Workload(w.key, rows, w.H, w.dtype, w.variant, w.describe)
+    dtype = np.float32 if w.dtype == "f32" else np.float64
+    s = O.Oracle().mix_seed(42, w.B * 1000003 + w.H)
+    ins = lib.gen(s, dtype, list(zip(sample.shapes(), sample.kinds())))
+    if ref:
+        ref.time_mixed(w.kernel, ins, warmup=args.warmup, reps=1)
+        ns = ref.time_mixed(w.kernel, ins, warmup=0, reps=args.steps)
+        cores = ref.max_threads()
+    else:
+        for _ in range(args.warmup):
+            lib.mixed_step(w.kernel, ins)
+        ns = []
+        for _ in range(args.steps):
+            t0 = time.perf_counter_ns()
+            lib.mixed_step(w.kernel, ins)
+            ns.append(time.perf_counter_ns() - t0)
+        cores = 1
+    total_s = sum(ns) * 1e-9
+    cells = rows * w.H * len(ns)
+    val = cells / total_s
+    line = {"impl": "reference", "metric": "HM-LSTM cell-update grad elements/s", "value": val,
+            "unit": "grad elements/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": total_s * 1e3 / len(ns) * (w.B / rows), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": w.dtype, "data": "synthetic (bcad Rng, mix_seed)",
+            "config": {"workload": w.describe, "B": w.B, "H": w.H, "variant": w.variant},
+            "cpu_baseline": {"value": val, "unit": "grad elements/s", "cores": cores, "kind": kind,
+                             "sample": f"{rows}x{w.H} of {w.B}x{w.H} per step (rows are independent)"},
+            "e2e": {"value": val, "unit": "grad elements/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------ native
+class Case:
+    """Device buffers of one mixed step on this rank's batch shard."""
+
+    def __init__(self, w: Workload, B_local: int, device, seed: int, policy: int = 0):
+        import torch
+        from paper_1810_08297_b200 import native
+        self.w, self.B, self.policy = w, B_local, policy
+        dt = torch.float32 if w.dtype == "f32" else torch.float64
+        self.dt = dt
+        g = torch.Generator(device=device)
+        g.manual_seed(seed)
+        shapes = w.shapes(B_local)
+        self.shapes = shapes
+        ins = []
+        for s, kind in zip(shapes, w.kinds()):
+            if kind == "pm1":
+                ins.append(torch.rand(s, generator=g, device=device, dtype=dt) * 2 - 1)
+            else:
+                ins.append((torch.rand(s, generator=g, device=device, dtype=dt) < 0.5).to(dt))
+        self.ins = ins
+        self.k = native.Kernel(w.kernel)
+        out = (B_local, w.H)
+        self.primal = [torch.empty(out, device=device, dtype=dt)]
+        self.partials = ([torch.empty(out, device=device, dtype=dt) for _ in range(self.k.n_in)]
+                         if policy == 0 else [])
+        self.seed = torch.ones(out, device=device, dtype=dt)
+        # Input adjoints; the (1,H) bias adjoints share one contiguous
+        # buffer so a single allreduce combines them.
+        self.adj = []
+        self.bias_adj = None
+        if w.variant == "bias":
+            self.bias_adj = torch.empty((3, w.H), device=device, dtype=dt)
+        for j, s in enumerate(shapes):
+            if w.variant == "bias" and 4 <= j <= 6:
+                self.adj.append(self.bias_adj[j - 4:j - 3])
+            else:
+                self.adj.append(torch.empty(s, device=device, dtype=dt))
+        self.ws = native.new_workspace(self.k, shapes, dt, device)
+        self.step = native.PreparedStep(self.k, ins, self.primal, self.partials, [self.seed], self.adj, self.ws,
+                                        policy=policy)
+
+
+def run_native(args, w: Workload, rank: int, world: int):
+    import torch
+    import torch.distributed as dist
+    from paper_1810_08297_b200 import native
+
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    device = torch.device("cuda", local)
+    native.check(native.LIB.bcad_cu_set_device(local))
+
+    strong = w.key == "cfg5"
+    if strong:
+        b0, b1 = shard_rows(w.B, world, rank)
+        B_local = b1 - b0
+    else:
+        B_local = w.B  # weak scaling: one B-row batch per GPU
+    case = Case(w, B_local, device, seed=1234 + rank, policy=args.policy)
+    stream = torch.cuda.Stream(device)
+    sp = int(stream.cuda_stream)
+
+    comm = None
+    if world > 1 and w.variant == "bias":
+        uid = [native.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        comm = native.Comm(world, uid[0], rank)
+
+    flush = torch.empty(256 * 1024 * 1024, dtype=torch.float32, device=device)  # 1 GiB > 126 MB L2
+    K, W = args.steps, args.warmup
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(K)]
+
+    def one_step(evs=None):
+        if evs:
+            evs[0].record(stream)
+        case.step.forward(sp)
+        if evs:
+            evs[1].record(stream)
+        case.step.pullback(sp)
+        if evs:
+            evs[2].record(stream)
+        if comm is not None:
+            comm.allreduce([case.bias_adj], stream=stream)
+        if evs:
+            evs[3].record(stream)
+
+    with torch.cuda.stream(stream):
+        for _ in range(W):
+            flush.fill_(1.0)
+            one_step()
+    torch.cuda.synchronize(device)
+    if world > 1:
+        dist.barrier()
+
+    clocks = ClockSampler(local)
+    clocks.start()
+    torch.cuda.synchronize(device)
+    if world > 1:
+        dist.barrier()
+    with torch.cuda.stream(stream):
+        for k in range(K):
+            flush.fill_(float(k))
+            one_step(ev[k])
+    torch.cuda.synchronize(device)
+    if world > 1:
+        dist.barrier()
+    clock_info = clocks.stop()
+
+    step_ms = [e[0].elapsed_time(e[3]) for e in ev]
+    k1_ms = [e[0].elapsed_time(e[1]) for e in ev]
+    k2_ms = [e[1].elapsed_time(e[2]) for e in ev]
+    ar_ms = [e[2].elapsed_time(e[3]) for e in ev]
+    total_ms = sum(step_ms)
+    if world > 1:
+        t = torch.tensor([total_ms], device=device, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+    ms_per_step = total_ms / K
+    cells_per_step = (w.B if strong else w.B * world) * w.H
+    value = cells_per_step / (ms_per_step * 1e-3)
+
+    # ---- end to end through the C-ABI with host buffers
+    e2e = run_e2e(case, stream, args.e2e_steps, device)
+    if world > 1:
+        t = torch.tensor([e2e["ms_per_step"]], device=device, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e["ms_per_step"] = float(t.item())
+    e2e_value = cells_per_step / (e2e["ms_per_step"] * 1e-3)
+
+    # ---- roofline of the dominant kernel
+    peak, peak_src = hbm_peak()
+    k1_avg, k2_avg = statistics.mean(k1_ms), statistics.mean(k2_ms)
+    dom = "K1_forward" if k1_avg >= k2_avg else "K2_pullback"
+    dom_bytes = w.k1_bytes(B_local, args.policy) if dom == "K1_forward" else w.k2_bytes(B_local, args.policy)
+    dom_ms = max(k1_avg, k2_avg)
+    achieved = dom_bytes / (dom_ms * 1e-3) / 1e9
+    traffic = None
+    try:
+        with open(NCU_SUMMARY) as f:
+            traffic = json.load(f).get(w.key, {}).get(dom)
+    except Exception:
+        pass
+    step_bytes = w.step_bytes(B_local, args.policy)
+
+    if rank != 0:
+        return
+    extra = {}
+    if world == 1 and args.extra:
+        for key in args.extra.split(","):
+            if key and key != w.key:
+                extra[key] = measure_secondary(WORKLOADS[key], device, stream, max(5, K // 2), args.policy)
+
+    cpu = None
+    if world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_reference_rate(w, budget_s=args.cpu_budget)
+
+    line = {
+        "metric": "HM-LSTM cell-update grad elements/s", "value": value, "unit": "grad elements/s",
+        "n_gpus": world, "steps": K, "warmup": W, "ms_per_step": ms_per_step, "higher_is_better": True,
+        "scaling": "strong" if strong else "weak", "vs_baseline": None, "dtype": w.dtype,
+        "data": "synthetic (device Philox U(-1,1) gates, Bernoulli(1/2) exact-binary z), seed of ones",
+        "config": {"workload": w.describe, "B": w.B, "H": w.H, "B_per_gpu": B_local, "variant": w.variant,
+                   "policy": "CacheForward" if args.policy == 0 else "RecomputeReverse",
+                   "parallelism": f"batch-sharded dp{world}" if world > 1 else "single GPU",
+                   "l2": "flushed between steps (1 GiB write outside the timed events)"},
+        "breakdown_ms": {"K1_forward": k1_avg, "K2_pullback": k2_avg, "allreduce": statistics.mean(ar_ms),
+                         "step_min": min(step_ms), "step_median": statistics.median(step_ms)},
+        "step_roofline": {"bytes": step_bytes, "achieved_GBps": step_bytes / (statistics.mean(step_ms) * 1e-3) / 1e9,
+                          "frac": step_bytes / (statistics.mean(step_ms) * 1e-3) / 1e9 / peak},
+        "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": traffic, "algorithmic_bytes_per_launch": dom_bytes,
+                     "peak_source": peak_src},
+        "e2e": {"value": e2e_value, "unit": "grad elements/s", "h2d_bytes_per_step": e2e["h2d"],
+                "d2h_bytes_per_step": e2e["d2h"], "ms_per_step": e2e["ms_per_step"]},
+        "gpu_launches": 2 * K,
+        "clocks": clock_info,
+    }
+    if cpu:
+        line["cpu_baseline"] = cpu
+    if extra:
+        line["extra"] = extra
+    print(json.dumps(line), flush=True)
+
+
+def run_e2e(case: Case, stream, steps: int, device):
+    """Host buffers in, host gradients out, every step: pinned H2D of the
+    inputs and the seed, K1, K2, D2H of every input gradient."""
+    import torch
+    host_in = [t.cpu().pin_memory() for t in case.ins]
+    host_seed = case.seed.cpu().pin_memory()
+    host_grad = [torch.empty(t.shape, dtype=t.dtype).pin_memory() for t in case.adj]
+    h2d = sum(t.numel() * t.element_size() for t in host_in) + host_seed.numel() * host_seed.element_size()
+    d2h = sum(t.numel() * t.element_size() for t in host_grad)
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    sp = int(stream.cuda_stream)
+
+    def go():
+        for d, h in zip(case.ins, host_in):
+            d.copy_(h, non_blocking=True)
+        case.seed.copy_(host_seed, non_blocking=True)
+        case.step.forward(sp)
+        case.step.pullback(sp)
+        for h, d in zip(host_grad, case.adj):
+            h.copy_(d, non_blocking=True)
+
+    with torch.cuda.stream(stream):
+        go()
+        torch.cuda.synchronize(device)
+        start.record(stream)
+        for _ in range(steps):
+            go()
+        end.record(stream)
+    torch.cuda.synchronize(device)
+    return {"ms_per_step": start.elapsed_time(end) / steps, "h2d": h2d, "d2h": d2h}
+
+
+def measure_secondary(w: Workload, device, stream, steps: int, policy: int):
+    import torch
+    case = Case(w, w.B, device, seed=99, policy=policy)
+    flush = torch.empty(256 * 1024 * 1024, dtype=torch.float32, device=device)
+    sp = int(stream.cuda_stream)
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(steps)]
+    with torch.cuda.stream(stream):
+        for k in range(3 + steps):
+            flush.fill_(1.0)
+            e = ev[k - 3] if k >= 3 else None
+            if e:
+                e[0].record(stream)
+            case.step.forward(sp)
+            if e:
+                e[1].record(stream)
+            case.step.pullback(sp)
+            if e:
+                e[2].record(stream)
+    torch.cuda.synchronize(device)
+    peak, _ = hbm_peak()
+    step = statistics.mean(e[0].elapsed_time(e[2]) for e in ev)
+    k1 = statistics.mean(e[0].elapsed_time(e[1]) for e in ev)
+    k2 = statistics.mean(e[1].elapsed_time(e[2]) for e in ev)
+    b1, b2 = w.k1_bytes(policy=policy), w.k2_bytes(policy=policy)
+    out = {"workload": w.describe, "ms_per_step": step, "value": w.E / (step * 1e-3), "unit": "grad elements/s",
+           "K1_ms": k1, "K2_ms": k2, "K1_frac_hbm": b1 / (k1 * 1e-3) / 1e9 / peak,
+           "K2_frac_hbm": b2 / (k2 * 1e-3) / 1e9 / peak,
+           "step_frac_hbm": (b1 + b2) / (step * 1e-3) / 1e9 / peak}
+    del case
+    torch.cuda.empty_cache()
+    return out
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default="cfg2", choices=sorted(WORKLOADS))
+    ap.add_argument("--impl", default="native", choices=["native", "reference"])
+    ap.add_argument("--policy", type=int, default=0, help="0 CacheForward, 1 RecomputeReverse")
+    ap.add_argument("--e2e-steps", type=int, default=10)
+    ap.add_argument("--extra", default="cfg3,cfg4,cfg4div,cfg5", help="secondary configs measured at N=1")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-budget", type=float, default=12.0)
+    args = ap.parse_args()
+    if args.warmup < 3:
+        ap.error("--warmup must be >= 3")
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    w = WORKLOADS[args.config]
+    if args.impl == "reference":
+        run_reference_arm(args, w, rank, world)
+        return
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")))
+        dist.init_process_group("nccl")
+    try:
+        run_native(args, w, rank, world)
+    finally:
+        if world > 1:
+            import torch.distributed as dist
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,132 @@
+// Forward broadcast evaluation on the device:
+//   broadcast_apply         (reference proj/include/bcad/broadcast.hpp:102-125)
+//   broadcast_diag_jacobian (reference proj/include/bcad/forward.hpp:98-150)
+//   scatter_add             (reference proj/include/bcad/broadcast.hpp:210-217)
+// Each is one C-ABI call into the fused sm_100a kernels.
+#pragma once
+
+#include <array>
+#include <span>
+#include <vector>
+
+#include "bcad/kernel.hpp"
+#include "bcad/tensor.hpp"
+
+namespace bcad {
+
+template <class Real>
+struct DiagJacobian {
+    Shape out_shape;
+    int outputs = 0;  // M
+    int inputs = 0;   // N
+    std::vector<Tensor<Real>> entries;  // M*N tensors, all of out_shape
+
+    Tensor<Real>& entry(int i, int j) { return entries[static_cast<std::size_t>(i * inputs + j)]; }
+    const Tensor<Real>& entry(int i, int j) const { return entries[static_cast<std::size_t>(i * inputs + j)]; }
+};
+
+template <class Real>
+struct ForwardBroadcastResult {
+    std::vector<Tensor<Real>> primals;  // populated only when requested
+    DiagJacobian<Real> jacobian;
+};
+
+namespace detail {
+
+template <class Real>
+std::vector<bcad_cu_shape> c_shapes(std::span<const Tensor<Real>* const> args) {
+    std::vector<bcad_cu_shape> s;
+    s.reserve(args.size());
+    for (const Tensor<Real>* t : args) s.push_back(t->shape().c_shape());
+    return s;
+}
+
+template <class Real>
+Shape out_shape_of(std::span<const Tensor<Real>* const> args) {
+    std::vector<Shape> s;
+    s.reserve(args.size());
+    for (const Tensor<Real>* t : args) s.push_back(t->shape());
+    return broadcast_shape(std::span<const Shape>(s));
+}
+
+template <class Real>
+void check_arity(const BroadcastKernel<Real>& kernel, std::size_t n, const char* who) {
+    if (static_cast<int>(n) != kernel.arity_in())
+        throw ArityMismatch(std::string(who) + ": kernel " + kernel.name() + " expects " +
+                            std::to_string(kernel.arity_in()) + " arguments, got " + std::to_string(n));
+}
+
+}  // namespace detail
+
+template <class Real>
+std::vector<Tensor<Real>> broadcast_apply(const BroadcastKernel<Real>& kernel,
+                                          std::span<const Tensor<Real>* const> args) {
+    detail::check_arity(kernel, args.size(), "broadcast_apply");
+    const Shape out = detail::out_shape_of<Real>(args);
+    const auto shapes = detail::c_shapes<Real>(args);
+    std::vector<const void*> in;
+    for (const Tensor<Real>* t : args) in.push_back(t->device_data());
+    std::vector<Tensor<Real>> outs;
+    std::vector<void*> po;
+    for (int i = 0; i < kernel.arity_out(); ++i) {
+        outs.push_back(Tensor<Real>::uninitialized(out));
+        po.push_back(outs.back().device_data());
+    }
+    check(bcad_cu_forward(kernel.handle(), dtype_of<Real>::value, kernel.arity_in(), in.data(), shapes.data(),
+                          kernel.arity_out(), po.data(), nullptr, current_stream()));
+    return outs;
+}
+
+template <class Real, class... Ts>
+    requires(std::same_as<std::remove_cvref_t<Ts>, Tensor<Real>> && ...)
+std::vector<Tensor<Real>> broadcast_apply(const BroadcastKernel<Real>& kernel, const Ts&... args) {
+    const std::array<const Tensor<Real>*, sizeof...(Ts)> ptrs{&args...};
+    return broadcast_apply<Real>(kernel, std::span<const Tensor<Real>* const>(ptrs));
+}
+
+template <class Real>
+ForwardBroadcastResult<Real> broadcast_diag_jacobian(const BroadcastKernel<Real>& kernel,
+                                                     std::span<const Tensor<Real>* const> args, bool want_primal) {
+    detail::check_arity(kernel, args.size(), "broadcast_diag_jacobian");
+    const Shape out = detail::out_shape_of<Real>(args);
+    const auto shapes = detail::c_shapes<Real>(args);
+    const int n = kernel.arity_in(), m = kernel.arity_out();
+    std::vector<const void*> in;
+    for (const Tensor<Real>* t : args) in.push_back(t->device_data());
+    ForwardBroadcastResult<Real> r;
+    r.jacobian.out_shape = out;
+    r.jacobian.outputs = m;
+    r.jacobian.inputs = n;
+    std::vector<void*> pp, po;
+    for (int k = 0; k < m * n; ++k) {
+        r.jacobian.entries.push_back(Tensor<Real>::uninitialized(out));
+        pp.push_back(r.jacobian.entries.back().device_data());
+    }
+    if (want_primal)
+        for (int i = 0; i < m; ++i) {
+            r.primals.push_back(Tensor<Real>::uninitialized(out));
+            po.push_back(r.primals.back().device_data());
+        }
+    check(bcad_cu_forward(kernel.handle(), dtype_of<Real>::value, n, in.data(), shapes.data(), m,
+                          want_primal ? po.data() : nullptr, pp.data(), current_stream()));
+    return r;
+}
+
+template <class Real, class... Ts>
+    requires(std::same_as<std::remove_cvref_t<Ts>, Tensor<Real>> && ...)
+ForwardBroadcastResult<Real> broadcast_diag_jacobian(const BroadcastKernel<Real>& kernel, bool want_primal,
+                                                     const Ts&... args) {
+    const std::array<const Tensor<Real>*, sizeof...(Ts)> ptrs{&args...};
+    return broadcast_diag_jacobian<Real>(kernel, std::span<const Tensor<Real>* const>(ptrs), want_primal);
+}
+
+// The central broadcast-adjoint rule: reduces `contribution` over axes `acc`
+// lacks, or expands it along axes `acc` has and it lacks.
+template <class Real>
+void scatter_add(Tensor<Real>& acc, const Tensor<Real>& contribution, bool zero_first = false) {
+    const bcad_cu_shape a = acc.shape().c_shape(), c = contribution.shape().c_shape();
+    check(bcad_cu_scatter_add(dtype_of<Real>::value, acc.device_data(), &a, contribution.device_data(), &c,
+                              zero_first ? 1 : 0, current_stream()));
+}
+
+}  // namespace bcad

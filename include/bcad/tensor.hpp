@@ -1,0 +1,171 @@
+// Dense row-major array of 32- or 64-bit reals, resident in device memory.
+//
+// Same value-type contract as the reference Tensor (proj/include/bcad/
+// tensor.hpp:12-69): copyable (deep copy, device-to-device), single writer,
+// no views. The storage lives in HBM, allocated stream-ordered from the
+// device's caching pool through the C-ABI (bcad_cu_malloc); host access is
+// explicit (from / to_host) or element-wise through a synchronous read.
+#pragma once
+
+#include <cstdint>
+#include <cstring>
+#include <memory>
+#include <ostream>
+#include <span>
+#include <vector>
+
+#include "bcad/errors.hpp"
+#include "bcad/rng.hpp"
+#include "bcad/shape.hpp"
+
+namespace bcad {
+
+template <class T> struct dtype_of;
+template <> struct dtype_of<float> { static constexpr int value = BCAD_CU_F32; };
+template <> struct dtype_of<double> { static constexpr int value = BCAD_CU_F64; };
+
+// The stream every device tensor and tape of this thread enqueues on
+// (nullptr = the legacy default stream).
+inline void*& current_stream() {
+    static thread_local void* s = nullptr;
+    return s;
+}
+
+// RAII scope that redirects the current stream.
+class StreamGuard {
+public:
+    explicit StreamGuard(void* s) : prev_(current_stream()) { current_stream() = s; }
+    ~StreamGuard() { current_stream() = prev_; }
+    StreamGuard(const StreamGuard&) = delete;
+    StreamGuard& operator=(const StreamGuard&) = delete;
+
+private:
+    void* prev_;
+};
+
+namespace detail {
+
+struct DeviceBuffer {
+    void* ptr = nullptr;
+    void* stream = nullptr;
+    DeviceBuffer(std::size_t bytes, void* s) : stream(s) { check(bcad_cu_malloc(&ptr, bytes, s)); }
+    ~DeviceBuffer() { bcad_cu_free(ptr, stream); }
+    DeviceBuffer(const DeviceBuffer&) = delete;
+    DeviceBuffer& operator=(const DeviceBuffer&) = delete;
+};
+
+}  // namespace detail
+
+template <class T>
+class Tensor {
+public:
+    using value_type = T;
+
+    Tensor() : Tensor(Shape{}) {}
+    explicit Tensor(Shape shape, T fill = T(0)) : shape_(std::move(shape)) {
+        allocate();
+        check(bcad_cu_fill(dtype_of<T>::value, buf_->ptr, volume(), static_cast<double>(fill), stream()));
+    }
+
+    // Allocation without initialisation (the device kernels overwrite it).
+    static Tensor uninitialized(Shape shape) {
+        Tensor t(NoInit{}, std::move(shape));
+        return t;
+    }
+
+    static Tensor scalar(T value) { return Tensor(Shape{}, value); }
+
+    static Tensor from(Shape shape, const std::vector<T>& data) {
+        if (static_cast<std::int64_t>(data.size()) != shape.volume())
+            throw ShapeMismatch("tensor data length " + std::to_string(data.size()) + " does not match shape " +
+                                shape.str());
+        return from_host(std::move(shape), data.data());
+    }
+
+    // Upload `shape.volume()` values from host memory (pinned memory makes
+    // the copy asynchronous; pageable memory is staged by the driver).
+    static Tensor from_host(Shape shape, const T* data) {
+        Tensor t(NoInit{}, std::move(shape));
+        check(bcad_cu_memcpy(t.buf_->ptr, data, t.bytes(), 0, t.stream()));
+        return t;
+    }
+
+    Tensor(const Tensor& o) : shape_(o.shape_) {
+        allocate();
+        check(bcad_cu_memcpy(buf_->ptr, o.buf_->ptr, bytes(), 2, stream()));
+    }
+    Tensor& operator=(const Tensor& o) {
+        if (this != &o) *this = Tensor(o);
+        return *this;
+    }
+    Tensor(Tensor&&) noexcept = default;
+    Tensor& operator=(Tensor&&) noexcept = default;
+
+    const Shape& shape() const { return shape_; }
+    std::int64_t volume() const { return shape_.volume(); }
+    std::size_t bytes() const { return static_cast<std::size_t>(volume()) * sizeof(T); }
+    T* device_data() { return static_cast<T*>(buf_->ptr); }
+    const T* device_data() const { return static_cast<const T*>(buf_->ptr); }
+    void* stream() const { return buf_ ? buf_->stream : current_stream(); }
+
+    void copy_to_host(T* dst) const {
+        check(bcad_cu_memcpy(dst, buf_->ptr, bytes(), 1, stream()));
+        check(bcad_cu_stream_synchronize(stream()));
+    }
+    std::vector<T> to_host() const {
+        std::vector<T> h(static_cast<std::size_t>(volume()));
+        copy_to_host(h.data());
+        return h;
+    }
+
+    // Synchronous single-element read (test convenience, not a hot path).
+    T operator[](std::int64_t flat) const {
+        T v{};
+        check(bcad_cu_memcpy(&v, device_data() + flat, sizeof(T), 1, stream()));
+        check(bcad_cu_stream_synchronize(stream()));
+        return v;
+    }
+    T at(std::span<const std::int64_t> index) const {
+        std::int64_t flat = 0;
+        for (int k = 0; k < shape_.rank(); ++k) flat = flat * shape_.dim(k) + index[static_cast<std::size_t>(k)];
+        return (*this)[flat];
+    }
+    T at(std::initializer_list<std::int64_t> index) const {
+        return at(std::span<const std::int64_t>(index.begin(), index.size()));
+    }
+
+    void write_csv(std::ostream& os) const {  // tensor.hpp:53-61
+        const std::vector<T> h = to_host();
+        os << "# shape " << shape_.str() << "\n";
+        const std::int64_t row = shape_.rank() > 0 ? shape_.dim(shape_.rank() - 1) : 1;
+        for (std::int64_t i = 0; i < volume(); ++i) {
+            os << h[static_cast<std::size_t>(i)];
+            os << ((i % row == row - 1) ? '\n' : ',');
+        }
+    }
+
+private:
+    struct NoInit {};
+    Tensor(NoInit, Shape shape) : shape_(std::move(shape)) { allocate(); }
+    void allocate() { buf_ = std::make_unique<detail::DeviceBuffer>(bytes(), current_stream()); }
+
+    Shape shape_;
+    std::unique_ptr<detail::DeviceBuffer> buf_;
+};
+
+// Host-generated, bit-identical to the reference's inputs (tensor.hpp:71-84).
+template <class T>
+Tensor<T> random_pm1(Shape shape, Rng& rng) {
+    std::vector<T> h(static_cast<std::size_t>(shape.volume()));
+    for (T& v : h) v = static_cast<T>(rng.uniform_pm1());
+    return Tensor<T>::from(std::move(shape), h);
+}
+
+template <class T>
+Tensor<T> random_binary(Shape shape, Rng& rng, double p_one = 0.5) {
+    std::vector<T> h(static_cast<std::size_t>(shape.volume()));
+    for (T& v : h) v = static_cast<T>(rng.binary(p_one));
+    return Tensor<T>::from(std::move(shape), h);
+}
+
+}  // namespace bcad

@@ -1,0 +1,122 @@
+"""In-tree build of the native libraries (no JIT cache: the .so files travel
+with the repo snapshot to the GPU box).
+
+* ``paper_1810_08297_b200/libbcad_cu.so`` — CUDA kernels + the C-ABI of
+  ``include/bcad_cu.h``; nvcc, sm_100a only, ``--fmad=false`` so every source
+  operation rounds once (the reference builds with ``-ffp-contract=off``,
+  proj/src/CMakeLists.txt:9-14).
+* ``paper_1810_08297_b200/libbcad_host.so`` — the C++ drop-in host API
+  (``include/bcad/*.hpp``) exported for end-to-end calls with host buffers.
+* ``tests/cpp/*`` — reference-style C++ test programs against the drop-in API.
+"""
+from __future__ import annotations
+
+import concurrent.futures as cf
+import glob
+import os
+import shutil
+import subprocess
+import sys
+
+PKG = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(PKG)
+CSRC = os.path.join(PKG, "csrc")
+INCLUDE = os.path.join(ROOT, "include")
+BUILD = os.path.join(ROOT, "build")
+LIB = os.path.join(PKG, "libbcad_cu.so")
+HOST_LIB = os.path.join(PKG, "libbcad_host.so")
+
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+NVCC_FLAGS = ["-std=c++20", "-O3", "--fmad=false", "-lineinfo", "-Xcompiler", "-fPIC,-O3",
+              "-I" + INCLUDE, "-I" + CSRC] + ARCH
+
+
+def nvcc() -> str:
+    cand = shutil.which("nvcc") or "/usr/local/cuda/bin/nvcc"
+    return cand
+
+
+def cxx() -> str:
+    # The image may export CXX=/opt/gcc/... (no libgomp); the system g++ is the
+    # one nvcc and the oracle use.
+    return "/usr/bin/g++" if os.path.exists("/usr/bin/g++") else "g++"
+
+
+def _newer(target: str, deps: list[str]) -> bool:
+    if not os.path.exists(target):
+        return True
+    t = os.path.getmtime(target)
+    return any(os.path.getmtime(d) > t for d in deps)
+
+
+def _run(cmd: list[str], verbose: bool):
+    if verbose:
+        print(" ".join(cmd), flush=True)
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        raise RuntimeError(f"command failed ({r.returncode}): {' '.join(cmd)}\n{r.stdout}\n{r.stderr}")
+    return r
+
+
+def build_cuda(verbose: bool = False, jobs: int | None = None) -> str:
+    os.makedirs(BUILD, exist_ok=True)
+    headers = glob.glob(os.path.join(CSRC, "*.cuh")) + glob.glob(os.path.join(CSRC, "*.hpp")) + \
+        [os.path.join(INCLUDE, "bcad_cu.h")]
+    sources = sorted(glob.glob(os.path.join(CSRC, "*.cu")))
+    objs = []
+    todo = []
+    for src in sources:
+        obj = os.path.join(BUILD, os.path.basename(src) + ".o")
+        objs.append(obj)
+        if _newer(obj, [src] + headers):
+            todo.append([nvcc(), *NVCC_FLAGS, "-c", src, "-o", obj])
+    jobs = jobs or max(1, min(len(todo), os.cpu_count() or 4))
+    with cf.ThreadPoolExecutor(jobs) as ex:
+        for f in [ex.submit(_run, c, verbose) for c in todo]:
+            f.result()
+    if todo or _newer(LIB, objs):
+        _run([nvcc(), "-shared", *ARCH, "-o", LIB, *objs, "-ldl", "-Xcompiler", "-fPIC"], verbose)
+    return LIB
+
+
+def build_host(verbose: bool = False) -> str:
+    src = os.path.join(CSRC, "host_api.cpp")
+    deps = [src] + glob.glob(os.path.join(INCLUDE, "bcad", "*.hpp")) + [os.path.join(INCLUDE, "bcad_cu.h"), LIB]
+    if _newer(HOST_LIB, deps):
+        _run([cxx(), "-std=c++20", "-O2", "-fPIC", "-shared", "-Wall", "-Wextra", "-I" + INCLUDE, src,
+              "-o", HOST_LIB, "-L" + PKG, "-lbcad_cu", "-Wl,-rpath,$ORIGIN"], verbose)
+    return HOST_LIB
+
+
+def build_cpp_tests(verbose: bool = False) -> list[str]:
+    out = []
+    tdir = os.path.join(ROOT, "tests", "cpp")
+    for src in sorted(glob.glob(os.path.join(tdir, "test_*.cpp"))):
+        exe = os.path.join(BUILD, os.path.splitext(os.path.basename(src))[0])
+        deps = [src] + glob.glob(os.path.join(tdir, "*.hpp")) + glob.glob(os.path.join(INCLUDE, "bcad", "*.hpp")) + [LIB]
+        if _newer(exe, deps):
+            _run([cxx(), "-std=c++20", "-O2", "-Wall", "-Wextra", "-I" + INCLUDE, "-I" + tdir, src, "-o", exe,
+                  "-L" + PKG, "-lbcad_cu", "-Wl,-rpath," + PKG], verbose)
+        out.append(exe)
+    return out
+
+
+def build_oracle(verbose: bool = False):
+    """Checker builds (test infrastructure): oracle/liboracle.so always;
+    oracle/_ref/libbcad_ref.so only where /root/reference exists."""
+    mk = os.path.join(ROOT, "oracle", "Makefile")
+    targets = ["all"] if os.path.isdir("/root/reference/proj") else [os.path.join(ROOT, "oracle", "liboracle.so")]
+    _run(["make", "-s", "-f", mk, *targets], verbose)
+
+
+def build_all(verbose: bool = False):
+    build_cuda(verbose)
+    if os.path.exists(os.path.join(CSRC, "host_api.cpp")):
+        build_host(verbose)
+    build_cpp_tests(verbose)
+    build_oracle(verbose)
+
+
+if __name__ == "__main__":
+    build_all(verbose="-v" in sys.argv)
+    print("built", LIB)

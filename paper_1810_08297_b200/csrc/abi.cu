@@ -1,0 +1,542 @@
+// C-ABI implementation (include/bcad_cu.h): registry lookup, plan checks,
+// launches, error-word decoding, device memory, streams and NCCL.
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+
+#include <cstdint>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "bcad_cu.h"
+#include "plan.hpp"
+#include "registry.hpp"
+
+using namespace bcad_cu_impl;
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string& msg) {
+    g_err = msg;
+    return code;
+}
+
+int cuda_fail(cudaError_t e, const char* what) {
+    return fail(BCAD_CU_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+#define CU_TRY(expr, what)                          \
+    do {                                            \
+        const cudaError_t e_ = (expr);              \
+        if (e_ != cudaSuccess) return cuda_fail(e_, what); \
+    } while (0)
+
+// ---------------------------------------------------------------- registry
+struct Registry {
+    std::vector<const bcad_cu_kernel_entry*> all;
+    Registry() {
+        int (*groups[])(const bcad_cu_kernel_entry**) = {&bcad_reg_hmlstm, &bcad_reg_pool, &bcad_reg_probe,
+                                                         &bcad_reg_arity};
+        for (auto g : groups) {
+            const bcad_cu_kernel_entry* e = nullptr;
+            const int n = g(&e);
+            for (int i = 0; i < n; ++i) all.push_back(e + i);
+        }
+    }
+};
+
+const Registry& registry() {
+    static const Registry r;
+    return r;
+}
+
+// ---------------------------------------------------------- error words
+constexpr int kMaxDevices = 64;
+std::mutex g_err_mutex;
+unsigned long long* g_err_word[kMaxDevices] = {};
+
+int error_word(unsigned long long** out) {
+    int dev = 0;
+    CU_TRY(cudaGetDevice(&dev), "cudaGetDevice");
+    if (dev < 0 || dev >= kMaxDevices) return fail(BCAD_CU_ERR_CUDA, "device ordinal out of range");
+    std::lock_guard<std::mutex> lock(g_err_mutex);
+    if (!g_err_word[dev]) {
+        void* p = nullptr;
+        CU_TRY(cudaMalloc(&p, sizeof(unsigned long long)), "cudaMalloc(error word)");
+        g_err_word[dev] = static_cast<unsigned long long*>(p);
+    }
+    *out = g_err_word[dev];
+    return BCAD_CU_OK;
+}
+
+std::string index_string(const Plan& plan, int64_t flat) {  // forward.hpp:76-87
+    int64_t idx[kMaxRank] = {};
+    for (int k = plan.out_rank - 1; k >= 0; --k) {
+        idx[k] = flat % plan.out_dims[k];
+        flat /= plan.out_dims[k];
+    }
+    std::string s = "(";
+    for (int k = 0; k < plan.out_rank; ++k) {
+        if (k) s += ", ";
+        s += std::to_string(idx[k]);
+    }
+    return s + ")";
+}
+
+int check_error_word(unsigned long long* word, cudaStream_t stream, const Plan& plan) {
+    unsigned long long host = 0;
+    CU_TRY(cudaMemcpyAsync(&host, word, sizeof(host), cudaMemcpyDeviceToHost, stream), "cudaMemcpyAsync(error word)");
+    CU_TRY(cudaStreamSynchronize(stream), "cudaStreamSynchronize");
+    if (host == ~0ull) return BCAD_CU_OK;
+    const int code = int(host >> 56);
+    const int64_t flat = int64_t(host & ((1ull << 56) - 1));
+    const char* what = code == BCAD_CU_ERR_DIVISION_BY_ZERO   ? "dual division by zero"
+                       : code == BCAD_CU_ERR_DOMAIN           ? "primal outside the primitive's domain"
+                       : code == BCAD_CU_ERR_NON_DIFFERENTIABLE ? "primitive is not differentiable at this primal"
+                                                               : "kernel error";
+    return fail(code, std::string(what) + " at output index " + index_string(plan, flat));
+}
+
+int arity_check(const bcad_cu_kernel_entry* k, int n_in, int m_out) {
+    if (!k) return fail(BCAD_CU_ERR_UNKNOWN_PRIMITIVE, "null kernel handle");
+    if (n_in != k->n_in)
+        return fail(BCAD_CU_ERR_ARITY_MISMATCH, std::string("kernel ") + k->name + " expects " +
+                                                    std::to_string(k->n_in) + " arguments, got " +
+                                                    std::to_string(n_in));
+    if (m_out != k->m_out)
+        return fail(BCAD_CU_ERR_ARITY_MISMATCH, std::string("kernel ") + k->name + " produces " +
+                                                    std::to_string(k->m_out) + " outputs, got " +
+                                                    std::to_string(m_out));
+    return BCAD_CU_OK;
+}
+
+int dtype_check(int dtype) {
+    if (dtype != BCAD_CU_F32 && dtype != BCAD_CU_F64) return fail(BCAD_CU_ERR_CONFIG, "dtype must be F32 or F64");
+    return BCAD_CU_OK;
+}
+
+// --------------------------------------------------------- utility kernels
+template <class T>
+__global__ void fill_kernel(T* p, int64_t n, T v) {
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x)
+        p[i] = v;
+}
+
+template <class T>
+__global__ void add_same_kernel(T* acc, const T* c, int64_t n, bool zero_first) {
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x)
+        acc[i] = (zero_first ? T(0) : acc[i]) + c[i];
+}
+
+struct ScatterGeom {
+    int rank;
+    int64_t out_dims[kMaxRank];
+    int64_t acc_strides[kMaxRank];
+    int64_t con_strides[kMaxRank];
+    int64_t acc_vol;
+};
+
+// One thread per slot element: the expanded cells of `acc` are walked in
+// row-major order (broadcast.hpp:210-217); reductions accumulate in fp64.
+template <class T>
+__global__ void scatter_add_kernel(T* acc, const T* con, ScatterGeom g, bool zero_first) {
+    for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < g.acc_vol;
+         e += int64_t(gridDim.x) * blockDim.x) {
+        int64_t coord[kMaxRank];
+        int64_t rem = e, cnt = 1;
+        for (int k = g.rank - 1; k >= 0; --k) {
+            if (g.acc_strides[k] != 0) {
+                coord[k] = rem % g.out_dims[k];
+                rem /= g.out_dims[k];
+            } else {
+                coord[k] = 0;
+                cnt *= g.out_dims[k];
+            }
+        }
+        T exact = zero_first ? T(0) : acc[e];
+        double sum = 0.0;
+        for (int64_t q = 0; q < cnt; ++q) {
+            int64_t ci = 0;
+            for (int k = 0; k < g.rank; ++k) ci += coord[k] * g.con_strides[k];
+            if (cnt == 1) exact = exact + con[ci];
+            else sum += double(con[ci]);
+            for (int k = g.rank - 1; k >= 0; --k) {
+                if (g.acc_strides[k] != 0 || g.out_dims[k] == 1) continue;
+                if (++coord[k] < g.out_dims[k]) break;
+                coord[k] = 0;
+            }
+        }
+        acc[e] = cnt == 1 ? exact : T((zero_first ? 0.0 : double(acc[e])) + sum);
+    }
+}
+
+int grid_for(int64_t n) {
+    const int64_t b = (n + 255) / 256;
+    return int(b < 1 ? 1 : (b > 148 * 16 ? 148 * 16 : b));
+}
+
+// ------------------------------------------------------------------ NCCL
+// Minimal run-time binding (nccl.h ABI: ncclUniqueId is 128 bytes; enum
+// values ncclFloat32 = 7, ncclFloat64 = 8, ncclSum = 0).
+struct Nccl {
+    void* h = nullptr;
+    int (*GetUniqueId)(void*) = nullptr;
+    int (*CommInitRank)(void**, int, const void*, int) = nullptr;  // id passed by value (128 B)
+    int (*CommDestroy)(void*) = nullptr;
+    int (*AllReduce)(const void*, void*, size_t, int, int, void*, cudaStream_t) = nullptr;
+    int (*GroupStart)() = nullptr;
+    int (*GroupEnd)() = nullptr;
+    const char* (*GetErrorString)(int) = nullptr;
+    bool ok = false;
+};
+
+struct NcclUniqueId {
+    char internal[128];
+};
+
+Nccl& nccl() {
+    static Nccl n = [] {
+        Nccl x;
+        for (const char* name : {"libnccl.so.2", "libnccl.so"}) {
+            x.h = dlopen(name, RTLD_NOW | RTLD_GLOBAL);
+            if (x.h) break;
+        }
+        if (!x.h) return x;
+        x.GetUniqueId = reinterpret_cast<int (*)(void*)>(dlsym(x.h, "ncclGetUniqueId"));
+        x.CommInitRank = reinterpret_cast<int (*)(void**, int, const void*, int)>(dlsym(x.h, "ncclCommInitRank"));
+        x.CommDestroy = reinterpret_cast<int (*)(void*)>(dlsym(x.h, "ncclCommDestroy"));
+        x.AllReduce = reinterpret_cast<int (*)(const void*, void*, size_t, int, int, void*, cudaStream_t)>(
+            dlsym(x.h, "ncclAllReduce"));
+        x.GroupStart = reinterpret_cast<int (*)()>(dlsym(x.h, "ncclGroupStart"));
+        x.GroupEnd = reinterpret_cast<int (*)()>(dlsym(x.h, "ncclGroupEnd"));
+        x.GetErrorString = reinterpret_cast<const char* (*)(int)>(dlsym(x.h, "ncclGetErrorString"));
+        x.ok = x.GetUniqueId && x.CommInitRank && x.CommDestroy && x.AllReduce && x.GroupStart && x.GroupEnd;
+        return x;
+    }();
+    return n;
+}
+
+int nccl_fail(int r, const char* what) {
+    const Nccl& n = nccl();
+    return fail(BCAD_CU_ERR_NCCL,
+                std::string(what) + ": " + (n.GetErrorString ? n.GetErrorString(r) : "nccl error"));
+}
+
+}  // namespace
+
+size_t bcad_cu_impl::pull_ws_any(const Plan& plan, int dtype) {
+    return dtype == BCAD_CU_F32 ? pull_ws_t<float>(plan) : pull_ws_t<double>(plan);
+}
+
+extern "C" {
+
+int bcad_cu_version(void) { return BCAD_CU_VERSION; }
+
+const char* bcad_cu_last_error(void) { return g_err.c_str(); }
+
+int bcad_cu_kernel_count(void) { return int(registry().all.size()); }
+
+const char* bcad_cu_kernel_name(int index) {
+    const auto& all = registry().all;
+    return index >= 0 && index < int(all.size()) ? all[size_t(index)]->name : nullptr;
+}
+
+int bcad_cu_kernel_lookup(const char* name, int n_in, int m_out, bcad_cu_kernel* out) {
+    if (!name || !out) return fail(BCAD_CU_ERR_CONFIG, "null argument");
+    // kernel.hpp:30-35
+    if (n_in < 1 || n_in > BCAD_CU_MAX_INPUTS)
+        return fail(BCAD_CU_ERR_ARITY_MISMATCH,
+                    "kernel input arity " + std::to_string(n_in) + " outside [1, " + std::to_string(BCAD_CU_MAX_INPUTS) + "]");
+    if (m_out < 1 || m_out > BCAD_CU_MAX_OUTPUTS)
+        return fail(BCAD_CU_ERR_ARITY_MISMATCH, "kernel output arity " + std::to_string(m_out) + " outside [1, " +
+                                                    std::to_string(BCAD_CU_MAX_OUTPUTS) + "]");
+    for (const bcad_cu_kernel_entry* e : registry().all) {
+        if (std::strcmp(e->name, name) != 0) continue;
+        if (e->n_in != n_in || e->m_out != m_out)
+            return fail(BCAD_CU_ERR_ARITY_MISMATCH, std::string("kernel ") + name + " is registered as (" +
+                                                        std::to_string(e->n_in) + " -> " + std::to_string(e->m_out) +
+                                                        "), requested (" + std::to_string(n_in) + " -> " +
+                                                        std::to_string(m_out) + ")");
+        *out = e;
+        return BCAD_CU_OK;
+    }
+    return fail(BCAD_CU_ERR_UNKNOWN_PRIMITIVE, std::string("no device body registered for kernel ") + name);
+}
+
+int bcad_cu_kernel_arity(bcad_cu_kernel k, int* n_in, int* m_out) {
+    if (!k) return fail(BCAD_CU_ERR_UNKNOWN_PRIMITIVE, "null kernel handle");
+    if (n_in) *n_in = k->n_in;
+    if (m_out) *m_out = k->m_out;
+    return BCAD_CU_OK;
+}
+
+int bcad_cu_kernel_may_raise(bcad_cu_kernel k) { return k && k->may_raise ? 1 : 0; }
+
+int bcad_cu_broadcast_shape(int n, const bcad_cu_shape* shapes, bcad_cu_shape* out) {
+    if (n < 1) return fail(BCAD_CU_ERR_SHAPE_MISMATCH, "broadcast_shape of an empty shape list");
+    if (n > BCAD_CU_MAX_INPUTS) return fail(BCAD_CU_ERR_ARITY_MISMATCH, "too many shapes");
+    Plan plan;
+    std::string err;
+    const int rc = make_plan(n, shapes, &plan, &err);
+    if (rc) return fail(rc, err);
+    *out = bcad_cu_shape{};
+    out->rank = plan.out_rank;
+    for (int k = 0; k < plan.out_rank; ++k) out->dims[k] = plan.out_dims[k];
+    return BCAD_CU_OK;
+}
+
+int bcad_cu_forward(bcad_cu_kernel k, int dtype, int n_in, const void* const* in, const bcad_cu_shape* in_shapes,
+                    int m_out, void* const* primal_out, void* const* partials_out, void* stream) {
+    int rc = arity_check(k, n_in, m_out);
+    if (rc) return rc;
+    if ((rc = dtype_check(dtype))) return rc;
+    if (!in || !in_shapes) return fail(BCAD_CU_ERR_CONFIG, "null inputs");
+    for (int j = 0; j < n_in; ++j)
+        if (!in[j]) return fail(BCAD_CU_ERR_CONFIG, "null input pointer " + std::to_string(j));
+    Plan plan;
+    std::string err;
+    if ((rc = make_plan(n_in, in_shapes, &plan, &err))) return fail(rc, err);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    unsigned long long* word = nullptr;
+    const bool check = k->may_raise && partials_out != nullptr;
+    if (check) {
+        if ((rc = error_word(&word))) return rc;
+        CU_TRY(cudaMemsetAsync(word, 0xff, sizeof(*word), s), "cudaMemsetAsync(error word)");
+    }
+    FwdArgs a{dtype, in, primal_out, partials_out, s, word, &plan};
+    if ((rc = k->fwd(a, &err))) return fail(rc, err);
+    if (check) return check_error_word(word, s, plan);
+    return BCAD_CU_OK;
+}
+
+int bcad_cu_pullback_workspace(bcad_cu_kernel k, int dtype, int n_in, const bcad_cu_shape* in_shapes, int m_out,
+                               size_t* bytes) {
+    int rc = arity_check(k, n_in, m_out);
+    if (rc) return rc;
+    if ((rc = dtype_check(dtype))) return rc;
+    Plan plan;
+    std::string err;
+    if ((rc = make_plan(n_in, in_shapes, &plan, &err))) return fail(rc, err);
+    *bytes = pull_ws_any(plan, dtype);
+    return BCAD_CU_OK;
+}
+
+int bcad_cu_pullback(bcad_cu_kernel k, int dtype, int n_in, const bcad_cu_shape* in_shapes, int m_out,
+                     const void* const* out_adj, const void* const* partials, const void* const* in,
+                     void* const* in_adj, const unsigned char* accumulate, void* workspace, size_t workspace_bytes,
+                     void* stream) {
+    int rc = arity_check(k, n_in, m_out);
+    if (rc) return rc;
+    if ((rc = dtype_check(dtype))) return rc;
+    if (!out_adj || !in_adj || !in_shapes) return fail(BCAD_CU_ERR_CONFIG, "null argument array");
+    const bool recompute = partials == nullptr;
+    if (recompute) {
+        if (!in) return fail(BCAD_CU_ERR_CONFIG, "recompute pullback needs the inputs");
+        for (int j = 0; j < n_in; ++j)
+            if (!in[j]) return fail(BCAD_CU_ERR_CONFIG, "null input pointer " + std::to_string(j));
+    } else {
+        for (int i = 0; i < m_out; ++i)
+            for (int j = 0; j < n_in; ++j)
+                if (out_adj[i] && in_adj[j] && !partials[i * n_in + j])
+                    return fail(BCAD_CU_ERR_CONFIG, "null cached partial");
+    }
+    for (int j = 0; j < n_in; ++j)
+        for (int l = 0; l < j; ++l)
+            if (in_adj[j] && in_adj[j] == in_adj[l])
+                return fail(BCAD_CU_ERR_CONFIG, "in_adj pointers must not alias");
+    bool any_w = false, any_adj = false;
+    for (int i = 0; i < m_out; ++i) any_w |= out_adj[i] != nullptr;
+    for (int j = 0; j < n_in; ++j) any_adj |= in_adj[j] != nullptr;
+    if (!any_w || !any_adj) return BCAD_CU_OK;  // tape.hpp:277-281: nothing flows
+    Plan plan;
+    std::string err;
+    if ((rc = make_plan(n_in, in_shapes, &plan, &err))) return fail(rc, err);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    unsigned long long* word = nullptr;
+    const bool check = k->may_raise && recompute;
+    if (check) {
+        if ((rc = error_word(&word))) return rc;
+        CU_TRY(cudaMemsetAsync(word, 0xff, sizeof(*word), s), "cudaMemsetAsync(error word)");
+    }
+    PullArgs a{dtype, out_adj, partials, in, in_adj, accumulate, workspace, workspace_bytes, s, word, &plan};
+    if ((rc = k->pull(a, &err))) return fail(rc, err);
+    if (check) return check_error_word(word, s, plan);
+    return BCAD_CU_OK;
+}
+
+int bcad_cu_scatter_add(int dtype, void* acc, const bcad_cu_shape* acc_shape, const void* contrib,
+                        const bcad_cu_shape* contrib_shape, int zero_first, void* stream) {
+    int rc = dtype_check(dtype);
+    if (rc) return rc;
+    const bcad_cu_shape both[2] = {*acc_shape, *contrib_shape};
+    Plan plan;
+    std::string err;
+    if ((rc = make_plan(2, both, &plan, &err))) return fail(rc, err);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const int64_t acc_vol = plan.arg_vol[0];
+    if (acc_vol == plan.vol && plan.arg_vol[1] == plan.vol) {
+        if (dtype == BCAD_CU_F32)
+            add_same_kernel<float><<<grid_for(acc_vol), 256, 0, s>>>(static_cast<float*>(acc), static_cast<const float*>(contrib), acc_vol, zero_first != 0);
+        else
+            add_same_kernel<double><<<grid_for(acc_vol), 256, 0, s>>>(static_cast<double*>(acc), static_cast<const double*>(contrib), acc_vol, zero_first != 0);
+    } else {
+        ScatterGeom g{};
+        g.rank = plan.out_rank;
+        for (int k = 0; k < kMaxRank; ++k) {
+            g.out_dims[k] = k < plan.out_rank ? plan.out_dims[k] : 1;
+            g.acc_strides[k] = plan.strides[0][k];
+            g.con_strides[k] = plan.strides[1][k];
+        }
+        g.acc_vol = acc_vol;
+        if (dtype == BCAD_CU_F32)
+            scatter_add_kernel<float><<<grid_for(acc_vol), 256, 0, s>>>(static_cast<float*>(acc), static_cast<const float*>(contrib), g, zero_first != 0);
+        else
+            scatter_add_kernel<double><<<grid_for(acc_vol), 256, 0, s>>>(static_cast<double*>(acc), static_cast<const double*>(contrib), g, zero_first != 0);
+    }
+    CU_TRY(cudaGetLastError(), "scatter_add launch");
+    return BCAD_CU_OK;
+}
+
+int bcad_cu_fill(int dtype, void* ptr, int64_t count, double value, void* stream) {
+    int rc = dtype_check(dtype);
+    if (rc) return rc;
+    if (count <= 0) return BCAD_CU_OK;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    if (dtype == BCAD_CU_F32) fill_kernel<float><<<grid_for(count), 256, 0, s>>>(static_cast<float*>(ptr), count, float(value));
+    else fill_kernel<double><<<grid_for(count), 256, 0, s>>>(static_cast<double*>(ptr), count, value);
+    CU_TRY(cudaGetLastError(), "fill launch");
+    return BCAD_CU_OK;
+}
+
+// ------------------------------------------------------- device / memory
+int bcad_cu_device_count(int* count) {
+    CU_TRY(cudaGetDeviceCount(count), "cudaGetDeviceCount");
+    return BCAD_CU_OK;
+}
+int bcad_cu_set_device(int device) {
+    CU_TRY(cudaSetDevice(device), "cudaSetDevice");
+    return BCAD_CU_OK;
+}
+int bcad_cu_get_device(int* device) {
+    CU_TRY(cudaGetDevice(device), "cudaGetDevice");
+    return BCAD_CU_OK;
+}
+
+int bcad_cu_malloc(void** ptr, size_t bytes, void* stream) {
+    static std::once_flag pools_once[kMaxDevices];
+    int dev = 0;
+    CU_TRY(cudaGetDevice(&dev), "cudaGetDevice");
+    if (dev >= 0 && dev < kMaxDevices)
+        std::call_once(pools_once[dev], [dev] {
+            cudaMemPool_t pool;
+            if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+                uint64_t threshold = UINT64_MAX;  // keep freed blocks cached
+                cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &threshold);
+            }
+        });
+    CU_TRY(cudaMallocAsync(ptr, bytes == 0 ? 1 : bytes, static_cast<cudaStream_t>(stream)), "cudaMallocAsync");
+    return BCAD_CU_OK;
+}
+int bcad_cu_free(void* ptr, void* stream) {
+    if (!ptr) return BCAD_CU_OK;
+    CU_TRY(cudaFreeAsync(ptr, static_cast<cudaStream_t>(stream)), "cudaFreeAsync");
+    return BCAD_CU_OK;
+}
+int bcad_cu_host_alloc(void** ptr, size_t bytes) {
+    CU_TRY(cudaMallocHost(ptr, bytes == 0 ? 1 : bytes), "cudaMallocHost");
+    return BCAD_CU_OK;
+}
+int bcad_cu_host_free(void* ptr) {
+    if (!ptr) return BCAD_CU_OK;
+    CU_TRY(cudaFreeHost(ptr), "cudaFreeHost");
+    return BCAD_CU_OK;
+}
+int bcad_cu_memcpy(void* dst, const void* src, size_t bytes, int kind, void* stream) {
+    if (bytes == 0) return BCAD_CU_OK;
+    const cudaMemcpyKind k = kind == 0 ? cudaMemcpyHostToDevice : kind == 1 ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice;
+    CU_TRY(cudaMemcpyAsync(dst, src, bytes, k, static_cast<cudaStream_t>(stream)), "cudaMemcpyAsync");
+    return BCAD_CU_OK;
+}
+int bcad_cu_memset(void* ptr, int value, size_t bytes, void* stream) {
+    if (bytes == 0) return BCAD_CU_OK;
+    CU_TRY(cudaMemsetAsync(ptr, value, bytes, static_cast<cudaStream_t>(stream)), "cudaMemsetAsync");
+    return BCAD_CU_OK;
+}
+int bcad_cu_stream_create(void** stream) {
+    cudaStream_t s;
+    CU_TRY(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking), "cudaStreamCreate");
+    *stream = s;
+    return BCAD_CU_OK;
+}
+int bcad_cu_stream_destroy(void* stream) {
+    if (!stream) return BCAD_CU_OK;
+    CU_TRY(cudaStreamDestroy(static_cast<cudaStream_t>(stream)), "cudaStreamDestroy");
+    return BCAD_CU_OK;
+}
+int bcad_cu_stream_synchronize(void* stream) {
+    CU_TRY(cudaStreamSynchronize(static_cast<cudaStream_t>(stream)), "cudaStreamSynchronize");
+    return BCAD_CU_OK;
+}
+int bcad_cu_device_synchronize(void) {
+    CU_TRY(cudaDeviceSynchronize(), "cudaDeviceSynchronize");
+    return BCAD_CU_OK;
+}
+
+// ------------------------------------------------------------------ NCCL
+int bcad_cu_nccl_unique_id(unsigned char id[128]) {
+    Nccl& n = nccl();
+    if (!n.ok) return fail(BCAD_CU_ERR_NCCL, "libnccl.so.2 not loadable");
+    NcclUniqueId u;
+    const int r = n.GetUniqueId(&u);
+    if (r) return nccl_fail(r, "ncclGetUniqueId");
+    std::memcpy(id, u.internal, 128);
+    return BCAD_CU_OK;
+}
+
+int bcad_cu_comm_init(void** comm, int nranks, const unsigned char id[128], int rank) {
+    Nccl& n = nccl();
+    if (!n.ok) return fail(BCAD_CU_ERR_NCCL, "libnccl.so.2 not loadable");
+    NcclUniqueId u;
+    std::memcpy(u.internal, id, 128);
+    // ncclCommInitRank takes the id by value: call through the by-value type.
+    auto init = reinterpret_cast<int (*)(void**, int, NcclUniqueId, int)>(n.CommInitRank);
+    const int r = init(comm, nranks, u, rank);
+    if (r) return nccl_fail(r, "ncclCommInitRank");
+    return BCAD_CU_OK;
+}
+
+int bcad_cu_comm_destroy(void* comm) {
+    Nccl& n = nccl();
+    if (!n.ok) return fail(BCAD_CU_ERR_NCCL, "libnccl.so.2 not loadable");
+    if (!comm) return BCAD_CU_OK;
+    const int r = n.CommDestroy(comm);
+    if (r) return nccl_fail(r, "ncclCommDestroy");
+    return BCAD_CU_OK;
+}
+
+int bcad_cu_allreduce_adjoints(void* const* bufs, const size_t* counts, int n_bufs, int dtype, void* comm,
+                               void* stream) {
+    int rc = dtype_check(dtype);
+    if (rc) return rc;
+    Nccl& n = nccl();
+    if (!n.ok) return fail(BCAD_CU_ERR_NCCL, "libnccl.so.2 not loadable");
+    const int nccl_type = dtype == BCAD_CU_F32 ? 7 : 8;  // ncclFloat32 / ncclFloat64
+    int r = n.GroupStart();
+    if (r) return nccl_fail(r, "ncclGroupStart");
+    for (int b = 0; b < n_bufs; ++b) {
+        if (!bufs[b] || counts[b] == 0) continue;
+        r = n.AllReduce(bufs[b], bufs[b], counts[b], nccl_type, /*ncclSum*/ 0, comm, static_cast<cudaStream_t>(stream));
+        if (r) {
+            n.GroupEnd();
+            return nccl_fail(r, "ncclAllReduce");
+        }
+    }
+    r = n.GroupEnd();
+    if (r) return nccl_fail(r, "ncclGroupEnd");
+    return BCAD_CU_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,592 @@
+// The hot-path CUDA kernels (sm_100a), templated on a registered body.
+//
+//   fwd2d       K1  fused dual-number forward: one visit per output cell,
+//                   primal + M*N partials (forward.hpp:98-150) or the primal
+//                   only through the real body (broadcast.hpp:102-125).
+//                   128-bit vector loads/stores on FULL/COL arguments,
+//                   stride-0 scalar loads for ROW/SCALAR ones; no expansion.
+//   pull2d      K2  pullback: w (.) D summed over outputs, written elementwise
+//                   for FULL arguments and sum-reduced over broadcast axes
+//                   for ROW (warp shuffles), COL (CTA shared-memory tiles +
+//                   fp64 per-tile partials) and SCALAR arguments; the last
+//                   CTA of a tile row/column (integer ticket) combines the
+//                   partials in fixed order. No floating-point atomics;
+//                   bitwise deterministic run to run. With kRecompute the
+//                   partials are re-derived from the inputs in the same pass
+//                   (RecomputeReverse, mixed.hpp:75-90) instead of read.
+//   fwd_generic / pull_generic   rank-N fallbacks (3+ irreducible axis
+//                   groups, odd widths, misaligned pointers).
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "dual.cuh"
+#include "plan.hpp"
+
+namespace bcad_dev {
+
+using bcad_cu_impl::kCol;
+using bcad_cu_impl::kFull;
+using bcad_cu_impl::kMaxRank;
+using bcad_cu_impl::kRow;
+using bcad_cu_impl::kScalar;
+using bcad_cu_impl::kThreads;
+
+// ----------------------------------------------------------- vector I/O
+template <class T, int V> struct alignas(sizeof(T) * V) Pack { T x[V]; };
+
+template <class T, int V>
+__device__ __forceinline__ Pack<T, V> ld_stream(const T* p) {
+    Pack<T, V> r;
+    if constexpr (V == 4 && sizeof(T) == 4) {
+        const float4 v = __ldcs(reinterpret_cast<const float4*>(p));
+        r.x[0] = v.x; r.x[1] = v.y; r.x[2] = v.z; r.x[3] = v.w;
+    } else if constexpr (V == 2 && sizeof(T) == 8) {
+        const double2 v = __ldcs(reinterpret_cast<const double2*>(p));
+        r.x[0] = v.x; r.x[1] = v.y;
+    } else {
+#pragma unroll
+        for (int v = 0; v < V; ++v) r.x[v] = __ldcs(p + v);
+    }
+    return r;
+}
+
+template <class T, int V>
+__device__ __forceinline__ Pack<T, V> ld_ro(const T* p) {  // read-only, may be re-read (COL args)
+    Pack<T, V> r;
+    if constexpr (V == 4 && sizeof(T) == 4) {
+        const float4 v = __ldg(reinterpret_cast<const float4*>(p));
+        r.x[0] = v.x; r.x[1] = v.y; r.x[2] = v.z; r.x[3] = v.w;
+    } else if constexpr (V == 2 && sizeof(T) == 8) {
+        const double2 v = __ldg(reinterpret_cast<const double2*>(p));
+        r.x[0] = v.x; r.x[1] = v.y;
+    } else {
+#pragma unroll
+        for (int v = 0; v < V; ++v) r.x[v] = __ldg(p + v);
+    }
+    return r;
+}
+
+template <class T, int V>
+__device__ __forceinline__ void st_vec(T* p, const Pack<T, V>& r) {
+    if constexpr (V == 4 && sizeof(T) == 4) {
+        *reinterpret_cast<float4*>(p) = make_float4(r.x[0], r.x[1], r.x[2], r.x[3]);
+    } else if constexpr (V == 2 && sizeof(T) == 8) {
+        *reinterpret_cast<double2*>(p) = make_double2(r.x[0], r.x[1]);
+    } else {
+#pragma unroll
+        for (int v = 0; v < V; ++v) p[v] = r.x[v];
+    }
+}
+
+// Load V consecutive cells of argument `cls` at (r, c0).
+template <class T, int V>
+__device__ __forceinline__ Pack<T, V> ld_arg(const T* base, int cls, int64_t r, int64_t c0, int64_t cols) {
+    Pack<T, V> a;
+    if (cls == kFull) {
+        a = ld_stream<T, V>(base + r * cols + c0);
+    } else if (cls == kCol) {
+        a = ld_ro<T, V>(base + c0);
+    } else {
+        const T s = __ldg(base + (cls == kRow ? r : 0));
+#pragma unroll
+        for (int v = 0; v < V; ++v) a.x[v] = s;
+    }
+    return a;
+}
+
+// Device error word: (status << 56) | flat output index; the lowest failing
+// cell wins (atomicMin), matching the reference's per-cell annotation.
+__device__ __forceinline__ void report_error(unsigned long long* word, int64_t flat) {
+    const uint8_t code = s_err_flag[threadIdx.x];
+    if (code) {
+        atomicMin(word, (static_cast<unsigned long long>(code) << 56) | static_cast<unsigned long long>(flat));
+        s_err_flag[threadIdx.x] = 0;
+    }
+}
+
+// ------------------------------------------------------------- K1 params
+template <int N, int M, class T>
+struct Fwd2DParams {
+    const T* in[N];
+    int cls[N];
+    T* primal[M];
+    T* partials[M * N];
+    int64_t rows, cols, vcols;
+    int txv_shift, ty, rpt;
+    int64_t n_col_tiles, tile_rows;
+    unsigned long long* err;
+};
+
+// K1. kReal: evaluate the real body (primal only). Otherwise the dual body,
+// storing whichever of primal / partials pointers are non-null.
+template <class Body, class T, int V, bool kReal>
+__global__ void __launch_bounds__(kThreads) fwd2d_kernel(const __grid_constant__ Fwd2DParams<Body::kIn, Body::kOut, T> p) {
+    constexpr int N = Body::kIn, M = Body::kOut;
+    if constexpr (Body::kMayRaise && !kReal) s_err_flag[threadIdx.x] = 0;
+    const int tx = threadIdx.x & ((1 << p.txv_shift) - 1);
+    const int ty = threadIdx.x >> p.txv_shift;
+    const int64_t ct = blockIdx.x % p.n_col_tiles;
+    const int64_t rt = blockIdx.x / p.n_col_tiles;
+    const int64_t vc = (ct << p.txv_shift) + tx;
+    if (vc >= p.vcols) return;
+    const int64_t c0 = vc * V;
+    const int64_t r_end = min(p.rows, (rt + 1) * p.tile_rows);
+    for (int64_t r = rt * p.tile_rows + ty; r < r_end; r += p.ty) {
+        Pack<T, V> x[N];
+#pragma unroll
+        for (int j = 0; j < N; ++j) x[j] = ld_arg<T, V>(p.in[j], p.cls[j], r, c0, p.cols);
+        if constexpr (kReal) {
+            Pack<T, V> y[M];
+#pragma unroll
+            for (int v = 0; v < V; ++v) {
+                T xi[N], yo[M];
+#pragma unroll
+                for (int j = 0; j < N; ++j) xi[j] = x[j].x[v];
+                Body::template body<T>(xi, yo);
+#pragma unroll
+                for (int i = 0; i < M; ++i) y[i].x[v] = yo[i];
+            }
+#pragma unroll
+            for (int i = 0; i < M; ++i)
+                if (p.primal[i]) st_vec<T, V>(p.primal[i] + r * p.cols + c0, y[i]);
+        } else {
+            Pack<T, V> y[M];
+            Pack<T, V> d[M * N];
+#pragma unroll
+            for (int v = 0; v < V; ++v) {
+                Dual<T, N> xi[N], yo[M];
+#pragma unroll
+                for (int j = 0; j < N; ++j) {  // seed x_j + e_j (forward.hpp:121-126)
+                    xi[j] = Dual<T, N>(x[j].x[v]);
+                    xi[j].d[j] = T(1);
+                }
+                Body::template body<Dual<T, N>>(xi, yo);
+                if constexpr (Body::kMayRaise) report_error(p.err, r * p.cols + c0 + v);
+#pragma unroll
+                for (int i = 0; i < M; ++i) {
+                    y[i].x[v] = yo[i].v;
+#pragma unroll
+                    for (int j = 0; j < N; ++j) d[i * N + j].x[v] = yo[i].d[j];
+                }
+            }
+#pragma unroll
+            for (int i = 0; i < M; ++i) {
+                if (p.primal[i]) st_vec<T, V>(p.primal[i] + r * p.cols + c0, y[i]);
+#pragma unroll
+                for (int j = 0; j < N; ++j)
+                    if (p.partials[i * N + j]) st_vec<T, V>(p.partials[i * N + j] + r * p.cols + c0, d[i * N + j]);
+            }
+        }
+    }
+}
+
+// ------------------------------------------------------------- K2 params
+template <int N, int M, class T>
+struct Pull2DParams {
+    const T* w[M];        // output adjoints (nullable)
+    const T* D[M * N];    // cached partials (CacheForward)
+    const T* in[N];       // inputs (RecomputeReverse)
+    T* adj[N];            // input adjoint slots (nullable)
+    int cls[N];
+    int slot[N];          // index among active args of the same reduced class
+    int row_j[N], col_j[N], scal_j[N];  // slot -> argument index
+    uint32_t acc_mask;    // bit j: add into the existing slot
+    int64_t rows, cols, vcols;
+    int txv_shift, ty, rpt;
+    int64_t n_col_tiles, n_row_tiles, tile_rows;
+    int n_row_args, n_col_args, n_scalar_args;
+    double* ws_row;       // [n_row_args][n_col_tiles][rows]
+    double* ws_col;       // [n_col_args][n_row_tiles][cols]
+    double* ws_scalar;    // [n_scalar_args][n_ctas]
+    unsigned int* counters;  // [n_row_tiles] [n_col_tiles] [1]
+    unsigned long long* err;
+};
+
+template <class T>
+__device__ __forceinline__ T finish(double s, const T* slot_ptr, bool accumulate) {
+    return accumulate ? T(double(*slot_ptr) + s) : T(s);
+}
+
+// Per-thread contribution of input j over the V cells: term_i = w_i * D_ij
+// rounded to T, exactly the tensor_zip of backprop_diag (mixed.hpp:34-38).
+template <class Body, class T, int V, bool kRecompute>
+__global__ void __launch_bounds__(kThreads) pull2d_kernel(const __grid_constant__ Pull2DParams<Body::kIn, Body::kOut, T> p) {
+    constexpr int N = Body::kIn, M = Body::kOut;
+    extern __shared__ double smem[];
+    double* col_acc = smem;                                        // [n_col_args][kThreads*V]
+    double* scal_acc = smem + size_t(p.n_col_args) * kThreads * V; // [n_scalar_args][kThreads]
+    __shared__ unsigned int s_last;
+    if constexpr (Body::kMayRaise && kRecompute) s_err_flag[threadIdx.x] = 0;
+
+    const int tid = threadIdx.x;
+    const int tx = tid & ((1 << p.txv_shift) - 1);
+    const int ty = tid >> p.txv_shift;
+    const int txv = 1 << p.txv_shift;
+    const int64_t ct = blockIdx.x % p.n_col_tiles;
+    const int64_t rt = blockIdx.x / p.n_col_tiles;
+    const int64_t vc = (ct << p.txv_shift) + tx;
+    const bool active = vc < p.vcols;
+    const int64_t c0 = vc * V;
+
+    for (int a = 0; a < p.n_col_args; ++a)
+#pragma unroll
+        for (int v = 0; v < V; ++v) col_acc[(size_t(a) * kThreads + tid) * V + v] = 0.0;
+    for (int a = 0; a < p.n_scalar_args; ++a) scal_acc[a * kThreads + tid] = 0.0;
+
+    const int64_t r_base = rt * p.tile_rows + ty;
+    // Every lane runs the same rpt iterations (rows past the end are masked),
+    // so the ROW shuffles below always see complete lane groups.
+    for (int k = 0; k < p.rpt; ++k) {
+        const int64_t r = r_base + int64_t(k) * p.ty;
+        const bool live = active && r < p.rows;
+        Pack<T, V> w[M];
+#pragma unroll
+        for (int i = 0; i < M; ++i)
+            if (p.w[i] && live) w[i] = ld_stream<T, V>(p.w[i] + r * p.cols + c0);
+        // D[i][j] for this row's V cells
+        Pack<T, V> D[M * N];
+        if (live) {
+            if constexpr (kRecompute) {
+                Pack<T, V> x[N];
+#pragma unroll
+                for (int j = 0; j < N; ++j) x[j] = ld_arg<T, V>(p.in[j], p.cls[j], r, c0, p.cols);
+#pragma unroll
+                for (int v = 0; v < V; ++v) {
+                    Dual<T, N> xi[N], yo[M];
+#pragma unroll
+                    for (int j = 0; j < N; ++j) {
+                        xi[j] = Dual<T, N>(x[j].x[v]);
+                        xi[j].d[j] = T(1);
+                    }
+                    Body::template body<Dual<T, N>>(xi, yo);
+                    if constexpr (Body::kMayRaise) report_error(p.err, r * p.cols + c0 + v);
+#pragma unroll
+                    for (int i = 0; i < M; ++i)
+#pragma unroll
+                        for (int j = 0; j < N; ++j) D[i * N + j].x[v] = yo[i].d[j];
+                }
+            } else {
+#pragma unroll
+                for (int i = 0; i < M; ++i)
+#pragma unroll
+                    for (int j = 0; j < N; ++j)
+                        if (p.w[i] && p.adj[j]) D[i * N + j] = ld_stream<T, V>(p.D[i * N + j] + r * p.cols + c0);
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < N; ++j) {
+            if (!p.adj[j]) continue;
+            const int cls = p.cls[j];
+            const bool acc = (p.acc_mask >> j) & 1u;
+            if (cls == kFull) {
+                if (!live) continue;
+                T* dst = p.adj[j] + r * p.cols + c0;
+                Pack<T, V> out;
+                if (acc) out = ld_stream<T, V>(dst);
+#pragma unroll
+                for (int v = 0; v < V; ++v) {
+                    T a = acc ? out.x[v] : T(0);
+#pragma unroll
+                    for (int i = 0; i < M; ++i)
+                        if (p.w[i]) a = a + w[i].x[v] * D[i * N + j].x[v];
+                    out.x[v] = a;
+                }
+                st_vec<T, V>(dst, out);
+                continue;
+            }
+            // reduced classes: fp64 sum of the rounded terms
+            double s[V];
+#pragma unroll
+            for (int v = 0; v < V; ++v) {
+                s[v] = 0.0;
+                if (live)
+#pragma unroll
+                    for (int i = 0; i < M; ++i)
+                        if (p.w[i]) s[v] += double(T(w[i].x[v] * D[i * N + j].x[v]));
+            }
+            if (cls == kCol) {
+                double* ca = col_acc + (size_t(p.slot[j]) * kThreads + tid) * V;
+#pragma unroll
+                for (int v = 0; v < V; ++v) ca[v] += s[v];
+            } else if (cls == kScalar) {
+                double t = 0.0;
+#pragma unroll
+                for (int v = 0; v < V; ++v) t += s[v];
+                scal_acc[p.slot[j] * kThreads + tid] += t;
+            } else {  // kRow: reduce the txv lanes of this row
+                double t = 0.0;
+#pragma unroll
+                for (int v = 0; v < V; ++v) t += s[v];
+                for (int off = txv >> 1; off > 0; off >>= 1) t += __shfl_xor_sync(0xffffffffu, t, off, txv);
+                if (tx == 0 && r < p.rows) {
+                    if (p.n_col_tiles == 1) {
+                        p.adj[j][r] = finish<T>(t, p.adj[j] + r, acc);
+                    } else {
+                        p.ws_row[(size_t(p.slot[j]) * p.n_col_tiles + ct) * p.rows + r] = t;
+                    }
+                }
+            }
+        }
+    }
+    if (p.n_col_args == 0 && p.n_scalar_args == 0 && (p.n_row_args == 0 || p.n_col_tiles == 1)) return;
+
+    // ---- CTA-level combination of COL / SCALAR partials (fixed order)
+    __syncthreads();
+    const int ccols = txv * V;  // columns covered by this tile
+    for (int item = tid; item < p.n_col_args * ccols; item += kThreads) {
+        const int a = item / ccols, cc = item % ccols;
+        const int txi = cc / V, v = cc % V;
+        const int64_t c = (ct << p.txv_shift) * V + cc;
+        if (c >= p.cols) continue;
+        double s = 0.0;
+        for (int y = 0; y < p.ty; ++y) s += col_acc[(size_t(a) * kThreads + (y << p.txv_shift) + txi) * V + v];
+        if (p.n_row_tiles == 1) {
+            const int j = p.col_j[a];
+            p.adj[j][c] = finish<T>(s, p.adj[j] + c, (p.acc_mask >> j) & 1u);
+        } else {
+            p.ws_col[(size_t(a) * p.n_row_tiles + rt) * p.cols + c] = s;
+        }
+    }
+    const int64_t n_ctas = p.n_row_tiles * p.n_col_tiles;
+    for (int a = 0; a < p.n_scalar_args; ++a) {
+        // fixed-shape tree over the 256 per-thread sums
+        __syncthreads();
+        for (int stride = kThreads / 2; stride > 0; stride >>= 1) {
+            if (tid < stride) scal_acc[a * kThreads + tid] += scal_acc[a * kThreads + tid + stride];
+            __syncthreads();
+        }
+        if (tid == 0) {
+            const double s = scal_acc[a * kThreads];
+            if (n_ctas == 1) {
+                const int j = p.scal_j[a];
+                p.adj[j][0] = finish<T>(s, p.adj[j], (p.acc_mask >> j) & 1u);
+            } else {
+                p.ws_scalar[size_t(a) * n_ctas + blockIdx.x] = s;
+            }
+        }
+    }
+
+    // ---- cross-CTA completion: the last CTA of a tile row / column / grid
+    // combines the fp64 partials in tile order.
+    __threadfence();
+    __syncthreads();
+    // rows of this row tile (partials from every column tile)
+    if (p.n_row_args > 0 && p.n_col_tiles > 1) {
+        if (tid == 0) s_last = atomicAdd(&p.counters[rt], 1u) == unsigned(p.n_col_tiles - 1);
+        __syncthreads();
+        if (s_last) {
+            __threadfence();
+            const int64_t r0 = rt * p.tile_rows;
+            const int64_t nr = min(p.tile_rows, p.rows - r0);
+            for (int64_t item = tid; item < p.n_row_args * nr; item += kThreads) {
+                const int a = int(item / nr);
+                const int64_t r = r0 + item % nr;
+                double s = 0.0;
+                for (int64_t k = 0; k < p.n_col_tiles; ++k) s += __ldcg(&p.ws_row[(size_t(a) * p.n_col_tiles + k) * p.rows + r]);
+                const int j = p.row_j[a];
+                p.adj[j][r] = finish<T>(s, p.adj[j] + r, (p.acc_mask >> j) & 1u);
+            }
+            if (tid == 0) p.counters[rt] = 0;
+        }
+        __syncthreads();
+    }
+    if (p.n_col_args > 0 && p.n_row_tiles > 1) {
+        if (tid == 0) s_last = atomicAdd(&p.counters[p.n_row_tiles + ct], 1u) == unsigned(p.n_row_tiles - 1);
+        __syncthreads();
+        if (s_last) {
+            __threadfence();
+            for (int item = tid; item < p.n_col_args * ccols; item += kThreads) {
+                const int a = item / ccols;
+                const int64_t c = (ct << p.txv_shift) * V + item % ccols;
+                if (c >= p.cols) continue;
+                double s = 0.0;
+                for (int64_t k = 0; k < p.n_row_tiles; ++k) s += __ldcg(&p.ws_col[(size_t(a) * p.n_row_tiles + k) * p.cols + c]);
+                const int j = p.col_j[a];
+                p.adj[j][c] = finish<T>(s, p.adj[j] + c, (p.acc_mask >> j) & 1u);
+            }
+            if (tid == 0) p.counters[p.n_row_tiles + ct] = 0;
+        }
+        __syncthreads();
+    }
+    if (p.n_scalar_args > 0 && n_ctas > 1) {
+        unsigned int* cnt = &p.counters[p.n_row_tiles + p.n_col_tiles];
+        if (tid == 0) s_last = atomicAdd(cnt, 1u) == unsigned(n_ctas - 1);
+        __syncthreads();
+        if (s_last) {
+            __threadfence();
+            for (int a = 0; a < p.n_scalar_args; ++a) {
+                double s = 0.0;
+                for (int64_t k = tid; k < n_ctas; k += kThreads) s += __ldcg(&p.ws_scalar[size_t(a) * n_ctas + k]);
+                scal_acc[a * kThreads + tid] = s;
+                __syncthreads();
+                for (int stride = kThreads / 2; stride > 0; stride >>= 1) {
+                    if (tid < stride) scal_acc[a * kThreads + tid] += scal_acc[a * kThreads + tid + stride];
+                    __syncthreads();
+                }
+                if (tid == 0) {
+                    const int j = p.scal_j[a];
+                    p.adj[j][0] = finish<T>(scal_acc[a * kThreads], p.adj[j], (p.acc_mask >> j) & 1u);
+                }
+                __syncthreads();
+            }
+            if (tid == 0) *cnt = 0;
+        }
+    }
+}
+
+// ------------------------------------------------------- generic kernels
+template <int N, int M, class T>
+struct GenParams {
+    const T* in[N];
+    int64_t strides[N][kMaxRank];
+    int64_t arg_vol[N];
+    int out_rank;
+    int64_t out_dims[kMaxRank];
+    int64_t vol;
+    T* primal[M];
+    T* partials[M * N];
+    // pullback
+    const T* w[M];
+    const T* D[M * N];
+    T* adj[N];
+    uint32_t acc_mask;
+    int64_t adj_offset[N + 1];  // prefix sums of arg volumes over active adj
+    unsigned long long* err;
+};
+
+template <int N, int M, class T>
+__device__ __forceinline__ void decode_offsets(const GenParams<N, M, T>& p, int64_t flat, int64_t* off) {
+#pragma unroll
+    for (int j = 0; j < N; ++j) off[j] = 0;
+    for (int k = p.out_rank - 1; k >= 0; --k) {
+        const int64_t len = p.out_dims[k];
+        const int64_t c = flat % len;
+        flat /= len;
+#pragma unroll
+        for (int j = 0; j < N; ++j) off[j] += c * p.strides[j][k];
+    }
+}
+
+template <class Body, class T, bool kReal>
+__global__ void __launch_bounds__(kThreads) fwd_generic_kernel(const __grid_constant__ GenParams<Body::kIn, Body::kOut, T> p) {
+    constexpr int N = Body::kIn, M = Body::kOut;
+    if constexpr (Body::kMayRaise && !kReal) s_err_flag[threadIdx.x] = 0;
+    for (int64_t cell = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; cell < p.vol;
+         cell += int64_t(gridDim.x) * blockDim.x) {
+        int64_t off[N];
+        decode_offsets<N, M, T>(p, cell, off);
+        if constexpr (kReal) {
+            T xi[N], yo[M];
+#pragma unroll
+            for (int j = 0; j < N; ++j) xi[j] = p.in[j][off[j]];
+            Body::template body<T>(xi, yo);
+#pragma unroll
+            for (int i = 0; i < M; ++i)
+                if (p.primal[i]) p.primal[i][cell] = yo[i];
+        } else {
+            Dual<T, N> xi[N], yo[M];
+#pragma unroll
+            for (int j = 0; j < N; ++j) {
+                xi[j] = Dual<T, N>(p.in[j][off[j]]);
+                xi[j].d[j] = T(1);
+            }
+            Body::template body<Dual<T, N>>(xi, yo);
+            if constexpr (Body::kMayRaise) report_error(p.err, cell);
+#pragma unroll
+            for (int i = 0; i < M; ++i) {
+                if (p.primal[i]) p.primal[i][cell] = yo[i].v;
+#pragma unroll
+                for (int j = 0; j < N; ++j)
+                    if (p.partials[i * N + j]) p.partials[i * N + j][cell] = yo[i].d[j];
+            }
+        }
+    }
+}
+
+// One thread per element e of each input j: walks the output cells that map
+// onto e (the broadcast axes of j, row-major) and sums the terms.
+template <class Body, class T, bool kRecompute>
+__global__ void __launch_bounds__(kThreads) pull_generic_kernel(const __grid_constant__ GenParams<Body::kIn, Body::kOut, T> p) {
+    constexpr int N = Body::kIn, M = Body::kOut;
+    if constexpr (Body::kMayRaise && kRecompute) s_err_flag[threadIdx.x] = 0;
+    const int64_t total = p.adj_offset[N];
+    for (int64_t g = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; g < total;
+         g += int64_t(gridDim.x) * blockDim.x) {
+        int j = 0;
+        while (j + 1 < N && g >= p.adj_offset[j + 1]) ++j;
+        const int64_t e = g - p.adj_offset[j];
+        // arg coordinates of e on the output axes; broadcast axes enumerate
+        int64_t base[kMaxRank], cnt = 1;
+        int nb = 0;
+        int bax[kMaxRank];
+        {
+            int64_t rem = e;
+            for (int k = p.out_rank - 1; k >= 0; --k) {
+                if (p.strides[j][k] != 0) {
+                    const int64_t len = p.out_dims[k];
+                    base[k] = rem % len;
+                    rem /= len;
+                } else {
+                    base[k] = 0;
+                }
+            }
+            for (int k = 0; k < p.out_rank; ++k)
+                if (p.strides[j][k] == 0 && p.out_dims[k] > 1) {
+                    bax[nb++] = k;
+                    cnt *= p.out_dims[k];
+                }
+        }
+        const bool acc = (p.acc_mask >> j) & 1u;
+        T exact = acc ? p.adj[j][e] : T(0);
+        double sum = 0.0;
+        int64_t coord[kMaxRank];
+        for (int k = 0; k < p.out_rank; ++k) coord[k] = base[k];
+        for (int64_t q = 0; q < cnt; ++q) {
+            int64_t flat = 0;
+            for (int k = 0; k < p.out_rank; ++k) flat = flat * p.out_dims[k] + coord[k];
+            T dj[M];
+            if constexpr (kRecompute) {
+                int64_t off[N];
+                decode_offsets<N, M, T>(p, flat, off);
+                Dual<T, N> xi[N], yo[M];
+#pragma unroll
+                for (int jj = 0; jj < N; ++jj) {
+                    xi[jj] = Dual<T, N>(p.in[jj][off[jj]]);
+                    xi[jj].d[jj] = T(1);
+                }
+                Body::template body<Dual<T, N>>(xi, yo);
+                if constexpr (Body::kMayRaise) report_error(p.err, flat);
+#pragma unroll
+                for (int i = 0; i < M; ++i) {
+                    T v = T(0);
+#pragma unroll
+                    for (int jj = 0; jj < N; ++jj)
+                        if (jj == j) v = yo[i].d[jj];
+                    dj[i] = v;
+                }
+            } else {
+#pragma unroll
+                for (int i = 0; i < M; ++i) dj[i] = p.w[i] ? p.D[i * N + j][flat] : T(0);
+            }
+#pragma unroll
+            for (int i = 0; i < M; ++i) {
+                if (!p.w[i]) continue;
+                const T term = p.w[i][flat] * dj[i];
+                if (cnt == 1) exact = exact + term;
+                else sum += double(term);
+            }
+            // odometer over the broadcast axes, last axis fastest
+            for (int b = nb - 1; b >= 0; --b) {
+                const int k = bax[b];
+                if (++coord[k] < p.out_dims[k]) break;
+                coord[k] = 0;
+            }
+        }
+        if (cnt == 1) p.adj[j][e] = exact;
+        else p.adj[j][e] = acc ? T(double(p.adj[j][e]) + sum) : T(sum);
+    }
+}
+
+}  // namespace bcad_dev

@@ -1,0 +1,200 @@
+// Host launchers: pick the 2-D vectorised kernels or the generic rank-N
+// fallback for one registered body, fill the by-value parameter block and
+// launch on the caller's stream. Included once per registration TU.
+#pragma once
+
+#include <cstdint>
+#include <string>
+
+#include "kernels.cuh"
+#include "registry.hpp"
+
+namespace bcad_cu_impl {
+
+inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+inline int cuda_status(cudaError_t e, std::string* err) {
+    if (e == cudaSuccess) return BCAD_CU_OK;
+    *err = std::string("CUDA error: ") + cudaGetErrorString(e);
+    return BCAD_CU_ERR_CUDA;
+}
+
+inline int generic_grid(int64_t work) {
+    const int64_t blocks = ceil_div(work, kThreads);
+    const int64_t cap = int64_t(kSmCount) * 16;
+    return int(blocks < 1 ? 1 : (blocks > cap ? cap : blocks));
+}
+
+template <int N, int M, class T>
+void fill_generic(bcad_dev::GenParams<N, M, T>& g, const Plan& plan) {
+    g.out_rank = plan.out_rank;
+    for (int k = 0; k < kMaxRank; ++k) g.out_dims[k] = k < plan.out_rank ? plan.out_dims[k] : 1;
+    g.vol = plan.vol;
+    for (int j = 0; j < N; ++j) {
+        for (int k = 0; k < kMaxRank; ++k) g.strides[j][k] = plan.strides[j][k];
+        g.arg_vol[j] = plan.arg_vol[j];
+    }
+}
+
+// ---------------------------------------------------------------- forward
+template <class Body, class T>
+int launch_fwd_t(const FwdArgs& a, std::string* err) {
+    constexpr int N = Body::kIn, M = Body::kOut, V = vec_width<T>();
+    const Plan& plan = *a.plan;
+    const bool real = a.partials == nullptr;
+    bool vec = plan.is2d && plan.cols % V == 0;
+    for (int j = 0; j < N && vec; ++j)
+        if ((plan.cls[j] == kFull || plan.cls[j] == kCol) && !aligned16(a.in[j])) vec = false;
+    for (int i = 0; i < M && vec; ++i) {
+        if (a.primal && a.primal[i] && !aligned16(a.primal[i])) vec = false;
+        for (int j = 0; j < N && a.partials && vec; ++j)
+            if (a.partials[i * N + j] && !aligned16(a.partials[i * N + j])) vec = false;
+    }
+    if (vec) {
+        const Tiling t = choose_tiling(plan, V, false);
+        bcad_dev::Fwd2DParams<N, M, T> p{};
+        for (int j = 0; j < N; ++j) {
+            p.in[j] = static_cast<const T*>(a.in[j]);
+            p.cls[j] = plan.cls[j];
+        }
+        for (int i = 0; i < M; ++i) {
+            p.primal[i] = a.primal ? static_cast<T*>(a.primal[i]) : nullptr;
+            for (int j = 0; j < N; ++j) p.partials[i * N + j] = a.partials ? static_cast<T*>(a.partials[i * N + j]) : nullptr;
+        }
+        p.rows = plan.rows;
+        p.cols = plan.cols;
+        p.vcols = t.vcols;
+        p.txv_shift = __builtin_ctz(unsigned(t.txv));
+        p.ty = t.ty;
+        p.rpt = t.rpt;
+        p.n_col_tiles = t.n_col_tiles;
+        p.tile_rows = t.tile_rows;
+        p.err = a.err;
+        if (real) bcad_dev::fwd2d_kernel<Body, T, V, true><<<unsigned(t.n_ctas), kThreads, 0, a.stream>>>(p);
+        else bcad_dev::fwd2d_kernel<Body, T, V, false><<<unsigned(t.n_ctas), kThreads, 0, a.stream>>>(p);
+        return cuda_status(cudaGetLastError(), err);
+    }
+    bcad_dev::GenParams<N, M, T> g{};
+    fill_generic(g, plan);
+    for (int j = 0; j < N; ++j) g.in[j] = static_cast<const T*>(a.in[j]);
+    for (int i = 0; i < M; ++i) {
+        g.primal[i] = a.primal ? static_cast<T*>(a.primal[i]) : nullptr;
+        for (int j = 0; j < N; ++j) g.partials[i * N + j] = a.partials ? static_cast<T*>(a.partials[i * N + j]) : nullptr;
+    }
+    g.err = a.err;
+    const int grid = generic_grid(plan.vol);
+    if (real) bcad_dev::fwd_generic_kernel<Body, T, true><<<grid, kThreads, 0, a.stream>>>(g);
+    else bcad_dev::fwd_generic_kernel<Body, T, false><<<grid, kThreads, 0, a.stream>>>(g);
+    return cuda_status(cudaGetLastError(), err);
+}
+
+// --------------------------------------------------------------- pullback
+template <class Body, class T>
+int launch_pull_t(const PullArgs& a, std::string* err) {
+    constexpr int N = Body::kIn, M = Body::kOut, V = vec_width<T>();
+    const Plan& plan = *a.plan;
+    const bool recompute = a.partials == nullptr;
+    bool vec = pull_vec_shape_ok<T>(plan);
+    for (int i = 0; i < M && vec; ++i)
+        if (a.out_adj[i] && !aligned16(a.out_adj[i])) vec = false;
+    for (int j = 0; j < N && vec; ++j) {
+        if (!a.in_adj[j]) continue;
+        if (plan.cls[j] == kFull && !aligned16(a.in_adj[j])) vec = false;
+        for (int i = 0; i < M && !recompute && vec; ++i)
+            if (a.out_adj[i] && !aligned16(a.partials[i * N + j])) vec = false;
+    }
+    for (int j = 0; j < N && recompute && vec; ++j)
+        if ((plan.cls[j] == kFull || plan.cls[j] == kCol) && !aligned16(a.in[j])) vec = false;
+
+    if (vec) {
+        bool has_col = false;
+        for (int j = 0; j < N; ++j) has_col |= plan.cls[j] == kCol;
+        const Tiling t = choose_tiling(plan, V, has_col);
+        const PullLayout L = pull_layout(plan, t);  // offsets sized for every argument
+        if (a.ws_bytes < L.total || (L.total > 0 && !a.workspace)) {
+            *err = "pullback workspace too small: need " + std::to_string(L.total) + " bytes";
+            return BCAD_CU_ERR_CONFIG;
+        }
+        bcad_dev::Pull2DParams<N, M, T> p{};
+        int nr = 0, nc = 0, ns = 0;
+        for (int j = 0; j < N; ++j) {
+            p.in[j] = a.in ? static_cast<const T*>(a.in[j]) : nullptr;
+            p.adj[j] = static_cast<T*>(a.in_adj[j]);
+            p.cls[j] = plan.cls[j];
+            p.slot[j] = -1;
+            if (a.accumulate && a.accumulate[j]) p.acc_mask |= 1u << j;
+            if (!p.adj[j]) continue;
+            if (plan.cls[j] == kRow) { p.row_j[nr] = j; p.slot[j] = nr++; }
+            if (plan.cls[j] == kCol) { p.col_j[nc] = j; p.slot[j] = nc++; }
+            if (plan.cls[j] == kScalar) { p.scal_j[ns] = j; p.slot[j] = ns++; }
+        }
+        for (int i = 0; i < M; ++i) {
+            p.w[i] = static_cast<const T*>(a.out_adj[i]);
+            for (int j = 0; j < N; ++j) p.D[i * N + j] = recompute ? nullptr : static_cast<const T*>(a.partials[i * N + j]);
+        }
+        p.rows = plan.rows;
+        p.cols = plan.cols;
+        p.vcols = t.vcols;
+        p.txv_shift = __builtin_ctz(unsigned(t.txv));
+        p.ty = t.ty;
+        p.rpt = t.rpt;
+        p.n_col_tiles = t.n_col_tiles;
+        p.n_row_tiles = t.n_row_tiles;
+        p.tile_rows = t.tile_rows;
+        p.n_row_args = nr;
+        p.n_col_args = nc;
+        p.n_scalar_args = ns;
+        char* ws = static_cast<char*>(a.workspace);
+        p.ws_row = reinterpret_cast<double*>(ws + L.ws_row);
+        p.ws_col = reinterpret_cast<double*>(ws + L.ws_col);
+        p.ws_scalar = reinterpret_cast<double*>(ws + L.ws_scalar);
+        p.counters = reinterpret_cast<unsigned int*>(ws + L.counters);
+        p.err = a.err;
+        const size_t smem = size_t(nc) * kThreads * V * 8 + size_t(ns) * kThreads * 8;
+        auto kern = recompute ? &bcad_dev::pull2d_kernel<Body, T, V, true> : &bcad_dev::pull2d_kernel<Body, T, V, false>;
+        if (smem > 48 * 1024) {
+            const cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+            if (e != cudaSuccess) return cuda_status(e, err);
+        }
+        kern<<<unsigned(t.n_ctas), kThreads, smem, a.stream>>>(p);
+        return cuda_status(cudaGetLastError(), err);
+    }
+    bcad_dev::GenParams<N, M, T> g{};
+    fill_generic(g, plan);
+    int64_t off = 0;
+    for (int j = 0; j < N; ++j) {
+        g.in[j] = a.in ? static_cast<const T*>(a.in[j]) : nullptr;
+        g.adj[j] = static_cast<T*>(a.in_adj[j]);
+        if (a.accumulate && a.accumulate[j]) g.acc_mask |= 1u << j;
+        g.adj_offset[j] = off;
+        if (g.adj[j]) off += plan.arg_vol[j];
+    }
+    g.adj_offset[N] = off;
+    for (int i = 0; i < M; ++i) {
+        g.w[i] = static_cast<const T*>(a.out_adj[i]);
+        for (int j = 0; j < N; ++j) g.D[i * N + j] = recompute ? nullptr : static_cast<const T*>(a.partials[i * N + j]);
+    }
+    g.err = a.err;
+    if (off == 0) return BCAD_CU_OK;
+    const int grid = generic_grid(off);
+    if (recompute) bcad_dev::pull_generic_kernel<Body, T, true><<<grid, kThreads, 0, a.stream>>>(g);
+    else bcad_dev::pull_generic_kernel<Body, T, false><<<grid, kThreads, 0, a.stream>>>(g);
+    return cuda_status(cudaGetLastError(), err);
+}
+
+template <class Body>
+int launch_fwd_any(const FwdArgs& a, std::string* err) {
+    return a.dtype == BCAD_CU_F32 ? launch_fwd_t<Body, float>(a, err) : launch_fwd_t<Body, double>(a, err);
+}
+template <class Body>
+int launch_pull_any(const PullArgs& a, std::string* err) {
+    return a.dtype == BCAD_CU_F32 ? launch_pull_t<Body, float>(a, err) : launch_pull_t<Body, double>(a, err);
+}
+
+}  // namespace bcad_cu_impl
+
+#define BCAD_ENTRY(Body)                                                                               \
+    bcad_cu_kernel_entry {                                                                             \
+        Body::kName, Body::kIn, Body::kOut, Body::kMayRaise, &bcad_cu_impl::launch_fwd_any<Body>,       \
+            &bcad_cu_impl::launch_pull_any<Body>                                                       \
+    }
