@@ -1,0 +1,39 @@
+/*
+ * bcad_host.h — C-ABI of the end-to-end host call (libbcad_host.so), built on
+ * the C++ drop-in API (include/bcad/*.hpp). One call is one reference step as
+ * proj/src/bench.cpp:112-128 (run_cell_once) performs it — tape inputs from
+ * HOST buffers, mixed_broadcast(kernel, ..., policy), backward(seeds), leaf
+ * gradients back to HOST buffers — with every device step on `stream`.
+ * This is the binding a non-C++ caller of the reference's
+ * mixed_broadcast + Tape::backward (proj/include/bcad/mixed.hpp:49-99,
+ * tape.hpp:185-211) would use.
+ */
+#ifndef BCAD_HOST_H
+#define BCAD_HOST_H
+
+#include <stdint.h>
+
+#include "bcad_cu.h"
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* policy: 0 CacheForward, 1 RecomputeReverse (mixed.hpp:17-20).
+ * host_seeds: m_out pointers at the output shape (entries may be NULL = no
+ * adjoint for that output). host_grads: n_in pointers at the input shapes
+ * (entries may be NULL = not wanted). Pinned host memory makes the copies
+ * asynchronous. Returns a bcad_cu_status; the message is in
+ * bcad_host_last_error(). */
+int bcad_host_mixed_step(const char* kernel, int dtype, int n_in, const void* const* host_in,
+                         const bcad_cu_shape* in_shapes, int m_out, int policy, const void* const* host_seeds,
+                         void* const* host_primal, void* const* host_grads, int64_t* peak_cached_bytes,
+                         void* stream);
+
+const char* bcad_host_last_error(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* BCAD_HOST_H */

@@ -92,11 +92,12 @@ def build_cpp_tests(verbose: bool = False) -> list[str]:
     out = []
     tdir = os.path.join(ROOT, "tests", "cpp")
     for src in sorted(glob.glob(os.path.join(tdir, "test_*.cpp"))):
-        exe = os.path.join(BUILD, os.path.splitext(os.path.basename(src))[0])
+        os.makedirs(os.path.join(tdir, "bin"), exist_ok=True)
+        exe = os.path.join(tdir, "bin", os.path.splitext(os.path.basename(src))[0])
         deps = [src] + glob.glob(os.path.join(tdir, "*.hpp")) + glob.glob(os.path.join(INCLUDE, "bcad", "*.hpp")) + [LIB]
         if _newer(exe, deps):
             _run([cxx(), "-std=c++20", "-O2", "-Wall", "-Wextra", "-I" + INCLUDE, "-I" + tdir, src, "-o", exe,
-                  "-L" + PKG, "-lbcad_cu", "-Wl,-rpath," + PKG], verbose)
+                  "-L" + PKG, "-lbcad_cu", "-Wl,-rpath,$ORIGIN/../../../paper_1810_08297_b200"], verbose)
         out.append(exe)
     return out
 

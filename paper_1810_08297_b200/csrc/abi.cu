@@ -38,7 +38,7 @@ int cuda_fail(cudaError_t e, const char* what) {
 struct Registry {
     std::vector<const bcad_cu_kernel_entry*> all;
     Registry() {
-        int (*groups[])(const bcad_cu_kernel_entry**) = {&bcad_reg_hmlstm, &bcad_reg_pool, &bcad_reg_probe,
+        int (*groups[])(const bcad_cu_kernel_entry**) = {&bcad_reg_hmlstm, &bcad_reg_pool, &bcad_reg_probe, &bcad_reg_prims,
                                                          &bcad_reg_arity};
         for (auto g : groups) {
             const bcad_cu_kernel_entry* e = nullptr;

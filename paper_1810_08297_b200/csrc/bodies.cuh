@@ -82,8 +82,8 @@ BCAD_BODY(KNeg, "neg", 1, 1, false, out[0] = -in[0])
 BCAD_BODY(KSigmoid, "sigmoid", 1, 1, false, out[0] = sigmoid(in[0]))
 BCAD_BODY(KTanh, "tanh", 1, 1, false, out[0] = tanh(in[0]))
 BCAD_BODY(KSelect, "select", 3, 1, false, out[0] = in[0] != 0.0 ? in[1] : in[2])
-BCAD_BODY(KSigmoidBwd, "sigmoid_bwd", 2, 1, false, out[0] = in[0] * in[1] * (1.0 - in[1]))
-BCAD_BODY(KTanhBwd, "tanh_bwd", 2, 1, false, out[0] = in[0] * (1.0 - in[1] * in[1]))
+BCAD_BODY(KSigmoidBwd, "sigmoid_bwd", 2, 1, false, out[0] = in[0] * in[1] * (S(1.0) - in[1]))
+BCAD_BODY(KTanhBwd, "tanh_bwd", 2, 1, false, out[0] = in[0] * (S(1.0) - in[1] * in[1]))
 BCAD_BODY(KSelectTrueBwd, "select_true_bwd", 2, 1, false, out[0] = in[1] != 0.0 ? in[0] : S(0.0))
 BCAD_BODY(KSelectFalseBwd, "select_false_bwd", 2, 1, false, out[0] = in[1] != 0.0 ? S(0.0) : in[0])
 #undef BCAD_BODY

@@ -53,3 +53,4 @@ int bcad_reg_hmlstm(const bcad_cu_kernel_entry** out);
 int bcad_reg_pool(const bcad_cu_kernel_entry** out);
 int bcad_reg_probe(const bcad_cu_kernel_entry** out);
 int bcad_reg_arity(const bcad_cu_kernel_entry** out);
+int bcad_reg_prims(const bcad_cu_kernel_entry** out);

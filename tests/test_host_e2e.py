@@ -1,0 +1,69 @@
+"""End-to-end host call (include/bcad_host.h -> C++ Tape + mixed_broadcast ->
+libbcad_cu.so): host buffers in, host gradients out, against the oracle."""
+import ctypes as C
+import os
+
+import numpy as np
+import pytest
+
+import oracle as O
+from helpers import assert_close, assert_grads, tol_for
+
+pytestmark = pytest.mark.gpu
+
+PKG = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "paper_1810_08297_b200")
+
+
+@pytest.fixture(scope="module")
+def host():
+    from paper_1810_08297_b200 import native  # noqa: F401 (loads libbcad_cu.so first)
+    lib = C.CDLL(os.path.join(PKG, "libbcad_host.so"))
+    lib.bcad_host_last_error.restype = C.c_char_p
+    return lib
+
+
+def host_step(lib, name, ins, seeds, policy):
+    from paper_1810_08297_b200 import native
+    n = len(ins)
+    out_shape = O.broadcast_shape_py([a.shape for a in ins])
+    m = len(seeds)
+    prim = [np.empty(out_shape, ins[0].dtype) for _ in range(m)]
+    grads = [np.empty(a.shape, a.dtype) for a in ins]
+    ptr = lambda arrs: (C.c_void_p * len(arrs))(*[None if a is None else a.ctypes.data for a in arrs])  # noqa: E731
+    shapes = (native.Shape * n)(*[native.Shape.of(a.shape) for a in ins])
+    peak = C.c_int64()
+    rc = lib.bcad_host_mixed_step(name.encode(), 0 if ins[0].dtype == np.float32 else 1, n, ptr(ins), shapes, m,
+                                  policy, ptr(seeds), ptr(prim), ptr(grads), C.byref(peak), None)
+    if rc:
+        raise native._BY_CODE.get(rc, native.Error)(lib.bcad_host_last_error().decode())
+    return prim, grads, peak.value
+
+
+@pytest.mark.parametrize("dtype", [np.float32, np.float64])
+@pytest.mark.parametrize("variant", ["canonical", "bias"])
+@pytest.mark.parametrize("policy", [0, 1])
+def test_host_step_matches_oracle(host, oracle_lib, dtype, variant, policy):
+    B, H = 32, 256
+    ins = O.hmlstm_inputs(oracle_lib, B, H, dtype, variant)
+    name = O.hmlstm_kernel(variant)
+    seeds = [np.random.default_rng(1).uniform(-1, 1, (B, H)).astype(dtype)]
+    want_p, want_g, want_a64 = oracle_lib.mixed_step(name, ins, policy, seeds)
+    got_p, got_g, peak = host_step(host, name, ins, seeds, policy)
+    rtol, atol = tol_for(dtype)
+    assert_close(got_p[0], want_p[0], rtol, atol, "host primal")
+    assert_grads(got_g, want_g, want_a64, [a.shape for a in ins], (B, H), dtype, "host e2e")
+    s = np.dtype(dtype).itemsize
+    E, n = B * H, len(ins)
+    inputs_bytes = sum(a.size for a in ins) * s
+    assert peak == inputs_bytes + E * s + (n * E * s if policy == 0 else 0)  # tape.hpp:236-243
+
+
+def test_host_step_maps_errors(host):
+    from paper_1810_08297_b200 import native
+    with pytest.raises(native.DomainError) as e:
+        host_step(host, "log", [np.array([[1.0, -2.0]])], [np.ones((1, 2))], 0)
+    assert "at output index (0, 1)" in str(e.value)
+    with pytest.raises(native.ShapeMismatch):
+        host_step(host, "mul", [np.ones((2, 3)), np.ones((4, 3))], [np.ones((2, 3))], 0)
+    with pytest.raises(native.UnknownPrimitive):
+        host_step(host, "nope", [np.ones(2)], [np.ones(2)], 0)

@@ -1,0 +1,191 @@
+"""The oracle is pinned before it is trusted (CPU, no GPU needed).
+
+1. Against the committed golden vectors produced by the unmodified reference
+   (tests/golden/make_golden.py): bit-exact, since both are built with the
+   reference's numerics (-ffp-contract=off) against the same libm.
+2. Against the reference build itself (oracle/_ref) on fresh random cases,
+   when it is present.
+3. Against the known-answer tests of the reference suite (exact scalars,
+   closed forms, structural zeros).
+"""
+import glob
+import os
+
+import numpy as np
+import pytest
+
+import oracle as O
+from helpers import assert_close
+
+GOLDEN = sorted(glob.glob(os.path.join(os.path.dirname(__file__), "golden", "*.npz")))
+
+
+def load(path):
+    z = np.load(path)
+    n, m = int(z["n_in"]), int(z["m_out"])
+    ins = [z[f"in{j}"] for j in range(n)]
+    seeds = [z[f"seed{i}"] if f"seed{i}" in z else None for i in range(m)]
+    return str(z["kernel"]), ins, seeds, z
+
+
+def bits_equal(a, b):
+    a, b = np.asarray(a), np.asarray(b)
+    return a.shape == b.shape and a.dtype == b.dtype and a.tobytes() == b.tobytes()
+
+
+def test_golden_fixtures_present():
+    assert len(GOLDEN) >= 30
+
+
+@pytest.mark.parametrize("path", GOLDEN, ids=[os.path.basename(p)[:-4] for p in GOLDEN])
+def test_oracle_matches_golden_bitexact(oracle_lib, path):
+    kernel, ins, seeds, z = load(path)
+    n, m = len(ins), int(z["m_out"])
+    prim, parts = oracle_lib.forward(kernel, ins)
+    for i in range(m):
+        assert bits_equal(prim[i], z[f"primal{i}"]), f"primal{i}"
+    for k in range(m * n):
+        assert bits_equal(parts[k], z[f"partial{k}"]), f"partial{k}"
+    _, grads, _ = oracle_lib.mixed_step(kernel, ins, O.CACHE_FORWARD, seeds)
+    for j in range(n):
+        assert bits_equal(grads[j], z[f"grad{j}"]), f"grad{j}"
+
+
+def test_oracle_rng_matches_reference_inputs(oracle_lib, ref_lib):
+    for dt in (np.float32, np.float64):
+        for variant in ("canonical", "bias", "divergence"):
+            a = O.hmlstm_inputs(oracle_lib, 32, 64, dt, variant)
+            b = O.hmlstm_inputs(ref_lib, 32, 64, dt, variant)
+            assert all(bits_equal(x, y) for x, y in zip(a, b))
+
+
+def test_oracle_matches_reference_random_cases(oracle_lib, ref_lib):
+    rng = np.random.default_rng(99)
+    names = [n for n in oracle_lib.kernel_names() if n not in ("log", "div", "sqrt", "abs", "pow_half", "recip")]
+    for name in names:
+        n, m = oracle_lib.arity(name)
+        for rep in range(2):
+            rank = int(rng.integers(1, 4))
+            out = [int(rng.integers(1, 5)) for _ in range(rank)]
+            shapes = [tuple(1 if rng.integers(0, 3) == 0 else out[k] for k in range(rank)) for _ in range(n)]
+            dt = np.float32 if rep else np.float64
+            ins = [rng.uniform(-1, 1, s).astype(dt) for s in shapes]
+            if name.startswith("hmlstm"):
+                for z in (-2, -1):
+                    ins[z] = (rng.uniform(0, 1, shapes[z]) < 0.5).astype(dt)
+            seeds = [rng.uniform(-1, 1, O.broadcast_shape_py(shapes)).astype(dt) for _ in range(m)]
+            for pol in (O.CACHE_FORWARD, O.RECOMPUTE_REVERSE):
+                p1, g1, _ = oracle_lib.mixed_step(name, ins, pol, seeds)
+                p2, g2, _ = ref_lib.mixed_step(name, ins, pol, seeds)
+                assert all(bits_equal(x, y) for x, y in zip(p1 + g1, p2 + g2)), (name, shapes, pol)
+
+
+def test_reference_peak_cached_bytes_delta(ref_lib, oracle_lib):
+    """cached - recomputed = 6*64*8 at n=8 fp64 (test_mixed.cpp:121-134)."""
+    ins = O.hmlstm_inputs(oracle_lib, 8, 8, np.float64, "canonical")
+    _, _, cached = ref_lib.mixed_step("hmlstm_update", ins, O.CACHE_FORWARD)
+    _, _, recomputed = ref_lib.mixed_step("hmlstm_update", ins, O.RECOMPUTE_REVERSE)
+    assert cached - recomputed == 6 * 64 * 8
+
+
+# ------------------------------------------------------------ known answers
+def scalar_cell(lib, c, f, i, g, z1, z2):
+    ins = [np.array([v], np.float64) for v in (c, f, i, g, z1, z2)]
+    p, _ = lib.forward("hmlstm_update", ins, real_body=True)
+    return float(p[0][0])
+
+
+def test_kat_scalar_cases(oracle_lib):
+    """test_hmlstm.cpp:32-38."""
+    assert scalar_cell(oracle_lib, 1.0, 0.0, 0.0, 0.0, 0.0, 1.0) == 0.5
+    assert scalar_cell(oracle_lib, 7.0, 0.3, -0.2, 0.9, 0.0, 0.0) == 7.0
+    assert scalar_cell(oracle_lib, 3.0, 0.1, 0.0, 0.0, 1.0, 1.0) == 0.0
+    assert scalar_cell(oracle_lib, 3.0, 0.1, 0.0, 0.0, 1.0, 0.0) == 0.0
+
+
+def test_kat_single_cell_gradients(oracle_lib):
+    """(c,f,i,g) = (1,0,0,0), z = (0,1): grads (0.5, 0.25, 0, 0.5) exactly (test_hmlstm.cpp:105-118)."""
+    ins = [np.full((1, 1), v) for v in (1.0, 0.0, 0.0, 0.0)] + [np.zeros(1), np.ones(1)]
+    for pol in (O.CACHE_FORWARD, O.RECOMPUTE_REVERSE):
+        _, g, _ = oracle_lib.mixed_step("hmlstm_update", ins, pol)
+        assert [float(x.ravel()[0]) for x in g[:4]] == [0.5, 0.25, 0.0, 0.5]
+
+
+def sigmoid(x):
+    return np.where(x >= 0, 1 / (1 + np.exp(-np.abs(x))), np.exp(-np.abs(x)) / (1 + np.exp(-np.abs(x))))
+
+
+def test_kat_closed_forms(oracle_lib):
+    """Piecewise closed-form gradients at 1e-12 (tests/support/hmlstm_closed_form.hpp:14-47)."""
+    for sid in range(1, 7):
+        rng = np.random.default_rng(sid)
+        n = 8
+        c, f, i, g = (rng.uniform(-1, 1, (n, n)) for _ in range(4))
+        z1, z2 = ((rng.uniform(0, 1, n) < 0.5).astype(float) for _ in range(2))
+        w = rng.uniform(-1, 1, (n, n))
+        _, got, _ = oracle_lib.mixed_step("hmlstm_update", [c, f, i, g, z1, z2], seeds=[w])
+        sf, si, tg = sigmoid(f), sigmoid(i), np.tanh(g)
+        upd = ((z1 == 0) & (z2 == 1))[:, None]
+        cpy = ((z1 == 0) & (z2 == 0))[:, None]
+        want = [w * np.where(upd, sf, np.where(cpy, 1.0, 0.0)),
+                w * np.where(upd, sf * (1 - sf) * c, 0.0),
+                w * np.where(cpy, 0.0, si * (1 - si) * tg),
+                w * np.where(cpy, 0.0, si * (1 - tg * tg))]
+        for k in range(4):
+            assert_close(got[k], want[k], 1e-12, 1e-14, f"closed form {k}")
+        assert np.all(got[4] == 0) and np.all(got[5] == 0)
+
+
+def test_kat_product_diag_and_reflect(oracle_lib):
+    """diag(x*y) = (y, x) exactly (test_forward.cpp:69-79); reflect derivative is
+    +-1 by branch (test_forward.cpp:116-136)."""
+    rng = np.random.default_rng(3)
+    x, y = rng.uniform(-1, 1, 4), rng.uniform(-1, 1, 4)
+    p, d = oracle_lib.forward("mul", [x, y])
+    assert bits_equal(d[0], y) and bits_equal(d[1], x) and bits_equal(p[0], x * y)
+    _, d = oracle_lib.forward("reflect", [np.array([-0.8, 0.1, 0.49, 0.51, 2.0])])
+    assert d[0].tolist() == [-1.0, -1.0, -1.0, 1.0, 1.0]
+
+
+def test_kat_scatter_add(oracle_lib):
+    """scatter_add reduces or expands (test_broadcast.cpp:265-283)."""
+    rng = np.random.default_rng(47)
+    contrib = rng.uniform(-1, 1, (3, 4))
+    row = np.zeros((3, 1))
+    oracle_lib.scatter_add(row, contrib)
+    assert np.allclose(row[:, 0], contrib.sum(axis=1), rtol=1e-15)
+    full = np.ones((3, 4))
+    r = rng.uniform(-1, 1, (3, 1))
+    oracle_lib.scatter_add(full, r)
+    assert np.array_equal(full, np.broadcast_to(1.0 + r, (3, 4)))
+
+
+def test_kat_policies_bit_identical(oracle_lib):
+    """CacheForward == RecomputeReverse bit-for-bit (mixed.hpp:103-130)."""
+    ins = O.hmlstm_inputs(oracle_lib, 16, 32, np.float64, "bias")
+    _, g0, _ = oracle_lib.mixed_step("hmlstm_update_bias", ins, O.CACHE_FORWARD)
+    _, g1, _ = oracle_lib.mixed_step("hmlstm_update_bias", ins, O.RECOMPUTE_REVERSE)
+    assert all(bits_equal(a, b) for a, b in zip(g0, g1))
+
+
+def test_kat_error_annotations(oracle_lib):
+    """Domain errors carry the output index (forward.hpp:137-146)."""
+    with pytest.raises(O.OracleError) as e:
+        oracle_lib.forward("log", [np.array([[0.5, 2.0], [-1.0, 3.0]])])
+    assert e.value.code == 3 and "at output index (1, 0)" in e.value.msg
+    with pytest.raises(O.OracleError) as e:
+        oracle_lib.forward("div", [np.ones(3), np.array([1.0, 0.0, 0.0])])
+    assert e.value.code == 2 and "(1)" in e.value.msg
+
+
+def test_fp64_accumulated_comparator_is_tighter(oracle_lib):
+    """the serial fp32 reduction drifts from the exact sum
+    by ~1e-5..1e-3 relative at B >= 1024; the fp64-accumulated comparator
+    tracks the fp64 sum of the same rounded terms to ~1 ulp."""
+    ins = O.hmlstm_inputs(oracle_lib, 1024, 64, np.float32, "bias")
+    _, g, a64 = oracle_lib.mixed_step("hmlstm_update_bias", ins)
+    _, d = oracle_lib.forward("hmlstm_update_bias", ins)
+    exact = d[4].astype(np.float64).sum(axis=0)  # w = 1
+    assert np.allclose(a64[4].ravel(), exact, rtol=1e-12, atol=1e-12)
+    drift = np.max(np.abs(g[4].ravel().astype(np.float64) - exact) / np.maximum(1e-3, np.abs(exact)))
+    assert drift < 1e-2
