@@ -106,37 +106,104 @@ __device__ __forceinline__ void report_error(unsigned long long* word, int64_t f
     }
 }
 
+// ------------------------------------------------- argument-class signatures
+// A signature fixes each argument's stride class at compile time so the
+// loads, stores and reductions of the hot kernels are branch-free and the
+// broadcast (ROW / COL / SCALAR) loads are hoisted; DynSig reads the class
+// from the parameter block (every other shape).
+struct DynSig {
+    static constexpr bool kStatic = false;
+    __host__ __device__ static constexpr int cls(int) { return -1; }
+    __host__ __device__ static constexpr bool has(int) { return true; }
+};
+template <int... C>
+struct Sig {
+    static constexpr bool kStatic = true;
+    static constexpr int kN = sizeof...(C);
+    __host__ __device__ static constexpr int cls(int j) {
+        constexpr int c[] = {C...};
+        return c[j];
+    }
+    __host__ __device__ static constexpr bool has(int k) {
+        constexpr int c[] = {C...};
+        for (int j = 0; j < kN; ++j)
+            if (c[j] == k) return true;
+        return false;
+    }
+};
+
+template <class S>
+__device__ __forceinline__ int arg_class(const int* dyn, int j) {
+    if constexpr (S::kStatic) return S::cls(j);
+    else return dyn[j];
+}
+
+// Programmatic dependent launch (PTX griddepcontrol): the dependent kernel
+// may be scheduled while its predecessor drains; it waits here before it
+// touches any memory, so ordering is exactly stream order.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 // ------------------------------------------------------------- K1 params
+// 2-D grid: blockIdx.x = column tile (txv vector-columns), blockIdx.y = row
+// tile (ty thread-rows x rpt rows per thread).
 template <int N, int M, class T>
 struct Fwd2DParams {
     const T* in[N];
     int cls[N];
     T* primal[M];
     T* partials[M * N];
-    int64_t rows, cols, vcols;
+    int64_t rows, cols;
+    int vcols;
     int txv_shift, ty, rpt;
-    int64_t n_col_tiles, tile_rows;
+    int64_t tile_rows;
     unsigned long long* err;
 };
 
 // K1. kReal: evaluate the real body (primal only). Otherwise the dual body,
 // storing whichever of primal / partials pointers are non-null.
-template <class Body, class T, int V, bool kReal>
+template <class Body, class T, int V, bool kReal, class S>
 __global__ void __launch_bounds__(kThreads) fwd2d_kernel(const __grid_constant__ Fwd2DParams<Body::kIn, Body::kOut, T> p) {
     constexpr int N = Body::kIn, M = Body::kOut;
+    pdl_wait();
+    pdl_trigger();
     if constexpr (Body::kMayRaise && !kReal) s_err_flag[threadIdx.x] = 0;
     const int tx = threadIdx.x & ((1 << p.txv_shift) - 1);
     const int ty = threadIdx.x >> p.txv_shift;
-    const int64_t ct = blockIdx.x % p.n_col_tiles;
-    const int64_t rt = blockIdx.x / p.n_col_tiles;
-    const int64_t vc = (ct << p.txv_shift) + tx;
+    const int vc = (blockIdx.x << p.txv_shift) + tx;
     if (vc >= p.vcols) return;
-    const int64_t c0 = vc * V;
-    const int64_t r_end = min(p.rows, (rt + 1) * p.tile_rows);
-    for (int64_t r = rt * p.tile_rows + ty; r < r_end; r += p.ty) {
+    const int64_t c0 = int64_t(vc) * V;
+    // broadcast loads that do not depend on the row: hoisted
+    Pack<T, V> xc[N];
+#pragma unroll
+    for (int j = 0; j < N; ++j) {
+        const int cls = arg_class<S>(p.cls, j);
+        if (cls == kCol) xc[j] = ld_ro<T, V>(p.in[j] + c0);
+        if (cls == kScalar) {
+            const T v0 = __ldg(p.in[j]);
+#pragma unroll
+            for (int v = 0; v < V; ++v) xc[j].x[v] = v0;
+        }
+    }
+    const int64_t r0 = int64_t(blockIdx.y) * p.tile_rows + ty;
+    for (int k = 0; k < p.rpt; ++k) {
+        const int64_t r = r0 + int64_t(k) * p.ty;
+        if (r >= p.rows) break;
+        const int64_t off = r * p.cols + c0;
         Pack<T, V> x[N];
 #pragma unroll
-        for (int j = 0; j < N; ++j) x[j] = ld_arg<T, V>(p.in[j], p.cls[j], r, c0, p.cols);
+        for (int j = 0; j < N; ++j) {
+            const int cls = arg_class<S>(p.cls, j);
+            if (cls == kFull) {
+                x[j] = ld_stream<T, V>(p.in[j] + off);
+            } else if (cls == kRow) {
+                const T v0 = __ldg(p.in[j] + r);
+#pragma unroll
+                for (int v = 0; v < V; ++v) x[j].x[v] = v0;
+            } else {
+                x[j] = xc[j];
+            }
+        }
         if constexpr (kReal) {
             Pack<T, V> y[M];
 #pragma unroll
@@ -150,7 +217,7 @@ __global__ void __launch_bounds__(kThreads) fwd2d_kernel(const __grid_constant__
             }
 #pragma unroll
             for (int i = 0; i < M; ++i)
-                if (p.primal[i]) st_vec<T, V>(p.primal[i] + r * p.cols + c0, y[i]);
+                if (p.primal[i]) st_vec<T, V>(p.primal[i] + off, y[i]);
         } else {
             Pack<T, V> y[M];
             Pack<T, V> d[M * N];
@@ -163,7 +230,7 @@ __global__ void __launch_bounds__(kThreads) fwd2d_kernel(const __grid_constant__
                     xi[j].d[j] = T(1);
                 }
                 Body::template body<Dual<T, N>>(xi, yo);
-                if constexpr (Body::kMayRaise) report_error(p.err, r * p.cols + c0 + v);
+                if constexpr (Body::kMayRaise) report_error(p.err, off + v);
 #pragma unroll
                 for (int i = 0; i < M; ++i) {
                     y[i].x[v] = yo[i].v;
@@ -173,10 +240,10 @@ __global__ void __launch_bounds__(kThreads) fwd2d_kernel(const __grid_constant__
             }
 #pragma unroll
             for (int i = 0; i < M; ++i) {
-                if (p.primal[i]) st_vec<T, V>(p.primal[i] + r * p.cols + c0, y[i]);
+                if (p.primal[i]) st_vec<T, V>(p.primal[i] + off, y[i]);
 #pragma unroll
                 for (int j = 0; j < N; ++j)
-                    if (p.partials[i * N + j]) st_vec<T, V>(p.partials[i * N + j] + r * p.cols + c0, d[i * N + j]);
+                    if (p.partials[i * N + j]) st_vec<T, V>(p.partials[i * N + j] + off, d[i * N + j]);
             }
         }
     }
@@ -193,9 +260,11 @@ struct Pull2DParams {
     int slot[N];          // index among active args of the same reduced class
     int row_j[N], col_j[N], scal_j[N];  // slot -> argument index
     uint32_t acc_mask;    // bit j: add into the existing slot
-    int64_t rows, cols, vcols;
+    int64_t rows, cols;
+    int vcols;
     int txv_shift, ty, rpt;
-    int64_t n_col_tiles, n_row_tiles, tile_rows;
+    int64_t tile_rows;
+    int n_row_tiles, n_col_tiles;
     int n_row_args, n_col_args, n_scalar_args;
     double* ws_row;       // [n_row_args][n_col_tiles][rows]
     double* ws_col;       // [n_col_args][n_row_tiles][cols]
@@ -209,49 +278,92 @@ __device__ __forceinline__ T finish(double s, const T* slot_ptr, bool accumulate
     return accumulate ? T(double(*slot_ptr) + s) : T(s);
 }
 
-// Per-thread contribution of input j over the V cells: term_i = w_i * D_ij
-// rounded to T, exactly the tensor_zip of backprop_diag (mixed.hpp:34-38).
-template <class Body, class T, int V, bool kRecompute>
+// Shared-memory layout of K2 (dynamic, doubles):
+//   col_acc [n_col_args][kThreads][V]      per-thread column partials
+//   row_acc [n_row_args][rpt*ty][wpr]      per-(row, warp) row partials
+//   scal_acc[n_scalar_args][kThreads]      per-thread scalar partials
+__host__ __device__ inline size_t pull_smem_doubles(int n_col, int n_row, int n_scal, int V, int rpt, int ty, int wpr) {
+    return size_t(n_col) * kThreads * V + size_t(n_row) * rpt * ty * wpr + size_t(n_scal) * kThreads;
+}
+
+// K2: terms w_i * D_ij rounded to T exactly like backprop_diag's tensor_zip
+// (mixed.hpp:34-38); FULL slots get the reference's element arithmetic,
+// reduced slots an fp64 sum of those terms in a fixed order.
+template <class Body, class T, int V, bool kRecompute, class S>
 __global__ void __launch_bounds__(kThreads) pull2d_kernel(const __grid_constant__ Pull2DParams<Body::kIn, Body::kOut, T> p) {
     constexpr int N = Body::kIn, M = Body::kOut;
+    constexpr bool kAnyRow = !S::kStatic || S::has(kRow);
+    constexpr bool kAnyCol = !S::kStatic || S::has(kCol);
+    constexpr bool kAnyScal = !S::kStatic || S::has(kScalar);
     extern __shared__ double smem[];
-    double* col_acc = smem;                                        // [n_col_args][kThreads*V]
-    double* scal_acc = smem + size_t(p.n_col_args) * kThreads * V; // [n_scalar_args][kThreads]
     __shared__ unsigned int s_last;
+    pdl_wait();
     if constexpr (Body::kMayRaise && kRecompute) s_err_flag[threadIdx.x] = 0;
 
     const int tid = threadIdx.x;
-    const int tx = tid & ((1 << p.txv_shift) - 1);
-    const int ty = tid >> p.txv_shift;
     const int txv = 1 << p.txv_shift;
-    const int64_t ct = blockIdx.x % p.n_col_tiles;
-    const int64_t rt = blockIdx.x / p.n_col_tiles;
-    const int64_t vc = (ct << p.txv_shift) + tx;
+    const int tx = tid & (txv - 1);
+    const int ty = tid >> p.txv_shift;
+    const int lanes = txv < 32 ? txv : 32;          // lanes sharing a row in one warp
+    const int wpr = txv > 32 ? txv >> 5 : 1;         // warps per row
+    const int wir = (tid & (txv - 1)) >> 5;          // warp index within its row
+    const int ct = blockIdx.x, rt = blockIdx.y;
+    const int vc = (ct << p.txv_shift) + tx;
     const bool active = vc < p.vcols;
-    const int64_t c0 = vc * V;
+    const int64_t c0 = int64_t(vc) * V;
+    const int trows = p.rpt * p.ty;                  // rows of this tile
 
-    for (int a = 0; a < p.n_col_args; ++a)
+    double* col_acc = smem;
+    double* row_acc = col_acc + size_t(p.n_col_args) * kThreads * V;
+    double* scal_acc = row_acc + size_t(p.n_row_args) * trows * wpr;
+    if constexpr (kAnyCol)
+        for (int i = tid; i < p.n_col_args * kThreads * V; i += kThreads) col_acc[i] = 0.0;
+    if constexpr (kAnyScal)
+        for (int a = 0; a < p.n_scalar_args; ++a) scal_acc[a * kThreads + tid] = 0.0;
+
+    // broadcast inputs that do not depend on the row (recompute only)
+    Pack<T, V> xc[N];
+    if constexpr (kRecompute) {
 #pragma unroll
-        for (int v = 0; v < V; ++v) col_acc[(size_t(a) * kThreads + tid) * V + v] = 0.0;
-    for (int a = 0; a < p.n_scalar_args; ++a) scal_acc[a * kThreads + tid] = 0.0;
+        for (int j = 0; j < N; ++j) {
+            const int cls = arg_class<S>(p.cls, j);
+            if (active && cls == kCol) xc[j] = ld_ro<T, V>(p.in[j] + c0);
+            if (cls == kScalar) {
+                const T v0 = __ldg(p.in[j]);
+#pragma unroll
+                for (int v = 0; v < V; ++v) xc[j].x[v] = v0;
+            }
+        }
+    }
 
-    const int64_t r_base = rt * p.tile_rows + ty;
+    const int64_t r0 = int64_t(rt) * p.tile_rows + ty;
     // Every lane runs the same rpt iterations (rows past the end are masked),
-    // so the ROW shuffles below always see complete lane groups.
+    // so the ROW shuffles always see complete lane groups.
     for (int k = 0; k < p.rpt; ++k) {
-        const int64_t r = r_base + int64_t(k) * p.ty;
+        const int64_t r = r0 + int64_t(k) * p.ty;
         const bool live = active && r < p.rows;
+        const int64_t off = r * p.cols + c0;
         Pack<T, V> w[M];
-#pragma unroll
-        for (int i = 0; i < M; ++i)
-            if (p.w[i] && live) w[i] = ld_stream<T, V>(p.w[i] + r * p.cols + c0);
-        // D[i][j] for this row's V cells
         Pack<T, V> D[M * N];
         if (live) {
+#pragma unroll
+            for (int i = 0; i < M; ++i)
+                if (p.w[i]) w[i] = ld_stream<T, V>(p.w[i] + off);
             if constexpr (kRecompute) {
                 Pack<T, V> x[N];
 #pragma unroll
-                for (int j = 0; j < N; ++j) x[j] = ld_arg<T, V>(p.in[j], p.cls[j], r, c0, p.cols);
+                for (int j = 0; j < N; ++j) {
+                    const int cls = arg_class<S>(p.cls, j);
+                    if (cls == kFull) {
+                        x[j] = ld_stream<T, V>(p.in[j] + off);
+                    } else if (cls == kRow) {
+                        const T v0 = __ldg(p.in[j] + r);
+#pragma unroll
+                        for (int v = 0; v < V; ++v) x[j].x[v] = v0;
+                    } else {
+                        x[j] = xc[j];
+                    }
+                }
 #pragma unroll
                 for (int v = 0; v < V; ++v) {
                     Dual<T, N> xi[N], yo[M];
@@ -261,7 +373,7 @@ __global__ void __launch_bounds__(kThreads) pull2d_kernel(const __grid_constant_
                         xi[j].d[j] = T(1);
                     }
                     Body::template body<Dual<T, N>>(xi, yo);
-                    if constexpr (Body::kMayRaise) report_error(p.err, r * p.cols + c0 + v);
+                    if constexpr (Body::kMayRaise) report_error(p.err, off + v);
 #pragma unroll
                     for (int i = 0; i < M; ++i)
 #pragma unroll
@@ -272,17 +384,17 @@ __global__ void __launch_bounds__(kThreads) pull2d_kernel(const __grid_constant_
                 for (int i = 0; i < M; ++i)
 #pragma unroll
                     for (int j = 0; j < N; ++j)
-                        if (p.w[i] && p.adj[j]) D[i * N + j] = ld_stream<T, V>(p.D[i * N + j] + r * p.cols + c0);
+                        if (p.w[i] && p.adj[j]) D[i * N + j] = ld_stream<T, V>(p.D[i * N + j] + off);
             }
         }
 #pragma unroll
         for (int j = 0; j < N; ++j) {
             if (!p.adj[j]) continue;
-            const int cls = p.cls[j];
+            const int cls = arg_class<S>(p.cls, j);
             const bool acc = (p.acc_mask >> j) & 1u;
             if (cls == kFull) {
                 if (!live) continue;
-                T* dst = p.adj[j] + r * p.cols + c0;
+                T* dst = p.adj[j] + off;
                 Pack<T, V> out;
                 if (acc) out = ld_stream<T, V>(dst);
 #pragma unroll
@@ -307,131 +419,144 @@ __global__ void __launch_bounds__(kThreads) pull2d_kernel(const __grid_constant_
                         if (p.w[i]) s[v] += double(T(w[i].x[v] * D[i * N + j].x[v]));
             }
             if (cls == kCol) {
-                double* ca = col_acc + (size_t(p.slot[j]) * kThreads + tid) * V;
+                if constexpr (kAnyCol) {
+                    double* ca = col_acc + (size_t(p.slot[j]) * kThreads + tid) * V;
 #pragma unroll
-                for (int v = 0; v < V; ++v) ca[v] += s[v];
-            } else if (cls == kScalar) {
-                double t = 0.0;
-#pragma unroll
-                for (int v = 0; v < V; ++v) t += s[v];
-                scal_acc[p.slot[j] * kThreads + tid] += t;
-            } else {  // kRow: reduce the txv lanes of this row
-                double t = 0.0;
-#pragma unroll
-                for (int v = 0; v < V; ++v) t += s[v];
-                for (int off = txv >> 1; off > 0; off >>= 1) t += __shfl_xor_sync(0xffffffffu, t, off, txv);
-                if (tx == 0 && r < p.rows) {
-                    if (p.n_col_tiles == 1) {
-                        p.adj[j][r] = finish<T>(t, p.adj[j] + r, acc);
-                    } else {
-                        p.ws_row[(size_t(p.slot[j]) * p.n_col_tiles + ct) * p.rows + r] = t;
-                    }
+                    for (int v = 0; v < V; ++v) ca[v] += s[v];
                 }
+            } else if (cls == kScalar) {
+                if constexpr (kAnyScal) {
+                    double t = 0.0;
+#pragma unroll
+                    for (int v = 0; v < V; ++v) t += s[v];
+                    scal_acc[p.slot[j] * kThreads + tid] += t;
+                }
+            } else if constexpr (kAnyRow) {  // kRow: lanes of this row in this warp
+                double t = 0.0;
+#pragma unroll
+                for (int v = 0; v < V; ++v) t += s[v];
+                for (int o = lanes >> 1; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o, lanes);
+                if ((tid & (lanes - 1)) == 0)
+                    row_acc[(size_t(p.slot[j]) * trows + k * p.ty + ty) * wpr + wir] = t;
             }
         }
     }
-    if (p.n_col_args == 0 && p.n_scalar_args == 0 && (p.n_row_args == 0 || p.n_col_tiles == 1)) return;
-
-    // ---- CTA-level combination of COL / SCALAR partials (fixed order)
-    __syncthreads();
-    const int ccols = txv * V;  // columns covered by this tile
-    for (int item = tid; item < p.n_col_args * ccols; item += kThreads) {
-        const int a = item / ccols, cc = item % ccols;
-        const int txi = cc / V, v = cc % V;
-        const int64_t c = (ct << p.txv_shift) * V + cc;
-        if (c >= p.cols) continue;
-        double s = 0.0;
-        for (int y = 0; y < p.ty; ++y) s += col_acc[(size_t(a) * kThreads + (y << p.txv_shift) + txi) * V + v];
-        if (p.n_row_tiles == 1) {
-            const int j = p.col_j[a];
-            p.adj[j][c] = finish<T>(s, p.adj[j] + c, (p.acc_mask >> j) & 1u);
-        } else {
-            p.ws_col[(size_t(a) * p.n_row_tiles + rt) * p.cols + c] = s;
-        }
-    }
-    const int64_t n_ctas = p.n_row_tiles * p.n_col_tiles;
-    for (int a = 0; a < p.n_scalar_args; ++a) {
-        // fixed-shape tree over the 256 per-thread sums
+    if constexpr (!kAnyRow && !kAnyCol && !kAnyScal) return;
+    else {
         __syncthreads();
-        for (int stride = kThreads / 2; stride > 0; stride >>= 1) {
-            if (tid < stride) scal_acc[a * kThreads + tid] += scal_acc[a * kThreads + tid + stride];
-            __syncthreads();
-        }
-        if (tid == 0) {
-            const double s = scal_acc[a * kThreads];
-            if (n_ctas == 1) {
-                const int j = p.scal_j[a];
-                p.adj[j][0] = finish<T>(s, p.adj[j], (p.acc_mask >> j) & 1u);
-            } else {
-                p.ws_scalar[size_t(a) * n_ctas + blockIdx.x] = s;
-            }
-        }
-    }
-
-    // ---- cross-CTA completion: the last CTA of a tile row / column / grid
-    // combines the fp64 partials in tile order.
-    __threadfence();
-    __syncthreads();
-    // rows of this row tile (partials from every column tile)
-    if (p.n_row_args > 0 && p.n_col_tiles > 1) {
-        if (tid == 0) s_last = atomicAdd(&p.counters[rt], 1u) == unsigned(p.n_col_tiles - 1);
-        __syncthreads();
-        if (s_last) {
-            __threadfence();
-            const int64_t r0 = rt * p.tile_rows;
-            const int64_t nr = min(p.tile_rows, p.rows - r0);
-            for (int64_t item = tid; item < p.n_row_args * nr; item += kThreads) {
-                const int a = int(item / nr);
-                const int64_t r = r0 + item % nr;
-                double s = 0.0;
-                for (int64_t k = 0; k < p.n_col_tiles; ++k) s += __ldcg(&p.ws_row[(size_t(a) * p.n_col_tiles + k) * p.rows + r]);
+        const int64_t n_ctas = int64_t(p.n_row_tiles) * p.n_col_tiles;
+        // ---- CTA-level combination (fixed order)
+        if constexpr (kAnyRow) {
+            for (int item = tid; item < p.n_row_args * trows; item += kThreads) {
+                const int a = item / trows, lr = item % trows;
+                const int kk = lr / p.ty, yy = lr % p.ty;
+                const int64_t r = int64_t(rt) * p.tile_rows + yy + int64_t(kk) * p.ty;
+                if (r >= p.rows) continue;
+                double sacc = 0.0;
+                for (int q = 0; q < wpr; ++q) sacc += row_acc[(size_t(a) * trows + lr) * wpr + q];
                 const int j = p.row_j[a];
-                p.adj[j][r] = finish<T>(s, p.adj[j] + r, (p.acc_mask >> j) & 1u);
+                if (p.n_col_tiles == 1) p.adj[j][r] = finish<T>(sacc, p.adj[j] + r, (p.acc_mask >> j) & 1u);
+                else p.ws_row[(size_t(a) * p.n_col_tiles + ct) * p.rows + r] = sacc;
             }
-            if (tid == 0) p.counters[rt] = 0;
         }
-        __syncthreads();
-    }
-    if (p.n_col_args > 0 && p.n_row_tiles > 1) {
-        if (tid == 0) s_last = atomicAdd(&p.counters[p.n_row_tiles + ct], 1u) == unsigned(p.n_row_tiles - 1);
-        __syncthreads();
-        if (s_last) {
-            __threadfence();
+        const int ccols = txv * V;
+        if constexpr (kAnyCol) {
             for (int item = tid; item < p.n_col_args * ccols; item += kThreads) {
-                const int a = item / ccols;
-                const int64_t c = (ct << p.txv_shift) * V + item % ccols;
+                const int a = item / ccols, cc = item % ccols;
+                const int txi = cc / V, v = cc % V;
+                const int64_t c = int64_t(ct) * ccols + cc;
                 if (c >= p.cols) continue;
-                double s = 0.0;
-                for (int64_t k = 0; k < p.n_row_tiles; ++k) s += __ldcg(&p.ws_col[(size_t(a) * p.n_row_tiles + k) * p.cols + c]);
+                double sacc = 0.0;
+                for (int y = 0; y < p.ty; ++y) sacc += col_acc[(size_t(a) * kThreads + (y << p.txv_shift) + txi) * V + v];
                 const int j = p.col_j[a];
-                p.adj[j][c] = finish<T>(s, p.adj[j] + c, (p.acc_mask >> j) & 1u);
+                if (p.n_row_tiles == 1) p.adj[j][c] = finish<T>(sacc, p.adj[j] + c, (p.acc_mask >> j) & 1u);
+                else p.ws_col[(size_t(a) * p.n_row_tiles + rt) * p.cols + c] = sacc;
             }
-            if (tid == 0) p.counters[p.n_row_tiles + ct] = 0;
         }
-        __syncthreads();
-    }
-    if (p.n_scalar_args > 0 && n_ctas > 1) {
-        unsigned int* cnt = &p.counters[p.n_row_tiles + p.n_col_tiles];
-        if (tid == 0) s_last = atomicAdd(cnt, 1u) == unsigned(n_ctas - 1);
-        __syncthreads();
-        if (s_last) {
-            __threadfence();
+        if constexpr (kAnyScal) {
             for (int a = 0; a < p.n_scalar_args; ++a) {
-                double s = 0.0;
-                for (int64_t k = tid; k < n_ctas; k += kThreads) s += __ldcg(&p.ws_scalar[size_t(a) * n_ctas + k]);
-                scal_acc[a * kThreads + tid] = s;
                 __syncthreads();
                 for (int stride = kThreads / 2; stride > 0; stride >>= 1) {
                     if (tid < stride) scal_acc[a * kThreads + tid] += scal_acc[a * kThreads + tid + stride];
                     __syncthreads();
                 }
                 if (tid == 0) {
+                    const double sacc = scal_acc[a * kThreads];
                     const int j = p.scal_j[a];
-                    p.adj[j][0] = finish<T>(scal_acc[a * kThreads], p.adj[j], (p.acc_mask >> j) & 1u);
+                    if (n_ctas == 1) p.adj[j][0] = finish<T>(sacc, p.adj[j], (p.acc_mask >> j) & 1u);
+                    else p.ws_scalar[size_t(a) * n_ctas + size_t(rt) * p.n_col_tiles + ct] = sacc;
                 }
-                __syncthreads();
             }
-            if (tid == 0) *cnt = 0;
+        }
+        const bool need_row = kAnyRow && p.n_row_args > 0 && p.n_col_tiles > 1;
+        const bool need_col = kAnyCol && p.n_col_args > 0 && p.n_row_tiles > 1;
+        const bool need_scal = kAnyScal && p.n_scalar_args > 0 && n_ctas > 1;
+        if (!(need_row || need_col || need_scal)) return;
+
+        // ---- cross-CTA completion: the last CTA of a tile row / column /
+        // grid (integer ticket) combines the fp64 partials in tile order.
+        __threadfence();
+        __syncthreads();
+        if (need_row) {
+            if (tid == 0) s_last = atomicAdd(&p.counters[rt], 1u) == unsigned(p.n_col_tiles - 1);
+            __syncthreads();
+            if (s_last) {
+                __threadfence();
+                const int64_t rb = int64_t(rt) * p.tile_rows;
+                const int64_t nr = min(p.tile_rows, p.rows - rb);
+                for (int64_t item = tid; item < p.n_row_args * nr; item += kThreads) {
+                    const int a = int(item / nr);
+                    const int64_t r = rb + item % nr;
+                    double sacc = 0.0;
+                    for (int q = 0; q < p.n_col_tiles; ++q) sacc += __ldcg(&p.ws_row[(size_t(a) * p.n_col_tiles + q) * p.rows + r]);
+                    const int j = p.row_j[a];
+                    p.adj[j][r] = finish<T>(sacc, p.adj[j] + r, (p.acc_mask >> j) & 1u);
+                }
+                if (tid == 0) p.counters[rt] = 0;
+            }
+            __syncthreads();
+        }
+        if (need_col) {
+            if (tid == 0) s_last = atomicAdd(&p.counters[p.n_row_tiles + ct], 1u) == unsigned(p.n_row_tiles - 1);
+            __syncthreads();
+            if (s_last) {
+                __threadfence();
+                for (int item = tid; item < p.n_col_args * ccols; item += kThreads) {
+                    const int a = item / ccols;
+                    const int64_t c = int64_t(ct) * ccols + item % ccols;
+                    if (c >= p.cols) continue;
+                    double sacc = 0.0;
+                    for (int q = 0; q < p.n_row_tiles; ++q) sacc += __ldcg(&p.ws_col[(size_t(a) * p.n_row_tiles + q) * p.cols + c]);
+                    const int j = p.col_j[a];
+                    p.adj[j][c] = finish<T>(sacc, p.adj[j] + c, (p.acc_mask >> j) & 1u);
+                }
+                if (tid == 0) p.counters[p.n_row_tiles + ct] = 0;
+            }
+            __syncthreads();
+        }
+        if (need_scal) {
+            unsigned int* cnt = &p.counters[p.n_row_tiles + p.n_col_tiles];
+            if (tid == 0) s_last = atomicAdd(cnt, 1u) == unsigned(n_ctas - 1);
+            __syncthreads();
+            if (s_last) {
+                __threadfence();
+                for (int a = 0; a < p.n_scalar_args; ++a) {
+                    double sacc = 0.0;
+                    for (int64_t q = tid; q < n_ctas; q += kThreads) sacc += __ldcg(&p.ws_scalar[size_t(a) * n_ctas + q]);
+                    scal_acc[a * kThreads + tid] = sacc;
+                    __syncthreads();
+                    for (int stride = kThreads / 2; stride > 0; stride >>= 1) {
+                        if (tid < stride) scal_acc[a * kThreads + tid] += scal_acc[a * kThreads + tid + stride];
+                        __syncthreads();
+                    }
+                    if (tid == 0) {
+                        const int j = p.scal_j[a];
+                        p.adj[j][0] = finish<T>(scal_acc[a * kThreads], p.adj[j], (p.acc_mask >> j) & 1u);
+                    }
+                    __syncthreads();
+                }
+                if (tid == 0) *cnt = 0;
+            }
         }
     }
 }

@@ -1,6 +1,8 @@
-// Host launchers: pick the 2-D vectorised kernels or the generic rank-N
-// fallback for one registered body, fill the by-value parameter block and
-// launch on the caller's stream. Included once per registration TU.
+// Host launchers: pick the 2-D vectorised kernels (with a compile-time
+// argument-class signature when one is registered for the body, else the
+// runtime-class variant) or the generic rank-N fallback, fill the by-value
+// parameter block and launch on the caller's stream with programmatic
+// dependent launch enabled. Included once per registration TU.
 #pragma once
 
 #include <cstdint>
@@ -10,6 +12,9 @@
 #include "registry.hpp"
 
 namespace bcad_cu_impl {
+
+using bcad_dev::DynSig;
+using bcad_dev::Sig;
 
 inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 
@@ -25,6 +30,42 @@ inline int generic_grid(int64_t work) {
     return int(blocks < 1 ? 1 : (blocks > cap ? cap : blocks));
 }
 
+// cudaLaunchKernelEx with cudaLaunchAttributeProgrammaticStreamSerialization:
+// the kernel may be scheduled while the previous kernel on the stream drains
+// and blocks in griddepcontrol.wait until it has completed.
+template <class Params>
+cudaError_t launch_pdl(void (*kern)(Params), dim3 grid, size_t smem, cudaStream_t stream, const Params& p) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kern, p);
+}
+
+template <class S>
+bool sig_matches(const Plan& plan) {
+    if (S::kN != plan.n) return false;
+    for (int j = 0; j < plan.n; ++j)
+        if (S::cls(j) != plan.cls[j]) return false;
+    return true;
+}
+
+template <class F>
+int with_sig(const Plan&, F&& f) {
+    return f(DynSig{});
+}
+template <class S0, class... Rest, class F>
+int with_sig(const Plan& plan, F&& f) {
+    if (sig_matches<S0>(plan)) return f(S0{});
+    return with_sig<Rest...>(plan, f);
+}
+
 template <int N, int M, class T>
 void fill_generic(bcad_dev::GenParams<N, M, T>& g, const Plan& plan) {
     g.out_rank = plan.out_rank;
@@ -37,7 +78,7 @@ void fill_generic(bcad_dev::GenParams<N, M, T>& g, const Plan& plan) {
 }
 
 // ---------------------------------------------------------------- forward
-template <class Body, class T>
+template <class Body, class T, class... Sigs>
 int launch_fwd_t(const FwdArgs& a, std::string* err) {
     constexpr int N = Body::kIn, M = Body::kOut, V = vec_width<T>();
     const Plan& plan = *a.plan;
@@ -51,7 +92,7 @@ int launch_fwd_t(const FwdArgs& a, std::string* err) {
             if (a.partials[i * N + j] && !aligned16(a.partials[i * N + j])) vec = false;
     }
     if (vec) {
-        const Tiling t = choose_tiling(plan, V, false);
+        const Tiling t = choose_tiling(plan, V, ClassMix{});  // no reductions in K1: wide row tiles
         bcad_dev::Fwd2DParams<N, M, T> p{};
         for (int j = 0; j < N; ++j) {
             p.in[j] = static_cast<const T*>(a.in[j]);
@@ -63,16 +104,18 @@ int launch_fwd_t(const FwdArgs& a, std::string* err) {
         }
         p.rows = plan.rows;
         p.cols = plan.cols;
-        p.vcols = t.vcols;
+        p.vcols = int(t.vcols);
         p.txv_shift = __builtin_ctz(unsigned(t.txv));
         p.ty = t.ty;
         p.rpt = t.rpt;
-        p.n_col_tiles = t.n_col_tiles;
         p.tile_rows = t.tile_rows;
         p.err = a.err;
-        if (real) bcad_dev::fwd2d_kernel<Body, T, V, true><<<unsigned(t.n_ctas), kThreads, 0, a.stream>>>(p);
-        else bcad_dev::fwd2d_kernel<Body, T, V, false><<<unsigned(t.n_ctas), kThreads, 0, a.stream>>>(p);
-        return cuda_status(cudaGetLastError(), err);
+        const dim3 grid(unsigned(t.n_col_tiles), unsigned(t.n_row_tiles));
+        return with_sig<Sigs...>(plan, [&](auto sig) {
+            using S = decltype(sig);
+            auto kern = real ? &bcad_dev::fwd2d_kernel<Body, T, V, true, S> : &bcad_dev::fwd2d_kernel<Body, T, V, false, S>;
+            return cuda_status(launch_pdl(kern, grid, 0, a.stream, p), err);
+        });
     }
     bcad_dev::GenParams<N, M, T> g{};
     fill_generic(g, plan);
@@ -89,7 +132,7 @@ int launch_fwd_t(const FwdArgs& a, std::string* err) {
 }
 
 // --------------------------------------------------------------- pullback
-template <class Body, class T>
+template <class Body, class T, class... Sigs>
 int launch_pull_t(const PullArgs& a, std::string* err) {
     constexpr int N = Body::kIn, M = Body::kOut, V = vec_width<T>();
     const Plan& plan = *a.plan;
@@ -107,9 +150,7 @@ int launch_pull_t(const PullArgs& a, std::string* err) {
         if ((plan.cls[j] == kFull || plan.cls[j] == kCol) && !aligned16(a.in[j])) vec = false;
 
     if (vec) {
-        bool has_col = false;
-        for (int j = 0; j < N; ++j) has_col |= plan.cls[j] == kCol;
-        const Tiling t = choose_tiling(plan, V, has_col);
+        const Tiling t = choose_tiling(plan, V, class_mix(plan));
         const PullLayout L = pull_layout(plan, t);  // offsets sized for every argument
         if (a.ws_bytes < L.total || (L.total > 0 && !a.workspace)) {
             *err = "pullback workspace too small: need " + std::to_string(L.total) + " bytes";
@@ -134,13 +175,13 @@ int launch_pull_t(const PullArgs& a, std::string* err) {
         }
         p.rows = plan.rows;
         p.cols = plan.cols;
-        p.vcols = t.vcols;
+        p.vcols = int(t.vcols);
         p.txv_shift = __builtin_ctz(unsigned(t.txv));
         p.ty = t.ty;
         p.rpt = t.rpt;
-        p.n_col_tiles = t.n_col_tiles;
-        p.n_row_tiles = t.n_row_tiles;
         p.tile_rows = t.tile_rows;
+        p.n_col_tiles = int(t.n_col_tiles);
+        p.n_row_tiles = int(t.n_row_tiles);
         p.n_row_args = nr;
         p.n_col_args = nc;
         p.n_scalar_args = ns;
@@ -150,14 +191,17 @@ int launch_pull_t(const PullArgs& a, std::string* err) {
         p.ws_scalar = reinterpret_cast<double*>(ws + L.ws_scalar);
         p.counters = reinterpret_cast<unsigned int*>(ws + L.counters);
         p.err = a.err;
-        const size_t smem = size_t(nc) * kThreads * V * 8 + size_t(ns) * kThreads * 8;
-        auto kern = recompute ? &bcad_dev::pull2d_kernel<Body, T, V, true> : &bcad_dev::pull2d_kernel<Body, T, V, false>;
-        if (smem > 48 * 1024) {
-            const cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-            if (e != cudaSuccess) return cuda_status(e, err);
-        }
-        kern<<<unsigned(t.n_ctas), kThreads, smem, a.stream>>>(p);
-        return cuda_status(cudaGetLastError(), err);
+        const size_t smem = pull_smem_bytes(nc, nr, ns, t);
+        const dim3 grid(unsigned(t.n_col_tiles), unsigned(t.n_row_tiles));
+        return with_sig<Sigs...>(plan, [&](auto sig) {
+            using S = decltype(sig);
+            auto kern = recompute ? &bcad_dev::pull2d_kernel<Body, T, V, true, S> : &bcad_dev::pull2d_kernel<Body, T, V, false, S>;
+            if (smem > 48 * 1024) {
+                const cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+                if (e != cudaSuccess) return cuda_status(e, err);
+            }
+            return cuda_status(launch_pdl(kern, grid, smem, a.stream, p), err);
+        });
     }
     bcad_dev::GenParams<N, M, T> g{};
     fill_generic(g, plan);
@@ -182,19 +226,28 @@ int launch_pull_t(const PullArgs& a, std::string* err) {
     return cuda_status(cudaGetLastError(), err);
 }
 
-template <class Body>
+template <class Body, class... Sigs>
 int launch_fwd_any(const FwdArgs& a, std::string* err) {
-    return a.dtype == BCAD_CU_F32 ? launch_fwd_t<Body, float>(a, err) : launch_fwd_t<Body, double>(a, err);
+    return a.dtype == BCAD_CU_F32 ? launch_fwd_t<Body, float, Sigs...>(a, err)
+                                  : launch_fwd_t<Body, double, Sigs...>(a, err);
 }
-template <class Body>
+template <class Body, class... Sigs>
 int launch_pull_any(const PullArgs& a, std::string* err) {
-    return a.dtype == BCAD_CU_F32 ? launch_pull_t<Body, float>(a, err) : launch_pull_t<Body, double>(a, err);
+    return a.dtype == BCAD_CU_F32 ? launch_pull_t<Body, float, Sigs...>(a, err)
+                                  : launch_pull_t<Body, double, Sigs...>(a, err);
 }
+
+// Argument-class signatures of the HM-LSTM workloads:
+// canonical (B,H)x4 + (B)x2; divergence (B,H)x6; bias (B,H)x4 + (1,H)x3 + (B)x2.
+using SigHmlstmCanonical = Sig<kFull, kFull, kFull, kFull, kRow, kRow>;
+using SigHmlstmDivergence = Sig<kFull, kFull, kFull, kFull, kFull, kFull>;
+using SigHmlstmBias = Sig<kFull, kFull, kFull, kFull, kCol, kCol, kCol, kRow, kRow>;
 
 }  // namespace bcad_cu_impl
 
-#define BCAD_ENTRY(Body)                                                                               \
+#define BCAD_ENTRY(Body, ...)                                                                          \
     bcad_cu_kernel_entry {                                                                             \
-        Body::kName, Body::kIn, Body::kOut, Body::kMayRaise, &bcad_cu_impl::launch_fwd_any<Body>,       \
-            &bcad_cu_impl::launch_pull_any<Body>                                                       \
+        Body::kName, Body::kIn, Body::kOut, Body::kMayRaise,                                           \
+            &bcad_cu_impl::launch_fwd_any<Body __VA_OPT__(, ) __VA_ARGS__>,                             \
+            &bcad_cu_impl::launch_pull_any<Body __VA_OPT__(, ) __VA_ARGS__>                             \
     }

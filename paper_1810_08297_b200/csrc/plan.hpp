@@ -137,35 +137,64 @@ inline int make_plan(int n, const bcad_cu_shape* shapes, Plan* p, std::string* e
 }
 
 // Tile geometry of the 2-D kernels: 256 threads as (txv vector-columns) x
-// (ty thread-rows); each thread walks `rpt` rows of its tile.
+// (ty thread-rows); each thread walks `rpt` rows of its tile. The grid is
+// (n_col_tiles, n_row_tiles).
 struct Tiling {
-    int V = 1;         // elements per vector access
-    int64_t vcols = 0; // cols / V
+    int V = 1;          // elements per vector access
+    int64_t vcols = 0;  // cols / V
     int txv = 32, ty = 8, rpt = 1;
-    int64_t tile_rows = 8, n_row_tiles = 1, n_col_tiles = 1, n_ctas = 1;
+    int64_t tile_rows = 8;
+    int64_t n_row_tiles = 1, n_col_tiles = 1, n_ctas = 1;
 };
 
 constexpr int kSmCount = 148;
+constexpr int kCtasPerSm = 4;  // 256-thread CTAs at <= 64 registers per thread
+constexpr int64_t kMaxGridY = 65535;
 
 inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
-inline Tiling choose_tiling(const Plan& p, int V, bool has_col_reduction) {
+struct ClassMix {
+    bool row = false, col = false, scalar = false;
+};
+
+inline ClassMix class_mix(const Plan& p) {
+    ClassMix m;
+    for (int j = 0; j < p.n; ++j) {
+        m.row |= p.cls[j] == kRow;
+        m.col |= p.cls[j] == kCol;
+        m.scalar |= p.cls[j] == kScalar && p.vol > 1;
+    }
+    return m;
+}
+
+// Shape of the tile by reduction mix:
+//  * column reductions ((1,H) args) use one warp per row segment (txv = 32,
+//    128 fp32 columns) and tall tiles, balancing the per-column fp64 partials
+//    (cols x row tiles) against the per-row ones (rows x column tiles);
+//  * otherwise a CTA spans up to 256 vector-columns of one row, so (B)-arg
+//    reductions finish inside the CTA (shuffles + one shared-memory pass).
+// Rows per thread: one wave of CTAs for small problems (latency-bound), about
+// eight waves for large ones (tail-bound), never more than 65535 row tiles.
+inline Tiling choose_tiling(const Plan& p, int V, const ClassMix& mix) {
     Tiling t;
     t.V = V;
     t.vcols = p.cols / V;
+    const int cap = mix.col ? 32 : 256;
     int txv = 1;
-    while (txv < 32 && txv < t.vcols) txv <<= 1;
+    while (txv < cap && txv < t.vcols) txv <<= 1;
     t.txv = txv;
     t.ty = kThreads / txv;
     t.n_col_tiles = ceil_div(t.vcols, txv);
     const int64_t tiles1 = ceil_div(p.rows, t.ty);  // row tiles at rpt = 1
-    // Aim for ~8 resident 256-thread CTAs on each of the 148 SMs, times a few
-    // waves, before growing the per-thread row count; column reductions
-    // favour fewer row tiles (each adds one fp64 partial row to combine).
-    const int64_t target = int64_t(kSmCount) * 8 * (has_col_reduction ? 2 : 4);
-    int64_t rpt = (tiles1 * t.n_col_tiles) / target;
+    const int64_t work = tiles1 * t.n_col_tiles;     // CTAs at rpt = 1
+    const int64_t slots = int64_t(kSmCount) * kCtasPerSm;
+    int64_t rpt = work <= 2 * slots ? ceil_div(work, slots) : work / (8 * slots);
     if (rpt < 1) rpt = 1;
-    if (rpt > 64) rpt = 64;
+    if (rpt > 512) rpt = 512;
+    // keep the per-tile row partials in shared memory small
+    if (mix.row)
+        while (rpt > 1 && rpt * t.ty * (txv > 32 ? txv / 32 : 1) > 4096) rpt >>= 1;
+    while (ceil_div(p.rows, int64_t(t.ty) * rpt) > kMaxGridY) rpt <<= 1;
     t.rpt = int(rpt);
     t.tile_rows = int64_t(t.ty) * t.rpt;
     t.n_row_tiles = ceil_div(p.rows, t.tile_rows);
@@ -173,7 +202,9 @@ inline Tiling choose_tiling(const Plan& p, int V, bool has_col_reduction) {
     return t;
 }
 
-// Workspace layout of the 2-D pullback (all offsets in bytes, 256-aligned).
+// Workspace (global, fp64 tile partials + tickets) and dynamic shared memory
+// of the 2-D pullback. Offsets are sized for every argument of a class, so a
+// workspace queried once serves any subset of wanted adjoints.
 struct PullLayout {
     int n_row_args = 0, n_col_args = 0, n_scalar_args = 0;
     size_t ws_row = 0, ws_col = 0, ws_scalar = 0, counters = 0, total = 0;
@@ -181,6 +212,11 @@ struct PullLayout {
 };
 
 inline size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
+
+inline size_t pull_smem_bytes(int n_col, int n_row, int n_scal, const Tiling& t) {
+    const int wpr = t.txv > 32 ? t.txv / 32 : 1;
+    return 8 * (size_t(n_col) * kThreads * t.V + size_t(n_row) * t.rpt * t.ty * wpr + size_t(n_scal) * kThreads);
+}
 
 inline PullLayout pull_layout(const Plan& p, const Tiling& t) {
     PullLayout L;
@@ -199,7 +235,7 @@ inline PullLayout pull_layout(const Plan& p, const Tiling& t) {
     L.counters = off;
     off += align256(size_t(t.n_row_tiles + t.n_col_tiles + 1) * 4);
     L.total = off;
-    L.smem = size_t(L.n_col_args) * kThreads * t.V * 8 + size_t(L.n_scalar_args) * kThreads * 8;
+    L.smem = pull_smem_bytes(L.n_col_args, L.n_row_args, L.n_scalar_args, t);
     return L;
 }
 
@@ -212,18 +248,14 @@ template <class T>
 bool pull_vec_shape_ok(const Plan& plan) {
     constexpr int V = vec_width<T>();
     if (!plan.is2d || plan.cols % V != 0) return false;
-    const Tiling t = choose_tiling(plan, V, true);
-    return pull_layout(plan, t).smem <= kMaxPullSmem;
+    return pull_layout(plan, choose_tiling(plan, V, class_mix(plan))).smem <= kMaxPullSmem;
 }
 
 template <class T>
 size_t pull_ws_t(const Plan& plan) {
     constexpr int V = vec_width<T>();
     if (!pull_vec_shape_ok<T>(plan)) return 256;
-    bool has_col = false;
-    for (int j = 0; j < plan.n; ++j) has_col |= plan.cls[j] == kCol;
-    return pull_layout(plan, choose_tiling(plan, V, has_col)).total;
+    return pull_layout(plan, choose_tiling(plan, V, class_mix(plan))).total;
 }
-
 
 }  // namespace bcad_cu_impl

@@ -3,8 +3,8 @@
 #include "launch.cuh"
 
 static const bcad_cu_kernel_entry kEntries[] = {
-    BCAD_ENTRY(bcad_dev::KHmlstm),
-    BCAD_ENTRY(bcad_dev::KHmlstmBias),
+    BCAD_ENTRY(bcad_dev::KHmlstm, bcad_cu_impl::SigHmlstmCanonical, bcad_cu_impl::SigHmlstmDivergence),
+    BCAD_ENTRY(bcad_dev::KHmlstmBias, bcad_cu_impl::SigHmlstmBias),
 };
 
 int bcad_reg_hmlstm(const bcad_cu_kernel_entry** out) {
