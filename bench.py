@@ -379,35 +379,31 @@ def run_native(args, w: Workload, rank: int, world: int):
 
 
 def run_e2e(case: Case, stream, steps: int, device):
-    """Host buffers in, host gradients out, every step: pinned H2D of the
-    inputs and the seed, K1, K2, D2H of every input gradient."""
+    """The user-facing call with HOST buffers (include/bcad_host.h ->
+    C++ Tape + mixed_broadcast + backward over libbcad_cu.so), every step:
+    pinned H2D of the inputs and the seed, K1, K2, D2H of every input
+    gradient, stream-synchronised return. Wall-clock per call."""
+    import numpy as np
     import torch
+    from paper_1810_08297_b200.host import HostStep
     host_in = [t.cpu().pin_memory() for t in case.ins]
     host_seed = case.seed.cpu().pin_memory()
     host_grad = [torch.empty(t.shape, dtype=t.dtype).pin_memory() for t in case.adj]
-    h2d = sum(t.numel() * t.element_size() for t in host_in) + host_seed.numel() * host_seed.element_size()
-    d2h = sum(t.numel() * t.element_size() for t in host_grad)
-    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    sp = int(stream.cuda_stream)
-
-    def go():
-        for d, h in zip(case.ins, host_in):
-            d.copy_(h, non_blocking=True)
-        case.seed.copy_(host_seed, non_blocking=True)
-        case.step.forward(sp)
-        case.step.pullback(sp)
-        for h, d in zip(host_grad, case.adj):
-            h.copy_(d, non_blocking=True)
-
-    with torch.cuda.stream(stream):
-        go()
-        torch.cuda.synchronize(device)
-        start.record(stream)
-        for _ in range(steps):
-            go()
-        end.record(stream)
+    np_in = [t.numpy() for t in host_in]
+    np_grad = [t.numpy() for t in host_grad]
+    call = HostStep(case.w.kernel, np_in, [host_seed.numpy()], grads_out=np_grad, policy=case.policy,
+                    stream=int(stream.cuda_stream))
+    h2d = sum(a.nbytes for a in np_in) + host_seed.numpy().nbytes
+    d2h = sum(a.nbytes for a in np_grad)
+    for _ in range(2):
+        call()
     torch.cuda.synchronize(device)
-    return {"ms_per_step": start.elapsed_time(end) / steps, "h2d": h2d, "d2h": d2h}
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        call()
+    ms = (time.perf_counter() - t0) * 1e3 / steps
+    del np
+    return {"ms_per_step": ms, "h2d": h2d, "d2h": d2h}
 
 
 def measure_secondary(w: Workload, device, stream, steps: int, policy: int):

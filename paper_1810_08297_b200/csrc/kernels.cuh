@@ -161,8 +161,10 @@ struct Fwd2DParams {
 };
 
 // K1. kReal: evaluate the real body (primal only). Otherwise the dual body,
-// storing whichever of primal / partials pointers are non-null.
-template <class Body, class T, int V, bool kReal, class S>
+// storing whichever of primal / partials pointers are non-null (kDense: all
+// of them, no checks). The next row's loads are issued before the current
+// row is evaluated, so every thread keeps two rows of loads in flight.
+template <class Body, class T, int V, bool kReal, class S, bool kDense>
 __global__ void __launch_bounds__(kThreads) fwd2d_kernel(const __grid_constant__ Fwd2DParams<Body::kIn, Body::kOut, T> p) {
     constexpr int N = Body::kIn, M = Body::kOut;
     pdl_wait();
@@ -185,12 +187,8 @@ __global__ void __launch_bounds__(kThreads) fwd2d_kernel(const __grid_constant__
             for (int v = 0; v < V; ++v) xc[j].x[v] = v0;
         }
     }
-    const int64_t r0 = int64_t(blockIdx.y) * p.tile_rows + ty;
-    for (int k = 0; k < p.rpt; ++k) {
-        const int64_t r = r0 + int64_t(k) * p.ty;
-        if (r >= p.rows) break;
+    auto load_row = [&](int64_t r, Pack<T, V>* x) {
         const int64_t off = r * p.cols + c0;
-        Pack<T, V> x[N];
 #pragma unroll
         for (int j = 0; j < N; ++j) {
             const int cls = arg_class<S>(p.cls, j);
@@ -204,6 +202,17 @@ __global__ void __launch_bounds__(kThreads) fwd2d_kernel(const __grid_constant__
                 x[j] = xc[j];
             }
         }
+    };
+    int64_t r = int64_t(blockIdx.y) * p.tile_rows + ty;
+    if (r >= p.rows) return;
+    Pack<T, V> x[N];
+    load_row(r, x);
+    for (int k = 0; k < p.rpt; ++k) {
+        const int64_t rn = r + p.ty;
+        const bool has_next = k + 1 < p.rpt && rn < p.rows;
+        Pack<T, V> xn[N];
+        if (has_next) load_row(rn, xn);
+        const int64_t off = r * p.cols + c0;
         if constexpr (kReal) {
             Pack<T, V> y[M];
 #pragma unroll
@@ -217,7 +226,7 @@ __global__ void __launch_bounds__(kThreads) fwd2d_kernel(const __grid_constant__
             }
 #pragma unroll
             for (int i = 0; i < M; ++i)
-                if (p.primal[i]) st_vec<T, V>(p.primal[i] + off, y[i]);
+                if (kDense || p.primal[i]) st_vec<T, V>(p.primal[i] + off, y[i]);
         } else {
             Pack<T, V> y[M];
             Pack<T, V> d[M * N];
@@ -240,12 +249,16 @@ __global__ void __launch_bounds__(kThreads) fwd2d_kernel(const __grid_constant__
             }
 #pragma unroll
             for (int i = 0; i < M; ++i) {
-                if (p.primal[i]) st_vec<T, V>(p.primal[i] + off, y[i]);
+                if (kDense || p.primal[i]) st_vec<T, V>(p.primal[i] + off, y[i]);
 #pragma unroll
                 for (int j = 0; j < N; ++j)
-                    if (p.partials[i * N + j]) st_vec<T, V>(p.partials[i * N + j] + off, d[i * N + j]);
+                    if (kDense || p.partials[i * N + j]) st_vec<T, V>(p.partials[i * N + j] + off, d[i * N + j]);
             }
         }
+        if (!has_next) break;
+#pragma unroll
+        for (int j = 0; j < N; ++j) x[j] = xn[j];
+        r = rn;
     }
 }
 
@@ -289,7 +302,7 @@ __host__ __device__ inline size_t pull_smem_doubles(int n_col, int n_row, int n_
 // K2: terms w_i * D_ij rounded to T exactly like backprop_diag's tensor_zip
 // (mixed.hpp:34-38); FULL slots get the reference's element arithmetic,
 // reduced slots an fp64 sum of those terms in a fixed order.
-template <class Body, class T, int V, bool kRecompute, class S>
+template <class Body, class T, int V, bool kRecompute, class S, bool kDense>
 __global__ void __launch_bounds__(kThreads) pull2d_kernel(const __grid_constant__ Pull2DParams<Body::kIn, Body::kOut, T> p) {
     constexpr int N = Body::kIn, M = Body::kOut;
     constexpr bool kAnyRow = !S::kStatic || S::has(kRow);
@@ -335,41 +348,58 @@ __global__ void __launch_bounds__(kThreads) pull2d_kernel(const __grid_constant_
             }
         }
     }
+    // One row's streamed operands: the output adjoints w_i and either the
+    // cached partials D_ij or (recompute) the inputs x_j.
+    constexpr int kStreams = kRecompute ? N : M * N;
+    auto load_row = [&](int64_t r, Pack<T, V>* w, Pack<T, V>* q) {
+        const int64_t off = r * p.cols + c0;
+#pragma unroll
+        for (int i = 0; i < M; ++i)
+            if (kDense || p.w[i]) w[i] = ld_stream<T, V>(p.w[i] + off);
+        if constexpr (kRecompute) {
+#pragma unroll
+            for (int j = 0; j < N; ++j) {
+                const int cls = arg_class<S>(p.cls, j);
+                if (cls == kFull) {
+                    q[j] = ld_stream<T, V>(p.in[j] + off);
+                } else if (cls == kRow) {
+                    const T v0 = __ldg(p.in[j] + r);
+#pragma unroll
+                    for (int v = 0; v < V; ++v) q[j].x[v] = v0;
+                } else {
+                    q[j] = xc[j];
+                }
+            }
+        } else {
+#pragma unroll
+            for (int i = 0; i < M; ++i)
+#pragma unroll
+                for (int j = 0; j < N; ++j)
+                    if (kDense || (p.w[i] && p.adj[j])) q[i * N + j] = ld_stream<T, V>(p.D[i * N + j] + off);
+        }
+    };
 
-    const int64_t r0 = int64_t(rt) * p.tile_rows + ty;
+    int64_t r = int64_t(rt) * p.tile_rows + ty;
+    bool live = active && r < p.rows;
+    Pack<T, V> w[M], q[kStreams];
+    if (live) load_row(r, w, q);
     // Every lane runs the same rpt iterations (rows past the end are masked),
     // so the ROW shuffles always see complete lane groups.
     for (int k = 0; k < p.rpt; ++k) {
-        const int64_t r = r0 + int64_t(k) * p.ty;
-        const bool live = active && r < p.rows;
+        const int64_t rn = r + p.ty;
+        const bool live_n = active && k + 1 < p.rpt && rn < p.rows;
+        Pack<T, V> wn[M], qn[kStreams];
+        if (live_n) load_row(rn, wn, qn);
         const int64_t off = r * p.cols + c0;
-        Pack<T, V> w[M];
         Pack<T, V> D[M * N];
-        if (live) {
-#pragma unroll
-            for (int i = 0; i < M; ++i)
-                if (p.w[i]) w[i] = ld_stream<T, V>(p.w[i] + off);
-            if constexpr (kRecompute) {
-                Pack<T, V> x[N];
-#pragma unroll
-                for (int j = 0; j < N; ++j) {
-                    const int cls = arg_class<S>(p.cls, j);
-                    if (cls == kFull) {
-                        x[j] = ld_stream<T, V>(p.in[j] + off);
-                    } else if (cls == kRow) {
-                        const T v0 = __ldg(p.in[j] + r);
-#pragma unroll
-                        for (int v = 0; v < V; ++v) x[j].x[v] = v0;
-                    } else {
-                        x[j] = xc[j];
-                    }
-                }
+        if constexpr (kRecompute) {
+            if (live) {
 #pragma unroll
                 for (int v = 0; v < V; ++v) {
                     Dual<T, N> xi[N], yo[M];
 #pragma unroll
                     for (int j = 0; j < N; ++j) {
-                        xi[j] = Dual<T, N>(x[j].x[v]);
+                        xi[j] = Dual<T, N>(q[j].x[v]);
                         xi[j].d[j] = T(1);
                     }
                     Body::template body<Dual<T, N>>(xi, yo);
@@ -379,19 +409,16 @@ __global__ void __launch_bounds__(kThreads) pull2d_kernel(const __grid_constant_
 #pragma unroll
                         for (int j = 0; j < N; ++j) D[i * N + j].x[v] = yo[i].d[j];
                 }
-            } else {
-#pragma unroll
-                for (int i = 0; i < M; ++i)
-#pragma unroll
-                    for (int j = 0; j < N; ++j)
-                        if (p.w[i] && p.adj[j]) D[i * N + j] = ld_stream<T, V>(p.D[i * N + j] + off);
             }
+        } else {
+#pragma unroll
+            for (int t = 0; t < M * N; ++t) D[t] = q[t];
         }
 #pragma unroll
         for (int j = 0; j < N; ++j) {
-            if (!p.adj[j]) continue;
+            if (!kDense && !p.adj[j]) continue;
             const int cls = arg_class<S>(p.cls, j);
-            const bool acc = (p.acc_mask >> j) & 1u;
+            const bool acc = !kDense && ((p.acc_mask >> j) & 1u);
             if (cls == kFull) {
                 if (!live) continue;
                 T* dst = p.adj[j] + off;
@@ -402,7 +429,7 @@ __global__ void __launch_bounds__(kThreads) pull2d_kernel(const __grid_constant_
                     T a = acc ? out.x[v] : T(0);
 #pragma unroll
                     for (int i = 0; i < M; ++i)
-                        if (p.w[i]) a = a + w[i].x[v] * D[i * N + j].x[v];
+                        if (kDense || p.w[i]) a = a + w[i].x[v] * D[i * N + j].x[v];
                     out.x[v] = a;
                 }
                 st_vec<T, V>(dst, out);
@@ -416,7 +443,7 @@ __global__ void __launch_bounds__(kThreads) pull2d_kernel(const __grid_constant_
                 if (live)
 #pragma unroll
                     for (int i = 0; i < M; ++i)
-                        if (p.w[i]) s[v] += double(T(w[i].x[v] * D[i * N + j].x[v]));
+                        if (kDense || p.w[i]) s[v] += double(T(w[i].x[v] * D[i * N + j].x[v]));
             }
             if (cls == kCol) {
                 if constexpr (kAnyCol) {
@@ -440,6 +467,12 @@ __global__ void __launch_bounds__(kThreads) pull2d_kernel(const __grid_constant_
                     row_acc[(size_t(p.slot[j]) * trows + k * p.ty + ty) * wpr + wir] = t;
             }
         }
+#pragma unroll
+        for (int i = 0; i < M; ++i) w[i] = wn[i];
+#pragma unroll
+        for (int t = 0; t < kStreams; ++t) q[t] = qn[t];
+        r = rn;
+        live = live_n;
     }
     if constexpr (!kAnyRow && !kAnyCol && !kAnyScal) return;
     else {

@@ -111,9 +111,20 @@ int launch_fwd_t(const FwdArgs& a, std::string* err) {
         p.tile_rows = t.tile_rows;
         p.err = a.err;
         const dim3 grid(unsigned(t.n_col_tiles), unsigned(t.n_row_tiles));
+        bool dense = true;  // every output pointer present: no per-store checks
+        for (int i = 0; i < M; ++i) {
+            dense = dense && p.primal[i];
+            for (int j = 0; j < N && !real; ++j) dense = dense && p.partials[i * N + j];
+        }
         return with_sig<Sigs...>(plan, [&](auto sig) {
             using S = decltype(sig);
-            auto kern = real ? &bcad_dev::fwd2d_kernel<Body, T, V, true, S> : &bcad_dev::fwd2d_kernel<Body, T, V, false, S>;
+            void (*kern)(bcad_dev::Fwd2DParams<N, M, T>);
+            if constexpr (S::kStatic) {
+                if (dense) kern = real ? &bcad_dev::fwd2d_kernel<Body, T, V, true, S, true> : &bcad_dev::fwd2d_kernel<Body, T, V, false, S, true>;
+                else kern = real ? &bcad_dev::fwd2d_kernel<Body, T, V, true, S, false> : &bcad_dev::fwd2d_kernel<Body, T, V, false, S, false>;
+            } else {
+                kern = real ? &bcad_dev::fwd2d_kernel<Body, T, V, true, S, false> : &bcad_dev::fwd2d_kernel<Body, T, V, false, S, false>;
+            }
             return cuda_status(launch_pdl(kern, grid, 0, a.stream, p), err);
         });
     }
@@ -193,9 +204,18 @@ int launch_pull_t(const PullArgs& a, std::string* err) {
         p.err = a.err;
         const size_t smem = pull_smem_bytes(nc, nr, ns, t);
         const dim3 grid(unsigned(t.n_col_tiles), unsigned(t.n_row_tiles));
+        bool dense = p.acc_mask == 0;  // every w and adjoint present, nothing accumulated
+        for (int i = 0; i < M; ++i) dense = dense && p.w[i];
+        for (int j = 0; j < N; ++j) dense = dense && p.adj[j];
         return with_sig<Sigs...>(plan, [&](auto sig) {
             using S = decltype(sig);
-            auto kern = recompute ? &bcad_dev::pull2d_kernel<Body, T, V, true, S> : &bcad_dev::pull2d_kernel<Body, T, V, false, S>;
+            void (*kern)(bcad_dev::Pull2DParams<N, M, T>);
+            if constexpr (S::kStatic) {
+                if (dense) kern = recompute ? &bcad_dev::pull2d_kernel<Body, T, V, true, S, true> : &bcad_dev::pull2d_kernel<Body, T, V, false, S, true>;
+                else kern = recompute ? &bcad_dev::pull2d_kernel<Body, T, V, true, S, false> : &bcad_dev::pull2d_kernel<Body, T, V, false, S, false>;
+            } else {
+                kern = recompute ? &bcad_dev::pull2d_kernel<Body, T, V, true, S, false> : &bcad_dev::pull2d_kernel<Body, T, V, false, S, false>;
+            }
             if (smem > 48 * 1024) {
                 const cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
                 if (e != cudaSuccess) return cuda_status(e, err);

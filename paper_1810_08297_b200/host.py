@@ -1,0 +1,56 @@
+"""ctypes binding of the end-to-end host call (include/bcad_host.h,
+libbcad_host.so): numpy host buffers in, host gradients out, one reference
+step (Tape + mixed_broadcast + backward) through the C++ drop-in API."""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+from . import native
+
+HOST_LIB_PATH = os.path.join(native.PKG, "libbcad_host.so")
+
+
+def _load():
+    if not os.path.exists(HOST_LIB_PATH):
+        raise ImportError(f"{HOST_LIB_PATH} is not built (run __graft_entry__.build())")
+    lib = C.CDLL(HOST_LIB_PATH)
+    lib.bcad_host_last_error.restype = C.c_char_p
+    lib.bcad_host_mixed_step.restype = C.c_int
+    lib.bcad_host_mixed_step.argtypes = [C.c_char_p, C.c_int, C.c_int, C.c_void_p, C.c_void_p, C.c_int, C.c_int,
+                                         C.c_void_p, C.c_void_p, C.c_void_p, C.POINTER(C.c_int64), C.c_void_p]
+    return lib
+
+
+LIB = _load()
+
+
+def _ptrs(arrs):
+    return (C.c_void_p * max(1, len(arrs)))(*[None if a is None else a.ctypes.data for a in arrs])
+
+
+class HostStep:
+    """A reusable call: fixed host buffers (ideally pinned), one
+    bcad_host_mixed_step per __call__."""
+
+    def __init__(self, kernel: str, inputs, seeds, primal_out=None, grads_out=None, policy: int = 0, stream=None):
+        self.kernel = kernel.encode()
+        self.dt = 0 if inputs[0].dtype == np.float32 else 1
+        self.n, self.m = len(inputs), len(seeds)
+        self.shapes = (native.Shape * self.n)(*[native.Shape.of(a.shape) for a in inputs])
+        self.ins, self.seeds = _ptrs(inputs), _ptrs(seeds)
+        self.prim = _ptrs(primal_out) if primal_out is not None else None
+        self.grads = _ptrs(grads_out) if grads_out is not None else None
+        self.policy = policy
+        self.stream = stream
+        self.peak = C.c_int64()
+        self._keep = (inputs, seeds, primal_out, grads_out)
+
+    def __call__(self) -> int:
+        rc = LIB.bcad_host_mixed_step(self.kernel, self.dt, self.n, self.ins, self.shapes, self.m, self.policy,
+                                      self.seeds, self.prim, self.grads, C.byref(self.peak), self.stream)
+        if rc:
+            raise native._BY_CODE.get(rc, native.Error)(LIB.bcad_host_last_error().decode())
+        return int(self.peak.value)
