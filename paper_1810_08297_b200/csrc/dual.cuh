@@ -97,48 +97,83 @@ BCAD_HD double pow(float x, double c) { return ::pow(double(x), c); }
 BCAD_HD double pow(double x, double c) { return ::pow(x, c); }
 
 // ------------------------------------------------------------ duals
+// Structural sparsity. Each dual carries `nz`, a bit per partial slot that
+// may be nonzero; a seeded input x_j has only bit j. Every rule below skips
+// the terms whose operand slot is a structural zero. Because the seeds are
+// compile-time constants once the body is inlined, the masks are integer
+// constants the compiler folds away: a product of two seeded duals costs two
+// multiplies instead of 3N flops. On every finite operand the nonzero
+// partials are bit-identical to the reference's dense rule (x + 0 == x and
+// x - 0 == x exactly, and the skipped products are of an exact zero); only
+// the sign of a zero partial and NaN propagation out of a non-finite primal
+// into structurally-zero slots can differ. kDenseDuals = true restores the
+// dense evaluation (every slot computed) for A/B checks.
+#ifndef BCAD_DENSE_DUALS
+#define BCAD_DENSE_DUALS 0
+#endif
+constexpr bool kDenseDuals = BCAD_DENSE_DUALS != 0;
+
 template <class T, int N>
 struct Dual {
     T v;
     T d[N];
+    uint32_t nz;
 
     Dual() = default;
-    BCAD_HD Dual(T x) : v(x) {  // NOLINT constant embedding (dual.hpp:78)
+    BCAD_HD Dual(T x) : v(x), nz(kDenseDuals ? ~0u : 0u) {  // NOLINT constant embedding (dual.hpp:78)
 #pragma unroll
         for (int k = 0; k < N; ++k) d[k] = T(0);
     }
+    // x_j + e_j (forward.hpp:121-126)
+    BCAD_HD static Dual seeded(T x, int j) {
+        Dual r(x);
+        r.d[j] = T(1);
+        r.nz = kDenseDuals ? ~0u : (1u << j);
+        return r;
+    }
+    BCAD_HD bool has(int k) const { return (nz >> k) & 1u; }
 };
 
 template <class T, int N>
 BCAD_HD Dual<T, N> operator-(const Dual<T, N>& a) {
     Dual<T, N> r;
     r.v = -a.v;
+    r.nz = a.nz;
 #pragma unroll
-    for (int k = 0; k < N; ++k) r.d[k] = -a.d[k];
+    for (int k = 0; k < N; ++k) r.d[k] = a.has(k) ? -a.d[k] : T(0);
     return r;
 }
 template <class T, int N>
 BCAD_HD Dual<T, N> operator+(const Dual<T, N>& a, const Dual<T, N>& b) {  // dual.hpp:107-112
     Dual<T, N> r;
     r.v = a.v + b.v;
+    r.nz = a.nz | b.nz;
 #pragma unroll
-    for (int k = 0; k < N; ++k) r.d[k] = a.d[k] + b.d[k];
+    for (int k = 0; k < N; ++k)
+        r.d[k] = a.has(k) && b.has(k) ? a.d[k] + b.d[k] : a.has(k) ? a.d[k] : b.has(k) ? b.d[k] : T(0);
     return r;
 }
 template <class T, int N>
 BCAD_HD Dual<T, N> operator-(const Dual<T, N>& a, const Dual<T, N>& b) {  // dual.hpp:114-119
     Dual<T, N> r;
     r.v = a.v - b.v;
+    r.nz = a.nz | b.nz;
 #pragma unroll
-    for (int k = 0; k < N; ++k) r.d[k] = a.d[k] - b.d[k];
+    for (int k = 0; k < N; ++k)
+        r.d[k] = a.has(k) && b.has(k) ? a.d[k] - b.d[k] : a.has(k) ? a.d[k] : b.has(k) ? -b.d[k] : T(0);
     return r;
 }
 template <class T, int N>
 BCAD_HD Dual<T, N> operator*(const Dual<T, N>& a, const Dual<T, N>& b) {  // dual.hpp:121-127
     Dual<T, N> r;
     r.v = a.v * b.v;
+    r.nz = a.nz | b.nz;
 #pragma unroll
-    for (int k = 0; k < N; ++k) r.d[k] = a.d[k] * b.v + a.v * b.d[k];
+    for (int k = 0; k < N; ++k)
+        r.d[k] = a.has(k) && b.has(k) ? a.d[k] * b.v + a.v * b.d[k]
+                 : a.has(k)            ? a.d[k] * b.v
+                 : b.has(k)            ? a.v * b.d[k]
+                                       : T(0);
     return r;
 }
 template <class T, int N>
@@ -146,9 +181,14 @@ BCAD_HD Dual<T, N> operator/(const Dual<T, N>& a, const Dual<T, N>& b) {  // dua
     if (b.v == T(0)) raise_status(kDevDivisionByZero);
     Dual<T, N> r;
     r.v = a.v / b.v;
+    r.nz = a.nz | b.nz;
     const T denom = b.v * b.v;
 #pragma unroll
-    for (int k = 0; k < N; ++k) r.d[k] = (a.d[k] * b.v - a.v * b.d[k]) / denom;
+    for (int k = 0; k < N; ++k)
+        r.d[k] = a.has(k) && b.has(k) ? (a.d[k] * b.v - a.v * b.d[k]) / denom
+                 : a.has(k)            ? (a.d[k] * b.v) / denom
+                 : b.has(k)            ? (-(a.v * b.d[k])) / denom
+                                       : T(0);
     return r;
 }
 
@@ -163,8 +203,9 @@ template <class T, int N>
 BCAD_HD Dual<T, N> scaled(const Dual<T, N>& a, T s) {
     Dual<T, N> r;
     r.v = a.v * s;
+    r.nz = a.nz;
 #pragma unroll
-    for (int k = 0; k < N; ++k) r.d[k] = a.d[k] * s;
+    for (int k = 0; k < N; ++k) r.d[k] = a.has(k) ? a.d[k] * s : T(0);
     return r;
 }
 template <class T, int N> BCAD_HD Dual<T, N> operator+(const Dual<T, N>& a, double s) { return shifted(a, T(s)); }
@@ -185,9 +226,10 @@ BCAD_HD Dual<T, N> operator/(double s, const Dual<T, N>& b) {
     const T rs = T(s);
     Dual<T, N> r;
     r.v = rs / b.v;
+    r.nz = b.nz;
     const T scale = -rs / (b.v * b.v);
 #pragma unroll
-    for (int k = 0; k < N; ++k) r.d[k] = scale * b.d[k];
+    for (int k = 0; k < N; ++k) r.d[k] = b.has(k) ? scale * b.d[k] : T(0);
     return r;
 }
 
@@ -211,8 +253,9 @@ template <class T, int N>
 BCAD_HD Dual<T, N> chain(const Dual<T, N>& a, T p, T scale) {
     Dual<T, N> r;
     r.v = p;
+    r.nz = a.nz;
 #pragma unroll
-    for (int k = 0; k < N; ++k) r.d[k] = scale * a.d[k];
+    for (int k = 0; k < N; ++k) r.d[k] = a.has(k) ? scale * a.d[k] : T(0);
     return r;
 }
 

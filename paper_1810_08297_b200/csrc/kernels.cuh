@@ -32,6 +32,7 @@ using bcad_cu_impl::kMaxRank;
 using bcad_cu_impl::kRow;
 using bcad_cu_impl::kScalar;
 using bcad_cu_impl::kThreads;
+using bcad_cu_impl::kCtasPerSm;
 
 // ----------------------------------------------------------- vector I/O
 template <class T, int V> struct alignas(sizeof(T) * V) Pack { T x[V]; };
@@ -132,6 +133,19 @@ struct Sig {
     }
 };
 
+// Index of argument j among the arguments of its class: compile-time for a
+// static signature when every adjoint is wanted (kDense), else from params.
+template <class S, bool kDense>
+__device__ __forceinline__ int arg_slot(const int* dyn, int j) {
+    if constexpr (S::kStatic && kDense) {
+        int n = 0;
+        for (int l = 0; l < j; ++l) n += S::cls(l) == S::cls(j);
+        return n;
+    } else {
+        return dyn[j];
+    }
+}
+
 template <class S>
 __device__ __forceinline__ int arg_class(const int* dyn, int j) {
     if constexpr (S::kStatic) return S::cls(j);
@@ -165,7 +179,7 @@ struct Fwd2DParams {
 // of them, no checks). The next row's loads are issued before the current
 // row is evaluated, so every thread keeps two rows of loads in flight.
 template <class Body, class T, int V, bool kReal, class S, bool kDense>
-__global__ void __launch_bounds__(kThreads) fwd2d_kernel(const __grid_constant__ Fwd2DParams<Body::kIn, Body::kOut, T> p) {
+__global__ void __launch_bounds__(kThreads, kCtasPerSm) fwd2d_kernel(const __grid_constant__ Fwd2DParams<Body::kIn, Body::kOut, T> p) {
     constexpr int N = Body::kIn, M = Body::kOut;
     pdl_wait();
     pdl_trigger();
@@ -235,8 +249,7 @@ __global__ void __launch_bounds__(kThreads) fwd2d_kernel(const __grid_constant__
                 Dual<T, N> xi[N], yo[M];
 #pragma unroll
                 for (int j = 0; j < N; ++j) {  // seed x_j + e_j (forward.hpp:121-126)
-                    xi[j] = Dual<T, N>(x[j].x[v]);
-                    xi[j].d[j] = T(1);
+                    xi[j] = Dual<T, N>::seeded(x[j].x[v], j);
                 }
                 Body::template body<Dual<T, N>>(xi, yo);
                 if constexpr (Body::kMayRaise) report_error(p.err, off + v);
@@ -325,6 +338,7 @@ __global__ void __launch_bounds__(kThreads) pull2d_kernel(const __grid_constant_
     const bool active = vc < p.vcols;
     const int64_t c0 = int64_t(vc) * V;
     const int trows = p.rpt * p.ty;                  // rows of this tile
+    const int row_base = ty * wpr + wir;             // this thread's row_acc column
 
     double* col_acc = smem;
     double* row_acc = col_acc + size_t(p.n_col_args) * kThreads * V;
@@ -399,8 +413,7 @@ __global__ void __launch_bounds__(kThreads) pull2d_kernel(const __grid_constant_
                     Dual<T, N> xi[N], yo[M];
 #pragma unroll
                     for (int j = 0; j < N; ++j) {
-                        xi[j] = Dual<T, N>(q[j].x[v]);
-                        xi[j].d[j] = T(1);
+                        xi[j] = Dual<T, N>::seeded(q[j].x[v], j);
                     }
                     Body::template body<Dual<T, N>>(xi, yo);
                     if constexpr (Body::kMayRaise) report_error(p.err, off + v);
@@ -447,7 +460,7 @@ __global__ void __launch_bounds__(kThreads) pull2d_kernel(const __grid_constant_
             }
             if (cls == kCol) {
                 if constexpr (kAnyCol) {
-                    double* ca = col_acc + (size_t(p.slot[j]) * kThreads + tid) * V;
+                    double* ca = col_acc + (size_t(arg_slot<S, kDense>(p.slot, j)) * kThreads + tid) * V;
 #pragma unroll
                     for (int v = 0; v < V; ++v) ca[v] += s[v];
                 }
@@ -456,15 +469,19 @@ __global__ void __launch_bounds__(kThreads) pull2d_kernel(const __grid_constant_
                     double t = 0.0;
 #pragma unroll
                     for (int v = 0; v < V; ++v) t += s[v];
-                    scal_acc[p.slot[j] * kThreads + tid] += t;
+                    scal_acc[arg_slot<S, kDense>(p.slot, j) * kThreads + tid] += t;
                 }
             } else if constexpr (kAnyRow) {  // kRow: lanes of this row in this warp
                 double t = 0.0;
 #pragma unroll
                 for (int v = 0; v < V; ++v) t += s[v];
-                for (int o = lanes >> 1; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o, lanes);
+                // xor offsets below `lanes` stay inside the row's aligned lane
+                // group; unrolled with a warp-uniform predicate (no loop)
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1)
+                    if (o < lanes) t += __shfl_xor_sync(0xffffffffu, t, o);
                 if ((tid & (lanes - 1)) == 0)
-                    row_acc[(size_t(p.slot[j]) * trows + k * p.ty + ty) * wpr + wir] = t;
+                    row_acc[(arg_slot<S, kDense>(p.slot, j) * trows + k * p.ty) * wpr + row_base] = t;
             }
         }
 #pragma unroll
@@ -647,8 +664,7 @@ __global__ void __launch_bounds__(kThreads) fwd_generic_kernel(const __grid_cons
             Dual<T, N> xi[N], yo[M];
 #pragma unroll
             for (int j = 0; j < N; ++j) {
-                xi[j] = Dual<T, N>(p.in[j][off[j]]);
-                xi[j].d[j] = T(1);
+                xi[j] = Dual<T, N>::seeded(p.in[j][off[j]], j);
             }
             Body::template body<Dual<T, N>>(xi, yo);
             if constexpr (Body::kMayRaise) report_error(p.err, cell);
@@ -711,8 +727,7 @@ __global__ void __launch_bounds__(kThreads) pull_generic_kernel(const __grid_con
                 Dual<T, N> xi[N], yo[M];
 #pragma unroll
                 for (int jj = 0; jj < N; ++jj) {
-                    xi[jj] = Dual<T, N>(p.in[jj][off[jj]]);
-                    xi[jj].d[jj] = T(1);
+                    xi[jj] = Dual<T, N>::seeded(p.in[jj][off[jj]], jj);
                 }
                 Body::template body<Dual<T, N>>(xi, yo);
                 if constexpr (Body::kMayRaise) report_error(p.err, flat);
