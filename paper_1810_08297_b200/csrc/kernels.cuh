@@ -179,7 +179,7 @@ struct Fwd2DParams {
 // of them, no checks). The next row's loads are issued before the current
 // row is evaluated, so every thread keeps two rows of loads in flight.
 template <class Body, class T, int V, bool kReal, class S, bool kDense>
-__global__ void __launch_bounds__(kThreads, kCtasPerSm) fwd2d_kernel(const __grid_constant__ Fwd2DParams<Body::kIn, Body::kOut, T> p) {
+__global__ void __launch_bounds__(kThreads) fwd2d_kernel(const __grid_constant__ Fwd2DParams<Body::kIn, Body::kOut, T> p) {
     constexpr int N = Body::kIn, M = Body::kOut;
     pdl_wait();
     pdl_trigger();
