@@ -36,21 +36,26 @@ BCAD_HD S cell_update_scalar(S c, S f, S i, S g, S z1, S z2) {
     return sigmoid(i) * tanh(g);                                                // FLUSH
 }
 
-#define BCAD_BODY(NAME, STR, NIN, NOUT, RAISES, ...)                         \
+// kPredicateArgs: bit j set when argument j feeds a branch predicate of
+// the body (a comparison). The lane-vector evaluation (VDual) is used only
+// when all of them are uniform across a thread's V cells.
+#define BCAD_BODY_P(NAME, STR, NIN, NOUT, RAISES, PRED, ...)                 \
     struct NAME {                                                            \
         static constexpr const char* kName = STR;                            \
         static constexpr int kIn = NIN, kOut = NOUT;                         \
         static constexpr bool kMayRaise = RAISES;                            \
+        static constexpr uint32_t kPredicateArgs = PRED;                     \
         template <class S>                                                   \
         BCAD_HD static void body(const S* in, S* out) { __VA_ARGS__; }       \
     };
+#define BCAD_BODY(NAME, STR, NIN, NOUT, RAISES, ...) BCAD_BODY_P(NAME, STR, NIN, NOUT, RAISES, 0u, __VA_ARGS__)
 
-BCAD_BODY(KHmlstm, "hmlstm_update", 6, 1, false,
+BCAD_BODY_P(KHmlstm, "hmlstm_update", 6, 1, false, 0x30u,
           out[0] = cell_update_scalar(in[0], in[1], in[2], in[3], in[4], in[5]))
-BCAD_BODY(KHmlstmBias, "hmlstm_update_bias", 9, 1, false,
+BCAD_BODY_P(KHmlstmBias, "hmlstm_update_bias", 9, 1, false, 0x180u,
           out[0] = cell_update_scalar(in[0], in[1] + in[4], in[2] + in[5], in[3] + in[6], in[7], in[8]))
 BCAD_BODY(KIdentity, "identity", 1, 1, false, out[0] = in[0])
-BCAD_BODY(KReflect, "reflect", 1, 1, false, out[0] = reflect_below_half(in[0]))
+BCAD_BODY_P(KReflect, "reflect", 1, 1, false, 0x1u, out[0] = reflect_below_half(in[0]))
 BCAD_BODY(KTanhSigmoid, "tanh_sigmoid", 1, 1, false, out[0] = tanh(in[0]) * sigmoid(in[0]))
 BCAD_BODY(KProduct, "product", 2, 1, false, out[0] = in[0] * in[1])
 BCAD_BODY(KMul, "mul", 2, 1, false, out[0] = in[0] * in[1])
@@ -81,12 +86,13 @@ BCAD_BODY(KMinus, "minus", 2, 1, false, out[0] = in[0] - in[1])
 BCAD_BODY(KNeg, "neg", 1, 1, false, out[0] = -in[0])
 BCAD_BODY(KSigmoid, "sigmoid", 1, 1, false, out[0] = sigmoid(in[0]))
 BCAD_BODY(KTanh, "tanh", 1, 1, false, out[0] = tanh(in[0]))
-BCAD_BODY(KSelect, "select", 3, 1, false, out[0] = in[0] != 0.0 ? in[1] : in[2])
+BCAD_BODY_P(KSelect, "select", 3, 1, false, 0x1u, out[0] = in[0] != 0.0 ? in[1] : in[2])
 BCAD_BODY(KSigmoidBwd, "sigmoid_bwd", 2, 1, false, out[0] = in[0] * in[1] * (S(1.0) - in[1]))
 BCAD_BODY(KTanhBwd, "tanh_bwd", 2, 1, false, out[0] = in[0] * (S(1.0) - in[1] * in[1]))
-BCAD_BODY(KSelectTrueBwd, "select_true_bwd", 2, 1, false, out[0] = in[1] != 0.0 ? in[0] : S(0.0))
-BCAD_BODY(KSelectFalseBwd, "select_false_bwd", 2, 1, false, out[0] = in[1] != 0.0 ? S(0.0) : in[0])
+BCAD_BODY_P(KSelectTrueBwd, "select_true_bwd", 2, 1, false, 0x2u, out[0] = in[1] != 0.0 ? in[0] : S(0.0))
+BCAD_BODY_P(KSelectFalseBwd, "select_false_bwd", 2, 1, false, 0x2u, out[0] = in[1] != 0.0 ? S(0.0) : in[0])
 #undef BCAD_BODY
+#undef BCAD_BODY_P
 
 template <int A>
 struct KTanhProduct {  // arity_workload.hpp:19-28
@@ -96,6 +102,7 @@ struct KTanhProduct {  // arity_workload.hpp:19-28
       : A == 32 ? "tanh_product_32" : "tanh_product_?";
     static constexpr int kIn = A, kOut = 1;
     static constexpr bool kMayRaise = false;
+    static constexpr uint32_t kPredicateArgs = A >= 32 ? ~0u : (1u << A) - 1u;  // reflect_below_half on every arg
     template <class S>
     BCAD_HD static void body(const S* in, S* out) {
         S acc = tanh(reflect_below_half(in[0]));

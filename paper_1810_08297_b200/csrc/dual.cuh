@@ -63,14 +63,15 @@ BCAD_HD double d_pow(double x, double c) { return ::pow(x, c); }
 BCAD_HD float d_floor(float x) { return ::floorf(x); }
 BCAD_HD double d_floor(double x) { return ::floor(x); }
 
+// Branch-free form of the same arithmetic: x >= 0 gives e = exp(-x) and
+// 1 / (1 + e); x < 0 gives e = exp(x) and e / (1 + e) — one exp and one
+// correctly rounded division either way, so the result is bit-identical to
+// the two-branch source while lanes never diverge.
 template <class F>
 BCAD_HD F raw_sigmoid(F x) {
-    if (x >= F(0)) {
-        const F e = d_exp(-x);
-        return F(1) / (F(1) + e);
-    }
-    const F e = d_exp(x);
-    return e / (F(1) + e);
+    const bool pos = x >= F(0);
+    const F e = d_exp(pos ? -x : x);
+    return (pos ? F(1) : e) / (F(1) + e);
 }
 
 // Real-body primitives (dual.hpp:55-63): what the generic kernel bodies call
@@ -297,5 +298,218 @@ template <class T, int N> BCAD_HD Dual<T, N> pow(const Dual<T, N>& a, double exp
 // Scalar selector used by kernel bodies that need the arithmetic type.
 template <class S> struct scalar_of { using type = S; };
 template <class T, int N> struct scalar_of<Dual<T, N>> { using type = T; };
+
+// ------------------------------------------------------- lane-vector duals
+// VDual<T, N, V>: the V cells one thread owns (its 128-bit vector), evaluated
+// together. Every rule is the Dual rule applied lane by lane, in the same
+// operation order, so each lane's result is bit-identical to evaluating that
+// cell alone. The point is control flow: a body's branch is taken ONCE for
+// all V lanes and their arithmetic interleaves (ILP V instead of V serial
+// branch regions). Comparisons read lane 0, so a VDual evaluation is only
+// valid when every branch predicate of the body depends on arguments that
+// are uniform across the V lanes (ROW / SCALAR stride class). The kernels use
+// it only under such a signature (Body::kPredicateArgs).
+template <class T, int N, int V>
+struct VDual {
+    T v[V];
+    T d[N][V];
+    uint32_t nz;
+
+    VDual() = default;
+    BCAD_HD VDual(T x) : nz(kDenseDuals ? ~0u : 0u) {  // NOLINT constant embedding
+#pragma unroll
+        for (int l = 0; l < V; ++l) {
+            v[l] = x;
+#pragma unroll
+            for (int k = 0; k < N; ++k) d[k][l] = T(0);
+        }
+    }
+    BCAD_HD bool has(int k) const { return (nz >> k) & 1u; }
+};
+
+#define BCAD_VLANES _Pragma("unroll") for (int l = 0; l < V; ++l)
+
+template <class T, int N, int V>
+BCAD_HD VDual<T, N, V> operator-(const VDual<T, N, V>& a) {
+    VDual<T, N, V> r;
+    r.nz = a.nz;
+    BCAD_VLANES {
+        r.v[l] = -a.v[l];
+#pragma unroll
+        for (int k = 0; k < N; ++k) r.d[k][l] = a.has(k) ? -a.d[k][l] : T(0);
+    }
+    return r;
+}
+template <class T, int N, int V>
+BCAD_HD VDual<T, N, V> operator+(const VDual<T, N, V>& a, const VDual<T, N, V>& b) {
+    VDual<T, N, V> r;
+    r.nz = a.nz | b.nz;
+    BCAD_VLANES {
+        r.v[l] = a.v[l] + b.v[l];
+#pragma unroll
+        for (int k = 0; k < N; ++k)
+            r.d[k][l] = a.has(k) && b.has(k) ? a.d[k][l] + b.d[k][l] : a.has(k) ? a.d[k][l] : b.has(k) ? b.d[k][l] : T(0);
+    }
+    return r;
+}
+template <class T, int N, int V>
+BCAD_HD VDual<T, N, V> operator-(const VDual<T, N, V>& a, const VDual<T, N, V>& b) {
+    VDual<T, N, V> r;
+    r.nz = a.nz | b.nz;
+    BCAD_VLANES {
+        r.v[l] = a.v[l] - b.v[l];
+#pragma unroll
+        for (int k = 0; k < N; ++k)
+            r.d[k][l] = a.has(k) && b.has(k) ? a.d[k][l] - b.d[k][l] : a.has(k) ? a.d[k][l] : b.has(k) ? -b.d[k][l] : T(0);
+    }
+    return r;
+}
+template <class T, int N, int V>
+BCAD_HD VDual<T, N, V> operator*(const VDual<T, N, V>& a, const VDual<T, N, V>& b) {
+    VDual<T, N, V> r;
+    r.nz = a.nz | b.nz;
+    BCAD_VLANES {
+        r.v[l] = a.v[l] * b.v[l];
+#pragma unroll
+        for (int k = 0; k < N; ++k)
+            r.d[k][l] = a.has(k) && b.has(k) ? a.d[k][l] * b.v[l] + a.v[l] * b.d[k][l]
+                        : a.has(k)            ? a.d[k][l] * b.v[l]
+                        : b.has(k)            ? a.v[l] * b.d[k][l]
+                                              : T(0);
+    }
+    return r;
+}
+template <class T, int N, int V>
+BCAD_HD VDual<T, N, V> operator/(const VDual<T, N, V>& a, const VDual<T, N, V>& b) {
+    VDual<T, N, V> r;
+    r.nz = a.nz | b.nz;
+    BCAD_VLANES {
+        if (b.v[l] == T(0)) raise_status(kDevDivisionByZero);
+        r.v[l] = a.v[l] / b.v[l];
+        const T denom = b.v[l] * b.v[l];
+#pragma unroll
+        for (int k = 0; k < N; ++k)
+            r.d[k][l] = a.has(k) && b.has(k) ? (a.d[k][l] * b.v[l] - a.v[l] * b.d[k][l]) / denom
+                        : a.has(k)            ? (a.d[k][l] * b.v[l]) / denom
+                        : b.has(k)            ? (-(a.v[l] * b.d[k][l])) / denom
+                                              : T(0);
+    }
+    return r;
+}
+template <class T, int N, int V>
+BCAD_HD VDual<T, N, V> shifted(const VDual<T, N, V>& a, T s) {
+    VDual<T, N, V> r = a;
+    BCAD_VLANES r.v[l] = a.v[l] + s;
+    return r;
+}
+template <class T, int N, int V>
+BCAD_HD VDual<T, N, V> scaled(const VDual<T, N, V>& a, T s) {
+    VDual<T, N, V> r;
+    r.nz = a.nz;
+    BCAD_VLANES {
+        r.v[l] = a.v[l] * s;
+#pragma unroll
+        for (int k = 0; k < N; ++k) r.d[k][l] = a.has(k) ? a.d[k][l] * s : T(0);
+    }
+    return r;
+}
+template <class T, int N, int V> BCAD_HD VDual<T, N, V> operator+(const VDual<T, N, V>& a, double s) { return shifted(a, T(s)); }
+template <class T, int N, int V> BCAD_HD VDual<T, N, V> operator+(double s, const VDual<T, N, V>& a) { return shifted(a, T(s)); }
+template <class T, int N, int V> BCAD_HD VDual<T, N, V> operator-(const VDual<T, N, V>& a, double s) { return shifted(a, -T(s)); }
+template <class T, int N, int V> BCAD_HD VDual<T, N, V> operator-(double s, const VDual<T, N, V>& a) { return shifted(-a, T(s)); }
+template <class T, int N, int V> BCAD_HD VDual<T, N, V> operator*(const VDual<T, N, V>& a, double s) { return scaled(a, T(s)); }
+template <class T, int N, int V> BCAD_HD VDual<T, N, V> operator*(double s, const VDual<T, N, V>& a) { return scaled(a, T(s)); }
+template <class T, int N, int V>
+BCAD_HD VDual<T, N, V> operator/(const VDual<T, N, V>& a, double s) {
+    const T rs = T(s);
+    if (rs == T(0)) raise_status(kDevDivisionByZero);
+    return scaled(a, T(1) / rs);
+}
+template <class T, int N, int V>
+BCAD_HD VDual<T, N, V> operator/(double s, const VDual<T, N, V>& b) {
+    VDual<T, N, V> r;
+    r.nz = b.nz;
+    const T rs = T(s);
+    BCAD_VLANES {
+        if (b.v[l] == T(0)) raise_status(kDevDivisionByZero);
+        r.v[l] = rs / b.v[l];
+        const T scale = -rs / (b.v[l] * b.v[l]);
+#pragma unroll
+        for (int k = 0; k < N; ++k) r.d[k][l] = b.has(k) ? scale * b.d[k][l] : T(0);
+    }
+    return r;
+}
+// Lane-0 comparisons (uniform predicates only; see above).
+template <class T, int N, int V> BCAD_HD bool operator<(const VDual<T, N, V>& a, double s) { return a.v[0] < T(s); }
+template <class T, int N, int V> BCAD_HD bool operator>(const VDual<T, N, V>& a, double s) { return a.v[0] > T(s); }
+template <class T, int N, int V> BCAD_HD bool operator<=(const VDual<T, N, V>& a, double s) { return a.v[0] <= T(s); }
+template <class T, int N, int V> BCAD_HD bool operator>=(const VDual<T, N, V>& a, double s) { return a.v[0] >= T(s); }
+template <class T, int N, int V> BCAD_HD bool operator==(const VDual<T, N, V>& a, double s) { return a.v[0] == T(s); }
+template <class T, int N, int V> BCAD_HD bool operator!=(const VDual<T, N, V>& a, double s) { return a.v[0] != T(s); }
+
+template <class T, int N, int V, class F>
+BCAD_HD VDual<T, N, V> vchain(const VDual<T, N, V>& a, F&& prim_and_scale) {
+    VDual<T, N, V> r;
+    r.nz = a.nz;
+    BCAD_VLANES {
+        T p, scale;
+        prim_and_scale(a.v[l], p, scale);
+        r.v[l] = p;
+#pragma unroll
+        for (int k = 0; k < N; ++k) r.d[k][l] = a.has(k) ? scale * a.d[k][l] : T(0);
+    }
+    return r;
+}
+template <class T, int N, int V> BCAD_HD VDual<T, N, V> exp(const VDual<T, N, V>& a) {
+    return vchain(a, [](T x, T& p, T& s) { p = d_exp(x); s = p; });
+}
+template <class T, int N, int V> BCAD_HD VDual<T, N, V> log(const VDual<T, N, V>& a) {
+    return vchain(a, [](T x, T& p, T& s) {
+        if (!(x > T(0))) raise_status(kDevDomainError);
+        p = d_log(x);
+        s = T(1) / x;
+    });
+}
+template <class T, int N, int V> BCAD_HD VDual<T, N, V> sin(const VDual<T, N, V>& a) {
+    return vchain(a, [](T x, T& p, T& s) { p = d_sin(x); s = d_cos(x); });
+}
+template <class T, int N, int V> BCAD_HD VDual<T, N, V> cos(const VDual<T, N, V>& a) {
+    return vchain(a, [](T x, T& p, T& s) { p = d_cos(x); s = -d_sin(x); });
+}
+template <class T, int N, int V> BCAD_HD VDual<T, N, V> tanh(const VDual<T, N, V>& a) {
+    return vchain(a, [](T x, T& p, T& s) { p = d_tanh(x); s = T(1) - p * p; });
+}
+template <class T, int N, int V> BCAD_HD VDual<T, N, V> sigmoid(const VDual<T, N, V>& a) {
+    return vchain(a, [](T x, T& p, T& s) { p = raw_sigmoid(x); s = p * (T(1) - p); });
+}
+template <class T, int N, int V> BCAD_HD VDual<T, N, V> sqrt(const VDual<T, N, V>& a) {
+    return vchain(a, [](T x, T& p, T& s) {
+        if (x < T(0)) raise_status(kDevDomainError);
+        p = d_sqrt(x);
+        s = T(1) / (T(2) * p);
+    });
+}
+template <class T, int N, int V> BCAD_HD VDual<T, N, V> pow(const VDual<T, N, V>& a, double exponent) {
+    const T c = T(exponent);
+    return vchain(a, [c](T x, T& p, T& s) {
+        if (x < T(0) && c != d_floor(c)) raise_status(kDevDomainError);
+        p = d_pow(x, c);
+        s = c * d_pow(x, c - T(1));
+    });
+}
+template <class T, int N, int V> BCAD_HD VDual<T, N, V> abs(const VDual<T, N, V>& a) {
+    VDual<T, N, V> r;
+    r.nz = a.nz;
+    BCAD_VLANES {
+        if (a.v[l] == T(0)) raise_status(kDevNonDifferentiable);
+        const bool pos = a.v[l] > T(0);
+        r.v[l] = pos ? a.v[l] : -a.v[l];
+#pragma unroll
+        for (int k = 0; k < N; ++k) r.d[k][l] = a.has(k) ? (pos ? a.d[k][l] : -a.d[k][l]) : T(0);
+    }
+    return r;
+}
+#undef BCAD_VLANES
+
 
 }  // namespace bcad_dev

@@ -158,6 +158,74 @@ __device__ __forceinline__ int arg_class(const int* dyn, int j) {
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
+// ------------------------------------------------------ cell evaluation
+// True when every branch predicate of the body reads an argument that is
+// uniform across a thread's V cells under signature S (ROW / SCALAR class),
+// so the V cells can be evaluated as one lane-vector dual (VDual).
+template <class Body, class S>
+__host__ __device__ constexpr bool vec_eval_ok() {
+    if (Body::kPredicateArgs == 0u) return true;
+    if (!S::kStatic) return false;
+    for (int j = 0; j < Body::kIn; ++j)
+        if (((Body::kPredicateArgs >> j) & 1u) && S::cls(j) != kRow && S::cls(j) != kScalar) return false;
+    return true;
+}
+
+// The dual evaluation of one thread's V cells: primals y[M] (nullable) and
+// partials d[M*N] from inputs x[N], seeded x_j + e_j (forward.hpp:121-126).
+template <class Body, class T, int V, class S>
+__device__ __forceinline__ void eval_cells(const Pack<T, V>* x, Pack<T, V>* y, Pack<T, V>* d,
+                                           unsigned long long* err, int64_t off) {
+    constexpr int N = Body::kIn, M = Body::kOut;
+    auto scalar_lane = [&](int v) {
+        Dual<T, N> xi[N], yo[M];
+#pragma unroll
+        for (int j = 0; j < N; ++j) xi[j] = Dual<T, N>::seeded(x[j].x[v], j);
+        Body::template body<Dual<T, N>>(xi, yo);
+        if constexpr (Body::kMayRaise) report_error(err, off + v);
+#pragma unroll
+        for (int i = 0; i < M; ++i) {
+            if (y) y[i].x[v] = yo[i].v;
+#pragma unroll
+            for (int j = 0; j < N; ++j) d[i * N + j].x[v] = yo[i].d[j];
+        }
+    };
+    if constexpr (vec_eval_ok<Body, S>() && V > 1) {
+        using VD = VDual<T, N, V>;
+        VD xi[N], yo[M];
+#pragma unroll
+        for (int j = 0; j < N; ++j) {
+            xi[j] = VD(T(0));
+#pragma unroll
+            for (int v = 0; v < V; ++v) xi[j].v[v] = x[j].x[v];
+#pragma unroll
+            for (int v = 0; v < V; ++v) xi[j].d[j][v] = T(1);
+            xi[j].nz = kDenseDuals ? ~0u : (1u << j);
+        }
+        Body::template body<VD>(xi, yo);
+        if constexpr (Body::kMayRaise) {
+            if (s_err_flag[threadIdx.x]) {  // rare: find the failing lane(s) in order
+                s_err_flag[threadIdx.x] = 0;
+#pragma unroll 1
+                for (int v = 0; v < V; ++v) scalar_lane(v);
+                return;
+            }
+        }
+#pragma unroll
+        for (int i = 0; i < M; ++i) {
+#pragma unroll
+            for (int v = 0; v < V; ++v) {
+                if (y) y[i].x[v] = yo[i].v[v];
+#pragma unroll
+                for (int j = 0; j < N; ++j) d[i * N + j].x[v] = yo[i].d[j][v];
+            }
+        }
+    } else {
+#pragma unroll
+        for (int v = 0; v < V; ++v) scalar_lane(v);
+    }
+}
+
 // ------------------------------------------------------------- K1 params
 // 2-D grid: blockIdx.x = column tile (txv vector-columns), blockIdx.y = row
 // tile (ty thread-rows x rpt rows per thread).
@@ -245,21 +313,7 @@ __global__ void __launch_bounds__(kThreads) fwd2d_kernel(const __grid_constant__
             Pack<T, V> y[M];
             Pack<T, V> d[M * N];
 #pragma unroll
-            for (int v = 0; v < V; ++v) {
-                Dual<T, N> xi[N], yo[M];
-#pragma unroll
-                for (int j = 0; j < N; ++j) {  // seed x_j + e_j (forward.hpp:121-126)
-                    xi[j] = Dual<T, N>::seeded(x[j].x[v], j);
-                }
-                Body::template body<Dual<T, N>>(xi, yo);
-                if constexpr (Body::kMayRaise) report_error(p.err, off + v);
-#pragma unroll
-                for (int i = 0; i < M; ++i) {
-                    y[i].x[v] = yo[i].v;
-#pragma unroll
-                    for (int j = 0; j < N; ++j) d[i * N + j].x[v] = yo[i].d[j];
-                }
-            }
+            eval_cells<Body, T, V, S>(x, y, d, p.err, off);
 #pragma unroll
             for (int i = 0; i < M; ++i) {
                 if (kDense || p.primal[i]) st_vec<T, V>(p.primal[i] + off, y[i]);
@@ -407,22 +461,7 @@ __global__ void __launch_bounds__(kThreads) pull2d_kernel(const __grid_constant_
         const int64_t off = r * p.cols + c0;
         Pack<T, V> D[M * N];
         if constexpr (kRecompute) {
-            if (live) {
-#pragma unroll
-                for (int v = 0; v < V; ++v) {
-                    Dual<T, N> xi[N], yo[M];
-#pragma unroll
-                    for (int j = 0; j < N; ++j) {
-                        xi[j] = Dual<T, N>::seeded(q[j].x[v], j);
-                    }
-                    Body::template body<Dual<T, N>>(xi, yo);
-                    if constexpr (Body::kMayRaise) report_error(p.err, off + v);
-#pragma unroll
-                    for (int i = 0; i < M; ++i)
-#pragma unroll
-                        for (int j = 0; j < N; ++j) D[i * N + j].x[v] = yo[i].d[j];
-                }
-            }
+            if (live) eval_cells<Body, T, V, S>(q, static_cast<Pack<T, V>*>(nullptr), D, p.err, off);
         } else {
 #pragma unroll
             for (int t = 0; t < M * N; ++t) D[t] = q[t];
