@@ -11,7 +11,8 @@ One step = one pass of the hot path over one batch: bcad_cu_forward (primal +
 M*N partials) then bcad_cu_pullback (all input adjoints) — what the
 reference's run_cell_once("mixed-cache") times (proj/src/bench.cpp:112-128).
 `value` = grad elements (output cells) per second over all ranks, inputs
-resident in HBM, L2 flushed between steps (a 1 GiB write, outside the timed
+resident in HBM, L2 flushed between steps (a 1 GiB write then a 1 GiB read,
+so the flush's own dirty lines are written back before the step; outside the timed
 events). `e2e` = the same step through the C-ABI with HOST buffers: pinned
 H2D of the step's inputs and seed, forward, pullback, D2H of the gradients.
 
@@ -186,6 +187,27 @@ def run_reference_arm(args, w: Workload, rank: int, world: int):
 
 
 # ------------------------------------------------------------------ native
+class L2Flush:
+    """Between timed steps: write 1 GiB (> the 126 MB L2), then read another
+    1 GiB so the written lines are cleaned out of L2 before the next step —
+    the step starts with a cold, clean L2 and does not pay the write-back of
+    the flush's own dirty lines."""
+
+    DESCRIPTION = ("flushed between steps outside the timed events: 1 GiB write (> 126 MB L2) then a 1 GiB read "
+                   "so no flush-dirty lines remain")
+
+    def __init__(self, device):
+        import torch
+        self.w = torch.empty(256 * 1024 * 1024, dtype=torch.float32, device=device)
+        self.r = torch.zeros(256 * 1024 * 1024, dtype=torch.float32, device=device)
+        self.acc = torch.zeros((), dtype=torch.float32, device=device)
+
+    def __call__(self):
+        import torch
+        self.w.fill_(1.0)
+        torch.sum(self.r, dim=0, out=self.acc)
+
+
 class Case:
     """Device buffers of one mixed step on this rank's batch shard."""
 
@@ -254,7 +276,7 @@ def run_native(args, w: Workload, rank: int, world: int):
         dist.broadcast_object_list(uid, src=0)
         comm = native.Comm(world, uid[0], rank)
 
-    flush = torch.empty(256 * 1024 * 1024, dtype=torch.float32, device=device)  # 1 GiB > 126 MB L2
+    l2 = L2Flush(device)
     K, W = args.steps, args.warmup
     ev = [[torch.cuda.Event(enable_timing=True) for _ in range(2)] for _ in range(K)]
     evb = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(K)]
@@ -277,7 +299,7 @@ def run_native(args, w: Workload, rank: int, world: int):
 
     with torch.cuda.stream(stream):
         for _ in range(W):
-            flush.fill_(1.0)
+            l2()
             one_step()
     torch.cuda.synchronize(device)
     if world > 1:
@@ -293,7 +315,7 @@ def run_native(args, w: Workload, rank: int, world: int):
             with torch.cuda.graph(graph, stream=stream):
                 one_step()
             for _ in range(W):
-                flush.fill_(1.0)
+                l2()
                 graph.replay()
         torch.cuda.synchronize(device)
         raw_step = one_step
@@ -312,7 +334,7 @@ def run_native(args, w: Workload, rank: int, world: int):
         dist.barrier()
     with torch.cuda.stream(stream):
         for k in range(K):
-            flush.fill_(float(k))
+            l2()
             one_step(ev[k])
     torch.cuda.synchronize(device)
     if world > 1:
@@ -320,7 +342,7 @@ def run_native(args, w: Workload, rank: int, world: int):
     clock_info = clocks.stop()
     with torch.cuda.stream(stream):  # breakdown pass (not the reported number)
         for k in range(K):
-            flush.fill_(float(k))
+            l2()
             one_step(evb[k])
     torch.cuda.synchronize(device)
 
@@ -380,7 +402,7 @@ def run_native(args, w: Workload, rank: int, world: int):
         "config": {"workload": w.describe, "B": w.B, "H": w.H, "B_per_gpu": B_local, "variant": w.variant,
                    "policy": "CacheForward" if args.policy == 0 else "RecomputeReverse",
                    "parallelism": f"batch-sharded dp{world}" if world > 1 else "single GPU",
-                   "l2": "flushed between steps (1 GiB write outside the timed events)",
+                   "l2": L2Flush.DESCRIPTION,
                    "launch": "CUDA graph replay of K1->K2 (PDL edges)" if args.graph else "stream launches (PDL)"},
         "breakdown_ms": {"K1_forward": k1_avg, "K2_pullback": k2_avg, "allreduce": statistics.mean(ar_ms),
                          "step_min": min(step_ms), "step_median": statistics.median(step_ms)},
@@ -432,13 +454,13 @@ def run_e2e(case: Case, stream, steps: int, device):
 def measure_secondary(w: Workload, device, stream, steps: int, policy: int):
     import torch
     case = Case(w, w.B, device, seed=99, policy=policy)
-    flush = torch.empty(256 * 1024 * 1024, dtype=torch.float32, device=device)
+    l2 = L2Flush(device)
     sp = int(stream.cuda_stream)
     ev = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(steps)]
     ev2 = [[torch.cuda.Event(enable_timing=True) for _ in range(2)] for _ in range(steps)]
     with torch.cuda.stream(stream):
         for k in range(3 + 2 * steps):
-            flush.fill_(1.0)
+            l2()
             e = ev[k - 3] if 3 <= k < 3 + steps else (ev2[k - 3 - steps] if k >= 3 + steps else None)
             if e:
                 e[0].record(stream)

@@ -92,7 +92,7 @@ int launch_fwd_t(const FwdArgs& a, std::string* err) {
             if (a.partials[i * N + j] && !aligned16(a.partials[i * N + j])) vec = false;
     }
     if (vec) {
-        const Tiling t = choose_tiling(plan, V, ClassMix{});  // no reductions in K1: wide row tiles
+        const Tiling t = choose_tiling(plan, V, ClassMix{}, /*fine=*/true);  // no reductions in K1: wide row tiles
         bcad_dev::Fwd2DParams<N, M, T> p{};
         for (int j = 0; j < N; ++j) {
             p.in[j] = static_cast<const T*>(a.in[j]);

@@ -175,7 +175,10 @@ inline ClassMix class_mix(const Plan& p) {
 //    reductions finish inside the CTA (shuffles + one shared-memory pass).
 // Rows per thread: one wave of CTAs for small problems (latency-bound), about
 // eight waves for large ones (tail-bound), never more than 65535 row tiles.
-inline Tiling choose_tiling(const Plan& p, int V, const ClassMix& mix) {
+// fine = true (forward): small problems keep one row per thread so the
+// hardware's dynamic CTA scheduling evens out rows of unequal cost (the
+// HM-LSTM UPDATE / FLUSH / COPY branch is per row).
+inline Tiling choose_tiling(const Plan& p, int V, const ClassMix& mix, bool fine = false) {
     Tiling t;
     t.V = V;
     t.vcols = p.cols / V;
@@ -188,7 +191,7 @@ inline Tiling choose_tiling(const Plan& p, int V, const ClassMix& mix) {
     const int64_t tiles1 = ceil_div(p.rows, t.ty);  // row tiles at rpt = 1
     const int64_t work = tiles1 * t.n_col_tiles;     // CTAs at rpt = 1
     const int64_t slots = int64_t(kSmCount) * kCtasPerSm;
-    int64_t rpt = work <= 2 * slots ? ceil_div(work, slots) : work / (8 * slots);
+    int64_t rpt = work <= 2 * slots ? (fine ? 1 : ceil_div(work, slots)) : work / (8 * slots);
     if (rpt < 1) rpt = 1;
     if (rpt > 512) rpt = 512;
     // keep the per-tile row partials in shared memory small
