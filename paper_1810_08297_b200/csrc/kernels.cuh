@@ -370,7 +370,7 @@ __host__ __device__ inline size_t pull_smem_doubles(int n_col, int n_row, int n_
 // (mixed.hpp:34-38); FULL slots get the reference's element arithmetic,
 // reduced slots an fp64 sum of those terms in a fixed order.
 template <class Body, class T, int V, bool kRecompute, class S, bool kDense>
-__global__ void __launch_bounds__(kThreads) pull2d_kernel(const __grid_constant__ Pull2DParams<Body::kIn, Body::kOut, T> p) {
+__global__ void __launch_bounds__(kThreads, kRecompute ? 1 : kCtasPerSm) pull2d_kernel(const __grid_constant__ Pull2DParams<Body::kIn, Body::kOut, T> p) {
     constexpr int N = Body::kIn, M = Body::kOut;
     constexpr bool kAnyRow = !S::kStatic || S::has(kRow);
     constexpr bool kAnyCol = !S::kStatic || S::has(kCol);
@@ -447,17 +447,16 @@ __global__ void __launch_bounds__(kThreads) pull2d_kernel(const __grid_constant_
         }
     };
 
-    int64_t r = int64_t(rt) * p.tile_rows + ty;
-    bool live = active && r < p.rows;
-    Pack<T, V> w[M], q[kStreams];
-    if (live) load_row(r, w, q);
+    const int64_t r0 = int64_t(rt) * p.tile_rows + ty;
     // Every lane runs the same rpt iterations (rows past the end are masked),
-    // so the ROW shuffles always see complete lane groups.
+    // so the ROW shuffles always see complete lane groups. (No next-row
+    // prefetch here: it would push the kernel past 64 registers, i.e. below
+    // four resident CTAs per SM, which the tiling assumes.)
     for (int k = 0; k < p.rpt; ++k) {
-        const int64_t rn = r + p.ty;
-        const bool live_n = active && k + 1 < p.rpt && rn < p.rows;
-        Pack<T, V> wn[M], qn[kStreams];
-        if (live_n) load_row(rn, wn, qn);
+        const int64_t r = r0 + int64_t(k) * p.ty;
+        const bool live = active && r < p.rows;
+        Pack<T, V> w[M], q[kStreams];
+        if (live) load_row(r, w, q);
         const int64_t off = r * p.cols + c0;
         Pack<T, V> D[M * N];
         if constexpr (kRecompute) {
@@ -523,12 +522,6 @@ __global__ void __launch_bounds__(kThreads) pull2d_kernel(const __grid_constant_
                     row_acc[(arg_slot<S, kDense>(p.slot, j) * trows + k * p.ty) * wpr + row_base] = t;
             }
         }
-#pragma unroll
-        for (int i = 0; i < M; ++i) w[i] = wn[i];
-#pragma unroll
-        for (int t = 0; t < kStreams; ++t) q[t] = qn[t];
-        r = rn;
-        live = live_n;
     }
     if constexpr (!kAnyRow && !kAnyCol && !kAnyScal) return;
     else {
