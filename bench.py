@@ -386,7 +386,7 @@ def run_native(args, w: Workload, rank: int, world: int):
         return
     extra = {}
     if world == 1 and args.extra:
-        for key in args.extra.split(","):
+        for key in ("" if args.extra == "none" else args.extra).split(","):
             if key and key != w.key:
                 extra[key] = measure_secondary(WORKLOADS[key], device, stream, max(5, K // 2), args.policy)
 
