@@ -387,7 +387,15 @@ def run_native(args, w: Workload, rank: int, world: int):
     extra = {}
     if world == 1 and args.extra:
         for key in ("" if args.extra == "none" else args.extra).split(","):
-            if key and key != w.key:
+            if not key or key == w.key:
+                continue
+            if key == "tape":
+                extra[key] = measure_tape(device, stream, max(5, K // 2))
+            elif key == "arity":
+                extra[key] = measure_arity(device, stream, max(5, K // 2))
+            elif key.endswith(":r"):  # RecomputeReverse: K1p primal + fused K2r
+                extra[key] = measure_secondary(WORKLOADS[key[:-2]], device, stream, max(5, K // 2), 1)
+            else:
                 extra[key] = measure_secondary(WORKLOADS[key], device, stream, max(5, K // 2), args.policy)
 
     cpu = None
@@ -485,6 +493,71 @@ def measure_secondary(w: Workload, device, stream, steps: int, policy: int):
     return out
 
 
+def timed_steps(fn, stream, device, steps):
+    """Median device time of fn() over `steps` runs, L2 flushed before each."""
+    import torch
+    l2 = L2Flush(device)
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+    with torch.cuda.stream(stream):
+        for _ in range(3):
+            l2()
+            fn()
+        for a, b in ev:
+            l2()
+            a.record(stream)
+            fn()
+            b.record(stream)
+    torch.cuda.synchronize(device)
+    return statistics.median(a.elapsed_time(b) for a, b in ev)
+
+
+def measure_tape(device, stream, steps: int):
+    """Paper Fig. 1 on B200: the four gradients of the n x n cell update
+    through the C++ tape (cell_gradients, hmlstm.hpp:123-142) — mixed-mode
+    (one fused node) vs the reverse-mode vectorised-select baseline (8 tensor
+    primitives), device-resident, tape input copies included as in the
+    reference's run_cell_once (bench.cpp:112-128)."""
+    import torch
+    from paper_1810_08297_b200 import host
+    n = 1024
+    g = torch.Generator(device=device)
+    g.manual_seed(5)
+    ins = [torch.rand((n, n), generator=g, device=device) * 2 - 1 for _ in range(4)]
+    ins += [(torch.rand(n, generator=g, device=device) < 0.5).float() for _ in range(2)]
+    seed = torch.ones((n, n), device=device)
+    grads = [torch.empty((n, n), device=device) for _ in range(4)]
+    out = {"n": n, "dtype": "f32"}
+    for impl in ("mixed-cache", "mixed-recompute", "reverse-unfused"):
+        nodes, peak = host.cell_gradients(impl, ins, seed, grads, stream)
+        ms = timed_steps(lambda: host.cell_gradients(impl, ins, seed, grads, stream), stream, device, steps)
+        out[impl] = {"ms": ms, "tape_nodes": nodes, "peak_cached_bytes": peak}
+    out["speedup_mixed_cache_vs_reverse_unfused"] = out["reverse-unfused"]["ms"] / out["mixed-cache"]["ms"]
+    return out
+
+
+def measure_arity(device, stream, steps: int):
+    """Paper §3.4.1 / Fig. 3 on B200: forward-mode diagonal Jacobian of
+    tanh_product_A (arity_workload.hpp:19-28) at 1024 x 1024 fp32, one fused
+    K1 per call; bytes = (A inputs + primal + A partials) * 4 per cell."""
+    import torch
+    from paper_1810_08297_b200 import native
+    n = 1024
+    peak, _ = hbm_peak()
+    out = {"n": n}
+    g = torch.Generator(device=device)
+    g.manual_seed(9)
+    for A in (1, 2, 4, 8, 16, 18, 32):
+        k = native.Kernel(f"tanh_product_{A}")
+        ins = [torch.rand((n, n), generator=g, device=device) * 2 - 1 for _ in range(A)]
+        prim = [torch.empty((n, n), device=device)]
+        parts = [torch.empty((n, n), device=device) for _ in range(A)]
+        ms = timed_steps(lambda: native.forward(k, ins, prim, parts, stream=stream), stream, device, steps)
+        b = (2 * A + 1) * n * n * 4
+        out[f"A{A}"] = {"ms": ms, "GBps": b / (ms * 1e-3) / 1e9, "frac_hbm": b / (ms * 1e-3) / 1e9 / peak}
+        del ins, parts
+    return out
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -495,7 +568,9 @@ def main():
     ap.add_argument("--policy", type=int, default=0, help="0 CacheForward, 1 RecomputeReverse")
     ap.add_argument("--e2e-steps", type=int, default=10)
     ap.add_argument("--graph", type=int, default=1, help="1: replay the step as a captured CUDA graph")
-    ap.add_argument("--extra", default="cfg3,cfg4,cfg4div,cfg5", help="secondary configs measured at N=1")
+    ap.add_argument("--extra", default="cfg3,cfg4,cfg4div,cfg5,cfg2:r,cfg5:r,tape,arity",
+                    help="secondary measurements at N=1 ('none' for none): configs, <cfg>:r = RecomputeReverse, "
+                         "tape = cell_gradients mixed vs reverse-unfused, arity = tanh_product study")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=12.0)
     args = ap.parse_args()

@@ -90,6 +90,13 @@ public:
         return t;
     }
 
+    // Deep copy of `shape.volume()` values already in device memory.
+    static Tensor from_device(Shape shape, const T* data) {
+        Tensor t(NoInit{}, std::move(shape));
+        check(bcad_cu_memcpy(t.buf_->ptr, data, t.bytes(), 2, t.stream()));
+        return t;
+    }
+
     Tensor(const Tensor& o) : shape_(o.shape_) {
         allocate();
         check(bcad_cu_memcpy(buf_->ptr, o.buf_->ptr, bytes(), 2, stream()));

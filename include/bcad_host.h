@@ -30,6 +30,16 @@ int bcad_host_mixed_step(const char* kernel, int dtype, int n_in, const void* co
                          void* const* host_primal, void* const* host_grads, int64_t* peak_cached_bytes,
                          void* stream);
 
+/* cell_gradients (proj/include/bcad/hmlstm.hpp:123-142) on an n x n cell:
+ * impl 0 mixed-cache, 1 mixed-recompute, 2 reverse-unfused (the 8-primitive
+ * vectorised-select baseline, hmlstm.hpp:82-99). Inputs c, f, i, g (n*n),
+ * z1, z2 (n) and the seed (n*n) are DEVICE pointers; they are copied into the
+ * tape as the reference's Tape::input copies (tape.hpp:75-82). Gradients
+ * dc, df, di, dg (n*n each) are written to DEVICE pointers. Reports the tape
+ * size and peak_cached_bytes. Asynchronous on `stream` (no host sync). */
+int bcad_host_cell_gradients(int impl, int dtype, int64_t n, const void* const* dev_in, const void* dev_seed,
+                             void* const* dev_grads, int64_t* tape_nodes, int64_t* peak_cached_bytes, void* stream);
+
 const char* bcad_host_last_error(void);
 
 #ifdef __cplusplus

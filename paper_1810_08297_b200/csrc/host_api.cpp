@@ -60,9 +60,48 @@ void step(const char* name, int n_in, const void* const* host_in, const bcad_cu_
     if (peak) *peak = tape.peak_cached_bytes();
 }
 
+template <class Real>
+void cell_grads(int impl, int64_t n, const void* const* dev_in, const void* dev_seed, void* const* dev_grads,
+                int64_t* nodes, int64_t* peak) {
+    using namespace bcad;
+    const Shape mat{n, n}, vec{n};
+    auto dev = [](const Shape& s, const void* p) { return Tensor<Real>::from_device(s, static_cast<const Real*>(p)); };
+    const CellInputs<Real> in{dev(mat, dev_in[0]), dev(mat, dev_in[1]), dev(mat, dev_in[2]),
+                              dev(mat, dev_in[3]), dev(vec, dev_in[4]), dev(vec, dev_in[5])};
+    const Tensor<Real> seed = dev(mat, dev_seed);
+    Tape<Real> tape;
+    CellGraph<Real> graph;
+    if (impl == 0) graph = cell_update_fused(tape, in, MixedPolicy::CacheForward);
+    else if (impl == 1) graph = cell_update_fused(tape, in, MixedPolicy::RecomputeReverse);
+    else if (impl == 2) graph = cell_update_unfused(tape, in);
+    else throw ConfigError("impl must be 0 (mixed-cache), 1 (mixed-recompute) or 2 (reverse-unfused)");
+    const Gradients<Real> g = tape.backward(graph.out, seed);
+    const Var<Real> leaves[4] = {graph.c_prev, graph.f, graph.i, graph.g};
+    for (int k = 0; k < 4; ++k) {
+        const Tensor<Real>& t = g.at(leaves[k]);
+        check(bcad_cu_memcpy(dev_grads[k], t.device_data(), t.bytes(), 2, current_stream()));
+    }
+    if (nodes) *nodes = static_cast<int64_t>(tape.size());
+    if (peak) *peak = tape.peak_cached_bytes();
+}
+
 }  // namespace
 
 extern "C" {
+
+int bcad_host_cell_gradients(int impl, int dtype, int64_t n, const void* const* dev_in, const void* dev_seed,
+                             void* const* dev_grads, int64_t* tape_nodes, int64_t* peak_cached_bytes, void* stream) {
+    try {
+        bcad::StreamGuard guard(stream);
+        if (dtype == BCAD_CU_F32) cell_grads<float>(impl, n, dev_in, dev_seed, dev_grads, tape_nodes, peak_cached_bytes);
+        else if (dtype == BCAD_CU_F64) cell_grads<double>(impl, n, dev_in, dev_seed, dev_grads, tape_nodes, peak_cached_bytes);
+        else throw bcad::ConfigError("dtype must be F32 or F64");
+        return BCAD_CU_OK;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return code_of(e);
+    }
+}
 
 const char* bcad_host_last_error(void) { return g_err.c_str(); }
 

@@ -353,6 +353,23 @@ struct Pull2DParams {
     unsigned long long* err;
 };
 
+// sum_{q < n} base[q * stride], added strictly in q order (deterministic),
+// with the loads issued eight at a time from L2 (__ldcg: partials written by
+// other CTAs) so the dependent adds do not serialise the memory latency.
+__device__ __forceinline__ double ordered_sum(const double* base, int n, size_t stride) {
+    double s = 0.0;
+    int q = 0;
+    for (; q + 8 <= n; q += 8) {
+        double v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) v[u] = __ldcg(base + size_t(q + u) * stride);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) s += v[u];
+    }
+    for (; q < n; ++q) s += __ldcg(base + size_t(q) * stride);
+    return s;
+}
+
 template <class T>
 __device__ __forceinline__ T finish(double s, const T* slot_ptr, bool accumulate) {
     return accumulate ? T(double(*slot_ptr) + s) : T(s);
@@ -590,7 +607,7 @@ __global__ void __launch_bounds__(kThreads, kRecompute ? 1 : kCtasPerSm) pull2d_
                     const int a = int(item / nr);
                     const int64_t r = rb + item % nr;
                     double sacc = 0.0;
-                    for (int q = 0; q < p.n_col_tiles; ++q) sacc += __ldcg(&p.ws_row[(size_t(a) * p.n_col_tiles + q) * p.rows + r]);
+                    sacc = ordered_sum(p.ws_row + size_t(a) * p.n_col_tiles * p.rows + r, p.n_col_tiles, size_t(p.rows));
                     const int j = p.row_j[a];
                     p.adj[j][r] = finish<T>(sacc, p.adj[j] + r, (p.acc_mask >> j) & 1u);
                 }
@@ -608,7 +625,7 @@ __global__ void __launch_bounds__(kThreads, kRecompute ? 1 : kCtasPerSm) pull2d_
                     const int64_t c = int64_t(ct) * ccols + item % ccols;
                     if (c >= p.cols) continue;
                     double sacc = 0.0;
-                    for (int q = 0; q < p.n_row_tiles; ++q) sacc += __ldcg(&p.ws_col[(size_t(a) * p.n_row_tiles + q) * p.cols + c]);
+                    sacc = ordered_sum(p.ws_col + size_t(a) * p.n_row_tiles * p.cols + c, p.n_row_tiles, size_t(p.cols));
                     const int j = p.col_j[a];
                     p.adj[j][c] = finish<T>(sacc, p.adj[j] + c, (p.acc_mask >> j) & 1u);
                 }

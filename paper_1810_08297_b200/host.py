@@ -54,3 +54,26 @@ class HostStep:
         if rc:
             raise native._BY_CODE.get(rc, native.Error)(LIB.bcad_host_last_error().decode())
         return int(self.peak.value)
+
+
+LIB.bcad_host_cell_gradients.restype = C.c_int
+LIB.bcad_host_cell_gradients.argtypes = [C.c_int, C.c_int, C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p,
+                                         C.POINTER(C.c_int64), C.POINTER(C.c_int64), C.c_void_p]
+
+IMPLS = {"mixed-cache": 0, "mixed-recompute": 1, "reverse-unfused": 2}
+
+
+def cell_gradients(impl: str, inputs, seed, grads, stream=None) -> tuple[int, int]:
+    """cell_gradients (hmlstm.hpp:123-142) through the C++ tape on device
+    tensors: inputs (c, f, i, g, z1, z2), seed, grads (dc, df, di, dg) are
+    torch CUDA tensors. Returns (tape_nodes, peak_cached_bytes)."""
+    dev = (C.c_void_p * 6)(*[t.data_ptr() for t in inputs])
+    out = (C.c_void_p * 4)(*[t.data_ptr() for t in grads])
+    nodes, peak = C.c_int64(), C.c_int64()
+    dt = 0 if str(inputs[0].dtype) == "torch.float32" else 1
+    sp = None if stream is None else int(stream.cuda_stream)
+    rc = LIB.bcad_host_cell_gradients(IMPLS[impl], dt, inputs[0].shape[0], dev, seed.data_ptr(), out,
+                                      C.byref(nodes), C.byref(peak), sp)
+    if rc:
+        raise native._BY_CODE.get(rc, native.Error)(LIB.bcad_host_last_error().decode())
+    return int(nodes.value), int(peak.value)

@@ -70,3 +70,30 @@ def test_host_step_maps_errors(host):
         host_step(host, "mul", [np.ones((2, 3)), np.ones((4, 3))], [np.ones((2, 3))], 0)
     with pytest.raises(native.UnknownPrimitive):
         host_step(host, "nope", [np.ones(2)], [np.ones(2)], 0)
+
+
+@pytest.mark.parametrize("dtype", [np.float32, np.float64])
+def test_cell_gradients_three_impls(oracle_lib, dtype):
+    """cell_gradients through the C++ tape for mixed-cache, mixed-recompute and
+    reverse-unfused (hmlstm.hpp:123-142) agree with the oracle; the tape sizes
+    are 7 vs 14 nodes (test_bench.cpp:73-90)."""
+    import torch
+    from paper_1810_08297_b200 import host
+    n = 64
+    ins = O.hmlstm_inputs(oracle_lib, n, n, dtype, "canonical")
+    seed = np.random.default_rng(3).uniform(-1, 1, (n, n)).astype(dtype)
+    _, want, want64 = oracle_lib.mixed_step("hmlstm_update", ins, seeds=[seed])
+    dins = [torch.from_numpy(a).cuda() for a in ins]
+    dseed = torch.from_numpy(seed).cuda()
+    rtol, atol = tol_for(dtype)
+    got = {}
+    for impl in ("mixed-cache", "mixed-recompute", "reverse-unfused"):
+        grads = [torch.empty((n, n), dtype=dins[0].dtype, device="cuda") for _ in range(4)]
+        nodes, peak = host.cell_gradients(impl, dins, dseed, grads)
+        torch.cuda.synchronize()
+        assert nodes == (14 if impl == "reverse-unfused" else 7)
+        got[impl] = [g.cpu().numpy() for g in grads]
+        for k in range(4):
+            assert_close(got[impl][k], want[k], rtol, atol, f"{impl} grad{k}")
+    for a, b in zip(got["mixed-cache"], got["mixed-recompute"]):
+        assert np.array_equal(a, b)
