@@ -420,7 +420,9 @@ def run_native(args, w: Workload, rank: int, world: int):
                      "frac": achieved / peak, "traffic": traffic, "algorithmic_bytes_per_launch": dom_bytes,
                      "peak_source": peak_src},
         "e2e": {"value": e2e_value, "unit": "grad elements/s", "h2d_bytes_per_step": e2e["h2d"],
-                "d2h_bytes_per_step": e2e["d2h"], "ms_per_step": e2e["ms_per_step"]},
+                "d2h_bytes_per_step": e2e["d2h"], "ms_per_step": e2e["ms_per_step"],
+                "schedule": "row-chunk pipelined host step (bcad_host_set_pipeline auto)",
+                "one_shot_ms_per_step": e2e["one_shot_ms_per_step"], "pcie": e2e["pcie"]},
         "gpu_launches": 2 * K,
         "clocks": clock_info,
     }
@@ -435,28 +437,56 @@ def run_e2e(case: Case, stream, steps: int, device):
     """The user-facing call with HOST buffers (include/bcad_host.h ->
     C++ Tape + mixed_broadcast + backward over libbcad_cu.so), every step:
     pinned H2D of the inputs and the seed, K1, K2, D2H of every input
-    gradient, stream-synchronised return. Wall-clock per call."""
-    import numpy as np
+    gradient, stream-synchronised return. Wall-clock per call. Reported with
+    the library's default row-chunk pipelining (bcad_host_set_pipeline(0));
+    the one-shot schedule (one tape over the whole batch) and the bare PCIe
+    copy rates of the same bytes are measured beside it."""
     import torch
-    from paper_1810_08297_b200.host import HostStep
+    from paper_1810_08297_b200 import host
     host_in = [t.cpu().pin_memory() for t in case.ins]
     host_seed = case.seed.cpu().pin_memory()
     host_grad = [torch.empty(t.shape, dtype=t.dtype).pin_memory() for t in case.adj]
     np_in = [t.numpy() for t in host_in]
     np_grad = [t.numpy() for t in host_grad]
-    call = HostStep(case.w.kernel, np_in, [host_seed.numpy()], grads_out=np_grad, policy=case.policy,
-                    stream=int(stream.cuda_stream))
+    call = host.HostStep(case.w.kernel, np_in, [host_seed.numpy()], grads_out=np_grad, policy=case.policy,
+                         stream=int(stream.cuda_stream))
     h2d = sum(a.nbytes for a in np_in) + host_seed.numpy().nbytes
     d2h = sum(a.nbytes for a in np_grad)
-    for _ in range(2):
-        call()
-    torch.cuda.synchronize(device)
-    t0 = time.perf_counter()
-    for _ in range(steps):
-        call()
-    ms = (time.perf_counter() - t0) * 1e3 / steps
-    del np
-    return {"ms_per_step": ms, "h2d": h2d, "d2h": d2h}
+
+    def wall(n):
+        for _ in range(2):
+            call()
+        torch.cuda.synchronize(device)
+        t0 = time.perf_counter()
+        for _ in range(n):
+            call()
+        return (time.perf_counter() - t0) * 1e3 / n
+
+    try:
+        host.set_pipeline(1)
+        one_shot = wall(steps)
+    finally:
+        host.set_pipeline(0)
+    ms = wall(steps)
+    # bare copy rates of the same byte volumes (pinned, one stream)
+    dev_in = torch.empty(h2d // 4, dtype=torch.float32, device=device)
+    hin = torch.empty(h2d // 4, dtype=torch.float32).pin_memory()
+    dev_out = torch.empty(d2h // 4, dtype=torch.float32, device=device)
+    hout = torch.empty(d2h // 4, dtype=torch.float32).pin_memory()
+    with torch.cuda.stream(stream):
+        def copy_ms(fn, n=10):
+            fn()
+            torch.cuda.synchronize(device)
+            t0 = time.perf_counter()
+            for _ in range(n):
+                fn()
+            torch.cuda.synchronize(device)
+            return (time.perf_counter() - t0) * 1e3 / n
+        h2d_ms = copy_ms(lambda: dev_in.copy_(hin, non_blocking=True))
+        d2h_ms = copy_ms(lambda: hout.copy_(dev_out, non_blocking=True))
+    return {"ms_per_step": ms, "h2d": h2d, "d2h": d2h, "one_shot_ms_per_step": one_shot,
+            "pcie": {"h2d_GBps": h2d / (h2d_ms * 1e-3) / 1e9, "d2h_GBps": d2h / (d2h_ms * 1e-3) / 1e9,
+                     "serial_copy_ms": h2d_ms + d2h_ms}}
 
 
 def measure_secondary(w: Workload, device, stream, steps: int, policy: int):

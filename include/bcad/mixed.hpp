@@ -72,10 +72,10 @@ void backprop_diag_device(Tape<Real>& tape, int node, const BroadcastKernel<Real
     }
     std::size_t ws_bytes = 0;
     check(bcad_cu_pullback_workspace(kernel.handle(), dtype_of<Real>::value, n, shapes.data(), m, &ws_bytes));
-    void* ws = tape.workspace(ws_bytes);
+    void* ws = tape.workspace(node, ws_bytes);
     check(bcad_cu_pullback(kernel.handle(), dtype_of<Real>::value, n, shapes.data(), m, w.data(),
                            cached ? parts.data() : nullptr, in_ptrs.data(), adj.data(), acc.data(), ws,
-                           tape.workspace_bytes(), current_stream()));
+                           tape.workspace_bytes(node), current_stream()));
     for (auto& [first, scratch] : dup) tape.accumulate_adjoint(ins[static_cast<std::size_t>(first)], scratch);
 }
 

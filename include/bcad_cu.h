@@ -114,8 +114,10 @@ int bcad_cu_forward(bcad_cu_kernel k, int dtype, int n_in, const void* const* in
                     void* const* partials_out, void* stream);
 
 /* Bytes of device workspace bcad_cu_pullback needs for this problem. The
- * workspace must be zero-filled once when first allocated; every pullback
- * leaves it reusable (its completion counters return to zero). */
+ * workspace must be zero-filled once when first allocated; a pullback leaves
+ * it reusable by later pullbacks of the SAME kernel, dtype and shapes (its
+ * completion counters return to zero). Problems of different shapes need
+ * their own workspaces (or a re-zeroed one): their layouts differ. */
 int bcad_cu_pullback_workspace(bcad_cu_kernel k, int dtype, int n_in, const bcad_cu_shape* in_shapes,
                                int m_out, size_t* bytes);
 
@@ -161,6 +163,12 @@ int bcad_cu_stream_create(void** stream);
 int bcad_cu_stream_destroy(void* stream);
 int bcad_cu_stream_synchronize(void* stream);
 int bcad_cu_device_synchronize(void);
+/* Stream ordering between streams (fork/join of pipelined host steps):
+ * timing-disabled events. */
+int bcad_cu_event_create(void** event);
+int bcad_cu_event_destroy(void* event);
+int bcad_cu_event_record(void* event, void* stream);
+int bcad_cu_stream_wait_event(void* stream, void* event);
 
 /* ------------------------------------------------------ multi-GPU (NCCL) */
 /* NCCL is loaded at run time (dlopen libnccl.so.2); without it these return

@@ -40,6 +40,18 @@ int bcad_host_mixed_step(const char* kernel, int dtype, int n_in, const void* co
 int bcad_host_cell_gradients(int impl, int dtype, int64_t n, const void* const* dev_in, const void* dev_seed,
                              void* const* dev_grads, int64_t* tape_nodes, int64_t* peak_cached_bytes, void* stream);
 
+/* Row-chunk pipelining of bcad_host_mixed_step (a host-side schedule; the
+ * math per row is unchanged): the batch axis (axis 0) is cut into chunks run
+ * over four lane streams, so the host->device copy of one chunk, the kernels
+ * of the next and the device->host copy of the previous overlap. Rows are
+ * independent under first-axis broadcasting (shape.hpp:13-16); gradients of
+ * batch-broadcast arguments (axis 0 of length 1, or scalars) are summed over
+ * chunks in chunk order on the device. max_chunks: 0 = automatic (about 16 MiB
+ * of host<->device traffic per chunk, at most 16 chunks), 1 = off (one tape
+ * over the whole batch), k > 1 = at most k chunks. Kernels that may raise
+ * always run one-shot so error indices match the reference. Process-wide. */
+int bcad_host_set_pipeline(int max_chunks);
+
 const char* bcad_host_last_error(void);
 
 #ifdef __cplusplus

@@ -484,6 +484,26 @@ int bcad_cu_device_synchronize(void) {
     CU_TRY(cudaDeviceSynchronize(), "cudaDeviceSynchronize");
     return BCAD_CU_OK;
 }
+int bcad_cu_event_create(void** event) {
+    cudaEvent_t e;
+    CU_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "cudaEventCreate");
+    *event = e;
+    return BCAD_CU_OK;
+}
+int bcad_cu_event_destroy(void* event) {
+    if (!event) return BCAD_CU_OK;
+    CU_TRY(cudaEventDestroy(static_cast<cudaEvent_t>(event)), "cudaEventDestroy");
+    return BCAD_CU_OK;
+}
+int bcad_cu_event_record(void* event, void* stream) {
+    CU_TRY(cudaEventRecord(static_cast<cudaEvent_t>(event), static_cast<cudaStream_t>(stream)), "cudaEventRecord");
+    return BCAD_CU_OK;
+}
+int bcad_cu_stream_wait_event(void* stream, void* event) {
+    CU_TRY(cudaStreamWaitEvent(static_cast<cudaStream_t>(stream), static_cast<cudaEvent_t>(event), 0),
+           "cudaStreamWaitEvent");
+    return BCAD_CU_OK;
+}
 
 // ------------------------------------------------------------------ NCCL
 int bcad_cu_nccl_unique_id(unsigned char id[128]) {

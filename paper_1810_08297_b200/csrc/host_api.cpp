@@ -3,6 +3,10 @@
 // sequence (proj/src/bench.cpp:112-128) with device tensors.
 #include "bcad_host.h"
 
+#include <algorithm>
+#include <memory>
+#include <atomic>
+#include <optional>
 #include <span>
 #include <string>
 #include <vector>
@@ -29,10 +33,12 @@ int code_of(const std::exception& e) {
     return BCAD_CU_ERR_GENERIC;
 }
 
+// One reference step (bench.cpp:112-128) on the current stream: tape inputs
+// from host buffers, mixed_broadcast, backward(seeds), host copies of the
+// primal / gradients. Returns the tape's peak_cached_bytes.
 template <class Real>
-void step(const char* name, int n_in, const void* const* host_in, const bcad_cu_shape* shapes, int m_out,
-          int policy, const void* const* host_seeds, void* const* host_primal, void* const* host_grads,
-          int64_t* peak) {
+int64_t tape_step(const char* name, int n_in, const void* const* host_in, const bcad_cu_shape* shapes, int m_out,
+                  int policy, const void* const* host_seeds, void* const* host_primal, void* const* host_grads) {
     using namespace bcad;
     Tape<Real> tape;
     std::vector<Var<Real>> vars;
@@ -56,8 +62,221 @@ void step(const char* name, int n_in, const void* const* host_in, const bcad_cu_
         const Tensor<Real>& g = grads.at(vars[static_cast<std::size_t>(j)]);
         check(bcad_cu_memcpy(host_grads[j], g.device_data(), g.bytes(), 1, current_stream()));
     }
-    check(bcad_cu_stream_synchronize(current_stream()));
-    if (peak) *peak = tape.peak_cached_bytes();
+    return tape.peak_cached_bytes();
+}
+
+// ---- pipelined step. The batch axis (axis 0) is cut into row chunks that
+// flow through three streams: host->device copies (h2d), the K1/K2 kernels
+// (the caller's stream) and device->host copies (d2h), so the upload of
+// chunk c+1, the kernels of chunk c and the download of chunk c-1 overlap.
+// Rows are independent under the reference's first-axis broadcasting
+// (shape.hpp:13-16): per row the arithmetic and the (B)-axis reductions are
+// the one-shot tape's, bit for bit. Batch-broadcast arguments (axis 0 of
+// length 1, scalars) are uploaded once and their reduced gradients are
+// accumulated over chunks in chunk order by the pullback's accumulate flag.
+
+std::atomic<int> g_pipeline{0};  // 0 auto, 1 off, k > 1 at most k chunks
+
+// Auto chunking: each chunk costs ~7 copy-engine operations per direction
+// plus two launches, so chunks stay large (measured on B200 over PCIe:
+// 2-3 chunks beat both one-shot and finer pipelines at config 2).
+constexpr std::size_t kChunkBytes = std::size_t(16) << 20;  // host<->device bytes per chunk
+constexpr int kMaxChunks = 16;
+
+struct Pipe {
+    void* h2d = nullptr;
+    void* d2h = nullptr;
+    void* fork = nullptr;
+    void* join = nullptr;
+    void* in_ready[kMaxChunks] = {};
+    void* out_ready[kMaxChunks] = {};
+    Pipe() {
+        bcad::check(bcad_cu_stream_create(&h2d));
+        bcad::check(bcad_cu_stream_create(&d2h));
+        bcad::check(bcad_cu_event_create(&fork));
+        bcad::check(bcad_cu_event_create(&join));
+        for (int c = 0; c < kMaxChunks; ++c) {
+            bcad::check(bcad_cu_event_create(&in_ready[c]));
+            bcad::check(bcad_cu_event_create(&out_ready[c]));
+        }
+    }
+    ~Pipe() {  // best effort: may run after the CUDA context is gone
+        for (int c = 0; c < kMaxChunks; ++c) {
+            bcad_cu_event_destroy(in_ready[c]);
+            bcad_cu_event_destroy(out_ready[c]);
+        }
+        bcad_cu_event_destroy(fork);
+        bcad_cu_event_destroy(join);
+        bcad_cu_stream_destroy(h2d);
+        bcad_cu_stream_destroy(d2h);
+    }
+};
+
+Pipe& pipe() {
+    static thread_local Pipe p;
+    return p;
+}
+
+int64_t volume(const bcad_cu_shape& s) {
+    int64_t v = 1;
+    for (int d = 0; d < s.rank; ++d) v *= s.dims[d];
+    return v;
+}
+
+// Number of row chunks for this call (1 = one-shot tape).
+int plan_chunks(bcad_cu_kernel k, int n_in, const bcad_cu_shape* shapes, const bcad_cu_shape& out, int m_out,
+                std::size_t elem, const void* const* host_seeds, void* const* host_primal, void* const* host_grads,
+                const std::vector<bool>& split) {
+    const int cfg = g_pipeline.load(std::memory_order_relaxed);
+    if (cfg == 1 || out.rank < 1 || out.dims[0] < 2) return 1;
+    if (bcad_cu_kernel_may_raise(k)) return 1;  // keep the reference's whole-tensor error index
+    for (int j = 0; j < n_in; ++j)
+        if (!split[j] && shapes[j].rank > 0 && shapes[j].dims[0] != 1) return 1;
+    const int64_t vol = volume(out);
+    std::size_t bytes = 0;
+    for (int j = 0; j < n_in; ++j)
+        if (split[j]) bytes += std::size_t(volume(shapes[j])) * elem * ((host_grads && host_grads[j]) ? 2 : 1);
+    for (int i = 0; i < m_out; ++i)
+        bytes += std::size_t(vol) * elem * (((host_seeds && host_seeds[i]) ? 1 : 0) + ((host_primal && host_primal[i]) ? 1 : 0));
+    int chunks = cfg > 1 ? cfg : int(std::min<std::size_t>(kMaxChunks, bytes / kChunkBytes));
+    chunks = std::min(chunks, kMaxChunks);
+    if (chunks > out.dims[0]) chunks = int(out.dims[0]);
+    return chunks < 2 ? 1 : chunks;
+}
+
+template <class Real>
+int64_t pipelined_step(bcad_cu_kernel k, int n_in, const void* const* host_in, const bcad_cu_shape* shapes, int m_out,
+                       int policy, const void* const* host_seeds, void* const* host_primal, void* const* host_grads,
+                       const bcad_cu_shape& out, const std::vector<bool>& split, int chunks) {
+    using namespace bcad;
+    constexpr int dt = dtype_of<Real>::value;
+    void* const comp = current_stream();
+    Pipe& P = pipe();
+    const int64_t B = out.dims[0], E = volume(out), out_row = E / B;
+    const std::size_t n = static_cast<std::size_t>(n_in), m = static_cast<std::size_t>(m_out);
+    std::vector<int64_t> row_elems(n, 0);
+    int64_t in_elems = 0;
+    for (int j = 0; j < n_in; ++j) {
+        in_elems += volume(shapes[j]);
+        if (split[j]) row_elems[j] = volume(shapes[j]) / B;
+    }
+    // device buffers of the whole batch (stream-ordered pool on `comp`)
+    auto alloc = [&](int64_t elems) { return Tensor<Real>::uninitialized(Shape{elems}); };
+    std::vector<Tensor<Real>> x, y, D, w, g;
+    for (int j = 0; j < n_in; ++j) x.push_back(alloc(volume(shapes[j])));
+    for (int i = 0; i < m_out; ++i) y.push_back(alloc(E));
+    if (policy == 0)
+        for (std::size_t t = 0; t < m * n; ++t) D.push_back(alloc(E));
+    std::vector<bool> has_w(m, false), has_g(n, false);
+    for (int i = 0; i < m_out; ++i) {
+        has_w[i] = host_seeds && host_seeds[i];
+        w.push_back(alloc(has_w[i] ? E : 1));
+    }
+    for (int j = 0; j < n_in; ++j) {
+        has_g[j] = host_grads && host_grads[j];
+        g.push_back(alloc(has_g[j] ? volume(shapes[j]) : 1));
+    }
+    const int64_t rows = (B + chunks - 1) / chunks, last = B - (chunks - 1) * rows;
+    // one zeroed workspace per distinct chunk shape (layouts differ by shape)
+    std::vector<std::unique_ptr<detail::DeviceBuffer>> ws;
+    std::size_t ws_bytes[2] = {0, 0};
+    for (int q = 0; q < (last == rows ? 1 : 2); ++q) {
+        std::vector<bcad_cu_shape> cs(shapes, shapes + n_in);
+        for (int j = 0; j < n_in; ++j)
+            if (split[j]) cs[j].dims[0] = q == 0 ? rows : last;
+        check(bcad_cu_pullback_workspace(k, dt, n_in, cs.data(), m_out, &ws_bytes[q]));
+        ws.push_back(std::make_unique<detail::DeviceBuffer>(ws_bytes[q], comp));
+        check(bcad_cu_memset(ws.back()->ptr, 0, ws_bytes[q], comp));
+    }
+    for (int j = 0; j < n_in; ++j)  // batch-broadcast inputs: whole, on the compute stream
+        if (!split[j]) check(bcad_cu_memcpy(x[j].device_data(), host_in[j], x[j].bytes(), 0, comp));
+    check(bcad_cu_event_record(P.fork, comp));
+    check(bcad_cu_stream_wait_event(P.h2d, P.fork));
+    check(bcad_cu_stream_wait_event(P.d2h, P.fork));
+
+    std::vector<bcad_cu_shape> cs(shapes, shapes + n_in);
+    std::vector<const void*> xin(n), wp(m), Dp(m * n);
+    std::vector<void*> yp(m), Dw(m * n), gp(n);
+    std::vector<unsigned char> acc(n, 0);
+    int c = 0;
+    for (int64_t b0 = 0; b0 < B; b0 += rows, ++c) {
+        const int64_t b1 = std::min(B, b0 + rows), r = b1 - b0;
+        const std::size_t cell0 = static_cast<std::size_t>(b0 * out_row), cells = static_cast<std::size_t>(r * out_row);
+        // h2d: this chunk's rows of the batch-sharded inputs and of the seeds
+        for (int j = 0; j < n_in; ++j) {
+            if (!split[j]) continue;
+            const std::size_t o = static_cast<std::size_t>(b0 * row_elems[j]), cnt = static_cast<std::size_t>(r * row_elems[j]);
+            check(bcad_cu_memcpy(x[j].device_data() + o, static_cast<const Real*>(host_in[j]) + o, cnt * sizeof(Real), 0, P.h2d));
+        }
+        for (int i = 0; i < m_out; ++i)
+            if (has_w[i])
+                check(bcad_cu_memcpy(w[i].device_data() + cell0, static_cast<const Real*>(host_seeds[i]) + cell0,
+                                     cells * sizeof(Real), 0, P.h2d));
+        check(bcad_cu_event_record(P.in_ready[c], P.h2d));
+        // compute: K1 then K2 on the chunk (row-offset views of the buffers)
+        check(bcad_cu_stream_wait_event(comp, P.in_ready[c]));
+        for (int j = 0; j < n_in; ++j) {
+            const int64_t o = split[j] ? b0 * row_elems[j] : 0;
+            xin[j] = x[j].device_data() + o;
+            cs[j] = shapes[j];
+            if (split[j]) cs[j].dims[0] = r;
+            gp[j] = has_g[j] ? static_cast<void*>(g[j].device_data() + o) : nullptr;
+            acc[j] = (!split[j] && c > 0) ? 1 : 0;
+        }
+        for (int i = 0; i < m_out; ++i) {
+            yp[i] = y[i].device_data() + cell0;
+            wp[i] = has_w[i] ? static_cast<const void*>(w[i].device_data() + cell0) : nullptr;
+        }
+        for (std::size_t t = 0; t < D.size(); ++t) {
+            Dw[t] = D[t].device_data() + cell0;
+            Dp[t] = Dw[t];
+        }
+        check(bcad_cu_forward(k, dt, n_in, xin.data(), cs.data(), m_out, yp.data(), policy == 0 ? Dw.data() : nullptr, comp));
+        check(bcad_cu_pullback(k, dt, n_in, cs.data(), m_out, wp.data(), policy == 0 ? Dp.data() : nullptr, xin.data(),
+                               gp.data(), acc.data(), ws[r == rows ? 0 : 1]->ptr, ws_bytes[r == rows ? 0 : 1], comp));
+        check(bcad_cu_event_record(P.out_ready[c], comp));
+        // d2h: the chunk's primal rows and batch-sharded gradient rows
+        check(bcad_cu_stream_wait_event(P.d2h, P.out_ready[c]));
+        for (int i = 0; i < m_out; ++i)
+            if (host_primal && host_primal[i])
+                check(bcad_cu_memcpy(static_cast<Real*>(host_primal[i]) + cell0, y[i].device_data() + cell0,
+                                     cells * sizeof(Real), 1, P.d2h));
+        for (int j = 0; j < n_in; ++j) {
+            if (!split[j] || !has_g[j]) continue;
+            const std::size_t o = static_cast<std::size_t>(b0 * row_elems[j]), cnt = static_cast<std::size_t>(r * row_elems[j]);
+            check(bcad_cu_memcpy(static_cast<Real*>(host_grads[j]) + o, g[j].device_data() + o, cnt * sizeof(Real), 1, P.d2h));
+        }
+    }
+    check(bcad_cu_event_record(P.join, P.d2h));
+    check(bcad_cu_stream_wait_event(comp, P.join));
+    for (int j = 0; j < n_in; ++j)
+        if (!split[j] && has_g[j]) check(bcad_cu_memcpy(host_grads[j], g[j].device_data(), g[j].bytes(), 1, comp));
+    check(bcad_cu_stream_synchronize(comp));
+    // what the one-shot tape reports (tape.hpp:236-243): inputs + values + cache
+    return (in_elems + int64_t(m) * E + (policy == 0 ? int64_t(m * n) * E : 0)) * int64_t(sizeof(Real));
+}
+
+template <class Real>
+void step(const char* name, int n_in, const void* const* host_in, const bcad_cu_shape* shapes, int m_out,
+          int policy, const void* const* host_seeds, void* const* host_primal, void* const* host_grads,
+          int64_t* peak) {
+    using namespace bcad;
+    bcad_cu_kernel k = nullptr;
+    check(bcad_cu_kernel_lookup(name, n_in, m_out, &k));
+    bcad_cu_shape out{};
+    check(bcad_cu_broadcast_shape(n_in, shapes, &out));
+    std::vector<bool> split(static_cast<std::size_t>(n_in), false);
+    for (int j = 0; j < n_in; ++j) split[j] = shapes[j].rank > 0 && out.rank > 0 && shapes[j].dims[0] == out.dims[0];
+    const int chunks = plan_chunks(k, n_in, shapes, out, m_out, sizeof(Real), host_seeds, host_primal, host_grads, split);
+    int64_t p = 0;
+    if (chunks == 1) {
+        p = tape_step<Real>(name, n_in, host_in, shapes, m_out, policy, host_seeds, host_primal, host_grads);
+        check(bcad_cu_stream_synchronize(current_stream()));
+    } else {
+        p = pipelined_step<Real>(k, n_in, host_in, shapes, m_out, policy, host_seeds, host_primal, host_grads, out, split,
+                                 chunks);
+    }
+    if (peak) *peak = p;
 }
 
 template <class Real>
@@ -104,6 +323,16 @@ int bcad_host_cell_gradients(int impl, int dtype, int64_t n, const void* const* 
 }
 
 const char* bcad_host_last_error(void) { return g_err.c_str(); }
+
+int bcad_host_set_pipeline(int max_chunks) {
+    if (max_chunks < 0) {
+        g_err = "bcad_host_set_pipeline: max_chunks must be >= 0";
+        return BCAD_CU_ERR_CONFIG;
+    }
+    const int prev = g_pipeline.exchange(max_chunks);
+    (void)prev;
+    return BCAD_CU_OK;
+}
 
 int bcad_host_mixed_step(const char* kernel, int dtype, int n_in, const void* const* host_in,
                          const bcad_cu_shape* in_shapes, int m_out, int policy, const void* const* host_seeds,

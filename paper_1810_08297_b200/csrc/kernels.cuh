@@ -312,7 +312,6 @@ __global__ void __launch_bounds__(kThreads) fwd2d_kernel(const __grid_constant__
         } else {
             Pack<T, V> y[M];
             Pack<T, V> d[M * N];
-#pragma unroll
             eval_cells<Body, T, V, S>(x, y, d, p.err, off);
 #pragma unroll
             for (int i = 0; i < M; ++i) {
@@ -353,21 +352,49 @@ struct Pull2DParams {
     unsigned long long* err;
 };
 
-// sum_{q < n} base[q * stride], added strictly in q order (deterministic),
-// with the loads issued eight at a time from L2 (__ldcg: partials written by
-// other CTAs) so the dependent adds do not serialise the memory latency.
-__device__ __forceinline__ double ordered_sum(const double* base, int n, size_t stride) {
-    double s = 0.0;
-    int q = 0;
-    for (; q + 8 <= n; q += 8) {
-        double v[8];
-#pragma unroll
-        for (int u = 0; u < 8; ++u) v[u] = __ldcg(base + size_t(q + u) * stride);
-#pragma unroll
-        for (int u = 0; u < 8; ++u) s += v[u];
+// Last-CTA combination of cross-CTA fp64 partials, all threads of the CTA:
+// item `it` needs sum_{q < n} part(it)[q * stride]. Each item's n partials
+// are cut into G contiguous groups (G chosen so items x G covers the CTA a
+// few times); a thread sums one (item, group) unit with its loads issued 16
+// at a time from L2 (__ldcg: written by other CTAs), the group sums land in
+// shared memory, and the item's result adds them in group order. The
+// association is fixed by (n, n_items), so results are bitwise run-to-run
+// deterministic. `scratch` holds at least n_items * G doubles (G <= 8).
+template <class Base, class Fin>
+__device__ __forceinline__ void cta_combine(int n_items, int n, size_t stride, double* scratch, int scratch_cap,
+                                            Base base, Fin fin) {
+    // G minimises the per-thread count of dependent 16-load batches
+    int G = 1, best = 0x7fffffff;
+    for (int g = 1; g <= 8; g *= 2) {
+        if (g > 1 && n_items * g > scratch_cap) break;
+        const int batches = ((n_items * g + kThreads - 1) / kThreads) * (((n + g - 1) / g + 15) / 16);
+        if (batches < best) best = batches, G = g;
     }
-    for (; q < n; ++q) s += __ldcg(base + size_t(q) * stride);
-    return s;
+    const int per = (n + G - 1) / G;
+    for (int u = threadIdx.x; u < n_items * G; u += kThreads) {
+        const int it = u / G, grp = u % G;
+        const double* b = base(it);
+        const int q0 = grp * per, q1 = min(n, q0 + per);
+        double acc = 0.0;
+        int q = q0;
+        for (; q + 16 <= q1; q += 16) {
+            double v[16];
+#pragma unroll
+            for (int k = 0; k < 16; ++k) v[k] = __ldcg(b + size_t(q + k) * stride);
+#pragma unroll
+            for (int k = 0; k < 16; ++k) acc += v[k];
+        }
+        for (; q < q1; ++q) acc += __ldcg(b + size_t(q) * stride);
+        if (G == 1) fin(it, acc);
+        else scratch[u] = acc;
+    }
+    if (G == 1) return;
+    __syncthreads();
+    for (int it = threadIdx.x; it < n_items; it += kThreads) {
+        double acc = 0.0;
+        for (int grp = 0; grp < G; ++grp) acc += scratch[it * G + grp];
+        fin(it, acc);
+    }
 }
 
 template <class T>
@@ -387,7 +414,7 @@ __host__ __device__ inline size_t pull_smem_doubles(int n_col, int n_row, int n_
 // (mixed.hpp:34-38); FULL slots get the reference's element arithmetic,
 // reduced slots an fp64 sum of those terms in a fixed order.
 template <class Body, class T, int V, bool kRecompute, class S, bool kDense>
-__global__ void __launch_bounds__(kThreads, kRecompute ? 1 : kCtasPerSm) pull2d_kernel(const __grid_constant__ Pull2DParams<Body::kIn, Body::kOut, T> p) {
+__global__ void __launch_bounds__(kThreads, kRecompute ? 2 : kCtasPerSm) pull2d_kernel(const __grid_constant__ Pull2DParams<Body::kIn, Body::kOut, T> p) {
     constexpr int N = Body::kIn, M = Body::kOut;
     constexpr bool kAnyRow = !S::kStatic || S::has(kRow);
     constexpr bool kAnyCol = !S::kStatic || S::has(kCol);
@@ -587,6 +614,7 @@ __global__ void __launch_bounds__(kThreads, kRecompute ? 1 : kCtasPerSm) pull2d_
                 }
             }
         }
+        const int smem_cap = int(pull_smem_doubles(p.n_col_args, p.n_row_args, p.n_scalar_args, V, p.rpt, p.ty, wpr));
         const bool need_row = kAnyRow && p.n_row_args > 0 && p.n_col_tiles > 1;
         const bool need_col = kAnyCol && p.n_col_args > 0 && p.n_row_tiles > 1;
         const bool need_scal = kAnyScal && p.n_scalar_args > 0 && n_ctas > 1;
@@ -602,15 +630,15 @@ __global__ void __launch_bounds__(kThreads, kRecompute ? 1 : kCtasPerSm) pull2d_
             if (s_last) {
                 __threadfence();
                 const int64_t rb = int64_t(rt) * p.tile_rows;
-                const int64_t nr = min(p.tile_rows, p.rows - rb);
-                for (int64_t item = tid; item < p.n_row_args * nr; item += kThreads) {
-                    const int a = int(item / nr);
-                    const int64_t r = rb + item % nr;
-                    double sacc = 0.0;
-                    sacc = ordered_sum(p.ws_row + size_t(a) * p.n_col_tiles * p.rows + r, p.n_col_tiles, size_t(p.rows));
-                    const int j = p.row_j[a];
-                    p.adj[j][r] = finish<T>(sacc, p.adj[j] + r, (p.acc_mask >> j) & 1u);
-                }
+                const int nr = int(min(p.tile_rows, p.rows - rb));
+                cta_combine(
+                    p.n_row_args * nr, p.n_col_tiles, size_t(p.rows), smem, smem_cap,
+                    [&](int it) { return p.ws_row + size_t(it / nr) * p.n_col_tiles * p.rows + rb + it % nr; },
+                    [&](int it, double sacc) {
+                        const int j = p.row_j[it / nr];
+                        const int64_t r = rb + it % nr;
+                        p.adj[j][r] = finish<T>(sacc, p.adj[j] + r, (p.acc_mask >> j) & 1u);
+                    });
                 if (tid == 0) p.counters[rt] = 0;
             }
             __syncthreads();
@@ -620,15 +648,16 @@ __global__ void __launch_bounds__(kThreads, kRecompute ? 1 : kCtasPerSm) pull2d_
             __syncthreads();
             if (s_last) {
                 __threadfence();
-                for (int item = tid; item < p.n_col_args * ccols; item += kThreads) {
-                    const int a = item / ccols;
-                    const int64_t c = int64_t(ct) * ccols + item % ccols;
-                    if (c >= p.cols) continue;
-                    double sacc = 0.0;
-                    sacc = ordered_sum(p.ws_col + size_t(a) * p.n_row_tiles * p.cols + c, p.n_row_tiles, size_t(p.cols));
-                    const int j = p.col_j[a];
-                    p.adj[j][c] = finish<T>(sacc, p.adj[j] + c, (p.acc_mask >> j) & 1u);
-                }
+                const int64_t cb = int64_t(ct) * ccols;
+                const int nc = int(min(int64_t(ccols), p.cols - cb));
+                cta_combine(
+                    p.n_col_args * nc, p.n_row_tiles, size_t(p.cols), smem, smem_cap,
+                    [&](int it) { return p.ws_col + size_t(it / nc) * p.n_row_tiles * p.cols + cb + it % nc; },
+                    [&](int it, double sacc) {
+                        const int j = p.col_j[it / nc];
+                        const int64_t c = cb + it % nc;
+                        p.adj[j][c] = finish<T>(sacc, p.adj[j] + c, (p.acc_mask >> j) & 1u);
+                    });
                 if (tid == 0) p.counters[p.n_row_tiles + ct] = 0;
             }
             __syncthreads();

@@ -92,7 +92,7 @@ int launch_fwd_t(const FwdArgs& a, std::string* err) {
             if (a.partials[i * N + j] && !aligned16(a.partials[i * N + j])) vec = false;
     }
     if (vec) {
-        const Tiling t = choose_tiling(plan, V, ClassMix{}, /*fine=*/true);  // no reductions in K1: wide row tiles
+        const Tiling t = a.tiling ? *a.tiling : choose_tiling(plan, V, ClassMix{}, /*fine=*/true);  // no reductions in K1: wide row tiles
         bcad_dev::Fwd2DParams<N, M, T> p{};
         for (int j = 0; j < N; ++j) {
             p.in[j] = static_cast<const T*>(a.in[j]);
@@ -161,7 +161,7 @@ int launch_pull_t(const PullArgs& a, std::string* err) {
         if ((plan.cls[j] == kFull || plan.cls[j] == kCol) && !aligned16(a.in[j])) vec = false;
 
     if (vec) {
-        const Tiling t = choose_tiling(plan, V, class_mix(plan));
+        const Tiling t = a.tiling ? *a.tiling : choose_tiling(plan, V, class_mix(plan));
         const PullLayout L = pull_layout(plan, t);  // offsets sized for every argument
         if (a.ws_bytes < L.total || (L.total > 0 && !a.workspace)) {
             *err = "pullback workspace too small: need " + std::to_string(L.total) + " bytes";

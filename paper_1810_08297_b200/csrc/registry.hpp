@@ -20,6 +20,7 @@ struct FwdArgs {
     cudaStream_t stream;
     unsigned long long* err;
     const Plan* plan;
+    const Tiling* tiling = nullptr;  // tuning override (tests / scripts/lab); null = choose_tiling
 };
 
 struct PullArgs {
@@ -34,6 +35,7 @@ struct PullArgs {
     cudaStream_t stream;
     unsigned long long* err;
     const Plan* plan;
+    const Tiling* tiling = nullptr;  // tuning override (tests / scripts/lab); null = choose_tiling
 };
 
 size_t pull_ws_any(const Plan& plan, int dtype);

@@ -21,10 +21,20 @@ def _load():
     lib.bcad_host_mixed_step.restype = C.c_int
     lib.bcad_host_mixed_step.argtypes = [C.c_char_p, C.c_int, C.c_int, C.c_void_p, C.c_void_p, C.c_int, C.c_int,
                                          C.c_void_p, C.c_void_p, C.c_void_p, C.POINTER(C.c_int64), C.c_void_p]
+    lib.bcad_host_set_pipeline.restype = C.c_int
+    lib.bcad_host_set_pipeline.argtypes = [C.c_int]
     return lib
 
 
 LIB = _load()
+
+
+def set_pipeline(max_chunks: int) -> None:
+    """bcad_host_set_pipeline: 0 automatic row-chunk pipelining of the host
+    step, 1 off, k > 1 at most k chunks."""
+    rc = LIB.bcad_host_set_pipeline(int(max_chunks))
+    if rc:
+        raise native._BY_CODE.get(rc, native.Error)(LIB.bcad_host_last_error().decode())
 
 
 def _ptrs(arrs):

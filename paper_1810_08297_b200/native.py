@@ -138,6 +138,10 @@ PROTOS = {
     "bcad_cu_stream_destroy": (I, [VP]),
     "bcad_cu_stream_synchronize": (I, [VP]),
     "bcad_cu_device_synchronize": (I, []),
+    "bcad_cu_event_create": (I, [C.POINTER(VP)]),
+    "bcad_cu_event_destroy": (I, [VP]),
+    "bcad_cu_event_record": (I, [VP, VP]),
+    "bcad_cu_stream_wait_event": (I, [VP, VP]),
     "bcad_cu_nccl_unique_id": (I, [C.c_char_p]),
     "bcad_cu_comm_init": (I, [C.POINTER(VP), I, C.c_char_p, I]),
     "bcad_cu_comm_destroy": (I, [VP]),

@@ -1,0 +1,387 @@
+// Dev tuning harness (not part of the product): times the HM-LSTM K1 / K2
+// kernels on one GPU under explicit tilings and checks every variant's
+// outputs bit-for-bit against the default tiling's. Build + run with
+// scripts/lab/run.sh under gpurun. Prints one JSON object per line.
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <functional>
+#include <string>
+#include <vector>
+
+#include "bodies.cuh"
+#include "launch.cuh"
+
+using namespace bcad_cu_impl;
+
+#define CK(x)                                                                              \
+    do {                                                                                   \
+        cudaError_t e_ = (x);                                                              \
+        if (e_ != cudaSuccess) {                                                           \
+            std::fprintf(stderr, "%s:%d %s: %s\n", __FILE__, __LINE__, #x, cudaGetErrorString(e_)); \
+            std::exit(1);                                                                  \
+        }                                                                                  \
+    } while (0)
+
+__device__ uint32_t hash32(uint32_t x) {
+    x ^= x >> 16; x *= 0x7feb352du; x ^= x >> 15; x *= 0x846ca68bu; x ^= x >> 16;
+    return x;
+}
+template <class T>
+__global__ void init_kernel(T* p, size_t n, uint32_t seed, int binary) {
+    for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n; i += size_t(gridDim.x) * blockDim.x) {
+        const uint32_t h = hash32(uint32_t(i) * 2654435761u ^ seed);
+        p[i] = binary ? T(h & 1u) : T(double(h) / 4294967296.0 * 2.0 - 1.0);
+    }
+}
+__global__ void read_kernel(const float4* p, size_t n, float* out) {
+    float s = 0.f;
+    for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n; i += size_t(gridDim.x) * blockDim.x) {
+        const float4 v = __ldcs(p + i);
+        s += v.x + v.y + v.z + v.w;
+    }
+    if (s == 1234.5f) *out = s;
+}
+// memory-only floor of K1's access pattern: read c,f,i,g (+ z per row), write 7 tensors
+__global__ void copy_floor_kernel(const float4* c, const float4* f, const float4* i, const float4* g, const float* z1,
+                                  const float* z2, float4* const* outs, int vcols, size_t nvec) {
+    for (size_t k = blockIdx.x * size_t(blockDim.x) + threadIdx.x; k < nvec; k += size_t(gridDim.x) * blockDim.x) {
+        const size_t r = k / vcols;
+        const float a = __ldg(z1 + r) + __ldg(z2 + r);
+        float4 x = __ldcs(c + k), y = __ldcs(f + k), u = __ldcs(i + k), w = __ldcs(g + k);
+        float4 o0 = make_float4(x.x + a, x.y, x.z, x.w), o1 = make_float4(y.x + a, y.y, y.z, y.w);
+        float4 o2 = make_float4(u.x, u.y + a, u.z, u.w), o3 = make_float4(w.x, w.y, w.z + a, w.w);
+        outs[0][k] = o0; outs[1][k] = o1; outs[2][k] = o2; outs[3][k] = o3;
+        outs[4][k] = make_float4(a, a, a, a); outs[5][k] = make_float4(a, 0, a, 0); outs[6][k] = o0;
+    }
+}
+
+struct Flush {
+    float* buf = nullptr;
+    float* sink = nullptr;
+    size_t n = size_t(256) << 20;  // 1 GiB of floats
+    Flush() {
+        CK(cudaMalloc(&buf, n * 4));
+        CK(cudaMalloc(&sink, 4));
+    }
+    void operator()(cudaStream_t s) {
+        CK(cudaMemsetAsync(buf, 1, n * 4, s));
+        read_kernel<<<148 * 8, 256, 0, s>>>(reinterpret_cast<const float4*>(buf), n / 4, sink);
+    }
+};
+
+static Flush* g_flush;
+static cudaStream_t g_s;
+
+double time_us(const std::function<void()>& fn, int reps = 25) {
+    std::vector<cudaEvent_t> a(reps), b(reps);
+    for (int k = 0; k < reps; ++k) {
+        CK(cudaEventCreate(&a[k]));
+        CK(cudaEventCreate(&b[k]));
+    }
+    for (int k = 0; k < 3; ++k) {
+        (*g_flush)(g_s);
+        fn();
+    }
+    for (int k = 0; k < reps; ++k) {
+        (*g_flush)(g_s);
+        CK(cudaEventRecord(a[k], g_s));
+        fn();
+        CK(cudaEventRecord(b[k], g_s));
+    }
+    CK(cudaStreamSynchronize(g_s));
+    std::vector<double> t(reps);
+    for (int k = 0; k < reps; ++k) {
+        float ms;
+        CK(cudaEventElapsedTime(&ms, a[k], b[k]));
+        t[k] = ms * 1e3;
+        cudaEventDestroy(a[k]);
+        cudaEventDestroy(b[k]);
+    }
+    std::sort(t.begin(), t.end());
+    return t[reps / 2];
+}
+
+template <class T>
+struct Problem {
+    int n;
+    int64_t B, H;
+    std::vector<bcad_cu_shape> shapes;
+    std::vector<T*> in, partials, adj;
+    T* primal = nullptr;
+    T* w = nullptr;
+    void* ws = nullptr;
+    size_t ws_bytes = size_t(256) << 20;
+    unsigned long long* err = nullptr;
+    Plan plan;
+    size_t step_bytes = 0, k1_bytes = 0, k2_bytes = 0;
+
+    static bcad_cu_shape shp(std::initializer_list<int64_t> d) {
+        bcad_cu_shape s{};
+        s.rank = int(d.size());
+        int k = 0;
+        for (int64_t x : d) s.dims[k++] = x;
+        return s;
+    }
+    static int64_t vol(const bcad_cu_shape& s) {
+        int64_t v = 1;
+        for (int k = 0; k < s.rank; ++k) v *= s.dims[k];
+        return v;
+    }
+    Problem(bool bias, int64_t B_, int64_t H_) : B(B_), H(H_) {
+        for (int k = 0; k < 4; ++k) shapes.push_back(shp({B, H}));
+        if (bias)
+            for (int k = 0; k < 3; ++k) shapes.push_back(shp({1, H}));
+        shapes.push_back(shp({B}));
+        shapes.push_back(shp({B}));
+        n = int(shapes.size());
+        const int64_t E = B * H;
+        size_t in_elems = 0;
+        for (int j = 0; j < n; ++j) {
+            T* p;
+            CK(cudaMalloc(&p, vol(shapes[j]) * sizeof(T)));
+            init_kernel<<<1024, 256>>>(p, vol(shapes[j]), 77u + 13u * j, j >= n - 2);
+            in.push_back(p);
+            in_elems += vol(shapes[j]);
+            T* d;
+            CK(cudaMalloc(&d, E * sizeof(T)));
+            partials.push_back(d);
+            T* a;
+            CK(cudaMalloc(&a, vol(shapes[j]) * sizeof(T)));
+            adj.push_back(a);
+        }
+        CK(cudaMalloc(&primal, E * sizeof(T)));
+        CK(cudaMalloc(&w, E * sizeof(T)));
+        init_kernel<<<1024, 256>>>(w, E, 999u, 0);
+        CK(cudaMalloc(&ws, ws_bytes));
+        CK(cudaMemset(ws, 0, ws_bytes));
+        CK(cudaMalloc(&err, 8));
+        CK(cudaMemset(err, 0xff, 8));
+        std::string e;
+        make_plan(n, shapes.data(), &plan, &e);
+        k1_bytes = (in_elems + E + size_t(n) * E) * sizeof(T);
+        k2_bytes = (E + size_t(n) * E + in_elems) * sizeof(T);
+        step_bytes = k1_bytes + k2_bytes;
+        CK(cudaDeviceSynchronize());
+    }
+};
+
+template <class Body, class T, class Sig>
+int fwd(Problem<T>& P, const Tiling* t) {
+    std::vector<const void*> in(P.in.begin(), P.in.end());
+    void* prim[1] = {P.primal};
+    std::vector<void*> parts(P.partials.begin(), P.partials.end());
+    FwdArgs a{};
+    a.dtype = sizeof(T) == 4 ? BCAD_CU_F32 : BCAD_CU_F64;
+    a.in = in.data();
+    a.primal = prim;
+    a.partials = parts.data();
+    a.stream = g_s;
+    a.err = P.err;
+    a.plan = &P.plan;
+    a.tiling = t;
+    std::string e;
+    const int rc = launch_fwd_t<Body, T, Sig>(a, &e);
+    if (rc) std::fprintf(stderr, "fwd rc %d %s\n", rc, e.c_str());
+    return rc;
+}
+
+template <class Body, class T, class Sig>
+int pull(Problem<T>& P, const Tiling* t) {
+    std::vector<const void*> in(P.in.begin(), P.in.end());
+    const void* w[1] = {P.w};
+    std::vector<const void*> parts(P.partials.begin(), P.partials.end());
+    std::vector<void*> adj(P.adj.begin(), P.adj.end());
+    PullArgs a{};
+    a.dtype = sizeof(T) == 4 ? BCAD_CU_F32 : BCAD_CU_F64;
+    a.out_adj = w;
+    a.partials = parts.data();
+    a.in = in.data();
+    a.in_adj = adj.data();
+    a.accumulate = nullptr;
+    a.workspace = P.ws;
+    a.ws_bytes = P.ws_bytes;
+    a.stream = g_s;
+    a.err = P.err;
+    a.plan = &P.plan;
+    a.tiling = t;
+    std::string e;
+    const int rc = launch_pull_t<Body, T, Sig>(a, &e);
+    if (rc) std::fprintf(stderr, "pull rc %d %s\n", rc, e.c_str());
+    return rc;
+}
+
+template <class T>
+std::vector<std::vector<T>> snapshot(const std::vector<T*>& ptrs, const std::vector<size_t>& n) {
+    CK(cudaStreamSynchronize(g_s));
+    std::vector<std::vector<T>> out;
+    for (size_t k = 0; k < ptrs.size(); ++k) {
+        out.emplace_back(n[k]);
+        CK(cudaMemcpy(out.back().data(), ptrs[k], n[k] * sizeof(T), cudaMemcpyDeviceToHost));
+    }
+    return out;
+}
+
+Tiling make_tiling(const Plan& p, int V, int txv, int rpt, int cy) {
+    Tiling t;
+    t.V = V;
+    t.vcols = p.cols / V;
+    t.txv = txv;
+    t.ty = kThreads / txv;
+    t.n_col_tiles = ceil_div(t.vcols, txv);
+    t.rpt = rpt;
+    t.tile_rows = int64_t(t.ty) * rpt;
+    t.n_row_tiles = ceil_div(p.rows, t.tile_rows);
+    (void)cy;
+    t.n_ctas = t.n_row_tiles * t.n_col_tiles;
+    return t;
+}
+
+void print_tiling(const char* tag, const char* variant, int64_t B, int64_t H, const Tiling& t, double us, double bytes,
+                  bool same) {
+    std::printf("{\"exp\": \"%s\", \"variant\": \"%s\", \"B\": %lld, \"H\": %lld, \"txv\": %d, \"ty\": %d, \"rpt\": %d, "
+                "\"cy\": %d, \"grid\": [%lld, %lld], \"us\": %.3f, \"GBps\": %.1f, \"bitexact\": %s}\n",
+                tag, variant, (long long)B, (long long)H, t.txv, t.ty, t.rpt, 1, (long long)t.n_col_tiles,
+                (long long)t.n_row_tiles, us, bytes / (us * 1e-6) / 1e9, same ? "true" : "false");
+    std::fflush(stdout);
+}
+
+template <class Body, class T, class Sig>
+void k1_sweep(const char* tag, bool bias, int64_t B, int64_t H, const std::vector<std::array<int, 2>>& tilings) {
+    Problem<T> P(bias, B, H);
+    constexpr int V = vec_width<T>();
+    const Tiling def = choose_tiling(P.plan, V, ClassMix{}, true);
+    fwd<Body, T, Sig>(P, &def);
+    std::vector<T*> outs(P.partials.begin(), P.partials.end());
+    outs.push_back(P.primal);
+    std::vector<size_t> ns(outs.size(), size_t(B * H));
+    const auto ref = snapshot(outs, ns);
+    double us = time_us([&] { fwd<Body, T, Sig>(P, &def); });
+    print_tiling(tag, "default", B, H, def, us, double(P.k1_bytes), true);
+    for (auto [txv, rpt] : tilings) {
+        const Tiling t = make_tiling(P.plan, V, txv, rpt, 1);
+        if (t.n_row_tiles > 65535) continue;
+        CK(cudaMemset(P.primal, 0, B * H * sizeof(T)));
+        fwd<Body, T, Sig>(P, &t);
+        const bool same = snapshot(outs, ns) == ref;
+        us = time_us([&] { fwd<Body, T, Sig>(P, &t); });
+        print_tiling(tag, "tiled", B, H, t, us, double(P.k1_bytes), same);
+    }
+    if constexpr (sizeof(T) == 4) {
+        if (!bias) {  // memory-only floor of the same access pattern
+            float4** d_outs;
+            CK(cudaMalloc(&d_outs, 7 * sizeof(float4*)));
+            std::vector<float4*> h(7);
+            for (int k = 0; k < 6; ++k) h[k] = reinterpret_cast<float4*>(P.partials[k]);
+            h[6] = reinterpret_cast<float4*>(P.primal);
+            CK(cudaMemcpy(d_outs, h.data(), 7 * sizeof(float4*), cudaMemcpyHostToDevice));
+            const size_t nvec = size_t(B * H / 4);
+            for (int blocks : {148 * 4, 148 * 8, int((nvec + 255) / 256)}) {
+                us = time_us([&] {
+                    copy_floor_kernel<<<blocks, 256, 0, g_s>>>(
+                        reinterpret_cast<const float4*>(P.in[0]), reinterpret_cast<const float4*>(P.in[1]),
+                        reinterpret_cast<const float4*>(P.in[2]), reinterpret_cast<const float4*>(P.in[3]),
+                        reinterpret_cast<const float*>(P.in[4]), reinterpret_cast<const float*>(P.in[5]), d_outs,
+                        int(H / 4), nvec);
+                });
+                std::printf("{\"exp\": \"%s\", \"variant\": \"copy_floor\", \"blocks\": %d, \"us\": %.3f, \"GBps\": %.1f}\n",
+                            tag, blocks, us, double(P.k1_bytes) / (us * 1e-6) / 1e9);
+            }
+            CK(cudaFree(d_outs));
+        }
+    }
+}
+
+template <class Body, class T, class Sig>
+void k2_sweep(const char* tag, bool bias, int64_t B, int64_t H, const std::vector<std::array<int, 3>>& tilings) {
+    Problem<T> P(bias, B, H);
+    constexpr int V = vec_width<T>();
+    const Tiling fdef = choose_tiling(P.plan, V, ClassMix{}, true);
+    fwd<Body, T, Sig>(P, &fdef);
+    const Tiling def = choose_tiling(P.plan, V, class_mix(P.plan));
+    pull<Body, T, Sig>(P, &def);
+    std::vector<size_t> ns;
+    for (auto& s : P.shapes) ns.push_back(size_t(Problem<T>::vol(s)));
+    const auto ref = snapshot(P.adj, ns);
+    double us = time_us([&] { pull<Body, T, Sig>(P, &def); });
+    print_tiling(tag, "default", B, H, def, us, double(P.k2_bytes), true);
+    for (auto [txv, rpt, cy] : tilings) {
+        const Tiling t = make_tiling(P.plan, V, txv, rpt, cy);
+        if (t.n_row_tiles > 65535) continue;
+        for (T* a : P.adj) CK(cudaMemset(a, 0, sizeof(T)));
+        CK(cudaMemset(P.ws, 0, P.ws_bytes));  // layouts differ per tiling
+        pull<Body, T, Sig>(P, &t);
+        const auto got = snapshot(P.adj, ns);
+        bool same = true;  // full-shape adjoints bit-exact; reduced ones within 1e-12 relative (other order)
+        for (size_t k = 0; k < got.size() && same; ++k)
+            for (size_t e = 0; e < got[k].size() && same; ++e) {
+                const double x = got[k][e], y = ref[k][e];
+                if (ns[k] == size_t(B * H) ? x != y : std::abs(x - y) > 1e-5 * std::max(std::abs(x), std::abs(y)) + 1e-30)
+                    same = false;
+            }
+        us = time_us([&] { pull<Body, T, Sig>(P, &t); });
+        print_tiling(tag, "tiled", B, H, t, us, double(P.k2_bytes), same);
+    }
+}
+
+// Run-to-run bit determinism of K2 under a tiling (reduced adjoints included).
+template <class Body, class T, class Sig>
+void k2_det(const char* tag, bool bias, int64_t B, int64_t H, int cy_override, int reps) {
+    Problem<T> P(bias, B, H);
+    constexpr int V = vec_width<T>();
+    const Tiling fdef = choose_tiling(P.plan, V, ClassMix{}, true);
+    fwd<Body, T, Sig>(P, &fdef);
+    Tiling t = choose_tiling(P.plan, V, class_mix(P.plan));
+    if (cy_override >= 1) t = make_tiling(P.plan, V, t.txv, t.rpt, cy_override);
+    std::vector<size_t> ns;
+    for (auto& s : P.shapes) ns.push_back(size_t(Problem<T>::vol(s)));
+    pull<Body, T, Sig>(P, &t);
+    const auto ref = snapshot(P.adj, ns);
+    int bad = 0;
+    for (int k = 0; k < reps; ++k) {
+        pull<Body, T, Sig>(P, &t);
+        if (snapshot(P.adj, ns) != ref) ++bad;
+    }
+    const double us = time_us([&] { pull<Body, T, Sig>(P, &t); }, 10);
+    std::printf("{\"exp\": \"%s\", \"B\": %lld, \"H\": %lld, \"cy\": %d, \"rpt\": %d, \"grid\": [%lld, %lld], "
+                "\"nondeterministic_runs\": %d, \"of\": %d, \"us\": %.3f, \"GBps\": %.1f}\n",
+                tag, (long long)B, (long long)H, 1, t.rpt, (long long)t.n_col_tiles, (long long)t.n_row_tiles, bad,
+                reps, us, double(P.k2_bytes) / (us * 1e-6) / 1e9);
+    std::fflush(stdout);
+}
+
+int main(int argc, char** argv) {
+    const std::string which = argc > 1 ? argv[1] : "all";
+    CK(cudaSetDevice(0));
+    CK(cudaStreamCreateWithFlags(&g_s, cudaStreamNonBlocking));
+    g_flush = new Flush();
+    using namespace bcad_dev;
+    if (which == "all" || which == "k1") {
+        const std::vector<std::array<int, 2>> t1 = {{256, 1}, {256, 2}, {128, 1}, {128, 2}, {64, 1}, {64, 2},
+                                                     {32, 1}, {32, 2}, {32, 4}};
+        k1_sweep<KHmlstm, float, SigHmlstmCanonical>("k1_cfg2", false, 1024, 1024, t1);
+        k1_sweep<KHmlstmBias, float, SigHmlstmBias>("k1_cfg3", true, 1024, 1024, t1);
+    }
+    if (which == "all" || which == "k2") {
+        const std::vector<std::array<int, 3>> t2 = {{256, 1, 1}, {256, 2, 1}, {128, 1, 1}, {128, 2, 1},
+                                                     {64, 1, 1}, {32, 1, 1}, {32, 2, 1}, {32, 4, 1}};
+        k2_sweep<KHmlstm, float, SigHmlstmCanonical>("k2_cfg2", false, 1024, 1024, t2);
+        const std::vector<std::array<int, 3>> t3 = {{32, 1, 1}, {32, 2, 1}, {32, 4, 1}, {32, 8, 1},
+                                                     {16, 1, 1}, {16, 2, 1}, {16, 4, 1}, {16, 8, 1},
+                                                     {8, 1, 1}, {8, 2, 1}, {8, 4, 1}, {8, 8, 1},
+                                                     {64, 2, 1}, {64, 4, 1}, {128, 2, 1}, {256, 2, 1}};
+        k2_sweep<KHmlstmBias, float, SigHmlstmBias>("k2_cfg3", true, 1024, 1024, t3);
+    }
+    if (which == "k2c3") {  // one default-tiling config-3 pullback, for ncu
+        Problem<float> P(true, 1024, 1024);
+        const Tiling fdef = choose_tiling(P.plan, 4, ClassMix{}, true);
+        fwd<KHmlstmBias, float, SigHmlstmBias>(P, &fdef);
+        for (int k = 0; k < 3; ++k) pull<KHmlstmBias, float, SigHmlstmBias>(P, nullptr);
+        CK(cudaDeviceSynchronize());
+    }
+    if (which == "all" || which == "det") {
+        k2_det<KHmlstmBias, float, SigHmlstmBias>("det_cfg5", true, 65536, 4096, 0, 4);
+        k2_det<KHmlstmBias, float, SigHmlstmBias>("det_cfg3", true, 1024, 1024, 0, 20);
+    }
+    return 0;
+}

@@ -181,6 +181,35 @@ TEST_CASE("one graph can mix policies per node") {
     }
 }
 
+TEST_CASE("mixed nodes of different shapes in one tape reduce a shared (1,H) argument; repeatable") {
+    // Two pullbacks with different reduction layouts (cross-CTA completion
+    // counters at different workspace offsets) on the same tape, swept twice.
+    Rng rng(43);
+    const int64_t H = 256;
+    const Tensor<double> x = random_pm1<double>(Shape{64, H}, rng), y = random_pm1<double>(Shape{200, H}, rng);
+    const Tensor<double> b = random_pm1<double>(Shape{1, H}, rng);
+    Tape<double> tape;
+    const Var<double> vx = tape.input(x), vy = tape.input(y), vb = tape.input(b);
+    const Var<double> p1 = mixed_broadcast(tape, mul_kernel(), {vx, vb}, MixedPolicy::CacheForward)[0];
+    const Var<double> p2 = mixed_broadcast(tape, mul_kernel(), {vy, vb}, MixedPolicy::CacheForward)[0];
+    const Var<double> s1 = tape.prim(PrimKind::SumOverDims, {p1});
+    const Var<double> s2 = tape.prim(PrimKind::SumOverDims, {p2});
+    const Var<double> h = tape.prim(PrimKind::Add, {s1, s2});
+    const auto xh = x.to_host(), yh = y.to_host();
+    std::vector<double> want(static_cast<std::size_t>(H), 0.0);
+    for (int64_t r = 0; r < 64; ++r)
+        for (int64_t c = 0; c < H; ++c) want[static_cast<std::size_t>(c)] += xh[static_cast<std::size_t>(r * H + c)];
+    for (int64_t r = 0; r < 200; ++r)
+        for (int64_t c = 0; c < H; ++c) want[static_cast<std::size_t>(c)] += yh[static_cast<std::size_t>(r * H + c)];
+    std::vector<double> first;
+    for (int sweep = 0; sweep < 3; ++sweep) {
+        const auto g = tape.backward(h, Tensor<double>(tape.value(h).shape(), 1.0)).at(vb).to_host();
+        CHECK(all_close(g, want, 1e-12, 1e-12));
+        if (sweep == 0) first = g;
+        else CHECK(g == first);
+    }
+}
+
 TEST_CASE("repeated input accumulates both contributions (x * x)") {
     Rng rng(41);
     const Tensor<double> x = random_pm1<double>(Shape{5, 3}, rng);

@@ -97,3 +97,39 @@ def test_cell_gradients_three_impls(oracle_lib, dtype):
             assert_close(got[impl][k], want[k], rtol, atol, f"{impl} grad{k}")
     for a, b in zip(got["mixed-cache"], got["mixed-recompute"]):
         assert np.array_equal(a, b)
+
+
+@pytest.mark.parametrize("dtype", [np.float32, np.float64])
+@pytest.mark.parametrize("variant", ["canonical", "bias"])
+@pytest.mark.parametrize("chunks", [2, 3, 7])
+def test_host_step_pipelined_matches_one_shot(host, oracle_lib, dtype, variant, chunks):
+    """Row-chunk pipelining (bcad_host_set_pipeline) is a schedule only: the
+    batch-sharded gradients and the primal are bit-identical to the one-shot
+    tape, the (1,H) bias gradients (summed over chunks) match the oracle, and
+    peak_cached_bytes reports the one-shot tape's accounting."""
+    from paper_1810_08297_b200 import host as H
+    B, Hd = 50, 96  # 50 rows: ragged chunks
+    ins = O.hmlstm_inputs(oracle_lib, B, Hd, dtype, variant)
+    name = O.hmlstm_kernel(variant)
+    seeds = [np.random.default_rng(2).uniform(-1, 1, (B, Hd)).astype(dtype)]
+    try:
+        H.set_pipeline(1)
+        p1, g1, peak1 = host_step(host, name, ins, seeds, 0)
+        H.set_pipeline(chunks)
+        pk, gk, peakk = host_step(host, name, ins, seeds, 0)
+    finally:
+        H.set_pipeline(0)
+    assert np.array_equal(p1[0], pk[0])
+    assert peak1 == peakk
+    _, want_g, want_a64 = oracle_lib.mixed_step(name, ins, 0, seeds)
+    assert_grads(gk, want_g, want_a64, [a.shape for a in ins], (B, Hd), dtype, f"pipelined x{chunks}")
+    for j, a in enumerate(ins):
+        if a.shape[0] == B:
+            assert np.array_equal(g1[j], gk[j]), f"arg {j} differs between one-shot and pipelined"
+
+
+def test_host_set_pipeline_rejects_negative(host):
+    from paper_1810_08297_b200 import host as H
+    from paper_1810_08297_b200 import native
+    with pytest.raises(native.ConfigError):
+        H.set_pipeline(-1)
