@@ -25,6 +25,7 @@ INCLUDE = os.path.join(ROOT, "include")
 BUILD = os.path.join(ROOT, "build")
 LIB = os.path.join(PKG, "libbcad_cu.so")
 HOST_LIB = os.path.join(PKG, "libbcad_host.so")
+BENCH_EXE = os.path.join(PKG, "bin", "bcad_bench")
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ["-std=c++20", "-O3", "--fmad=false", "-lineinfo", "-Xcompiler", "-fPIC,-O3",
@@ -80,24 +81,33 @@ def build_cuda(verbose: bool = False, jobs: int | None = None) -> str:
 
 
 def build_host(verbose: bool = False) -> str:
-    src = os.path.join(CSRC, "host_api.cpp")
-    deps = [src] + glob.glob(os.path.join(INCLUDE, "bcad", "*.hpp")) + [os.path.join(INCLUDE, "bcad_cu.h"), LIB]
+    """libbcad_host.so (end-to-end host C-ABI + bench records/CLI over the C++
+    drop-in API) and the bcad_bench executable."""
+    srcs = [os.path.join(CSRC, "host_api.cpp"), os.path.join(CSRC, "bench.cpp")]
+    deps = srcs + glob.glob(os.path.join(INCLUDE, "bcad", "*.hpp")) + [os.path.join(INCLUDE, "bcad_cu.h"),
+                                                                        os.path.join(INCLUDE, "bcad_host.h"), LIB]
     if _newer(HOST_LIB, deps):
-        _run([cxx(), "-std=c++20", "-O2", "-fPIC", "-shared", "-Wall", "-Wextra", "-I" + INCLUDE, src,
+        _run([cxx(), "-std=c++20", "-O2", "-fPIC", "-shared", "-Wall", "-Wextra", "-I" + INCLUDE, *srcs,
               "-o", HOST_LIB, "-L" + PKG, "-lbcad_cu", "-Wl,-rpath,$ORIGIN"], verbose)
+    main = os.path.join(CSRC, "bench_main.cpp")
+    if _newer(BENCH_EXE, [main, HOST_LIB]):
+        os.makedirs(os.path.dirname(BENCH_EXE), exist_ok=True)
+        _run([cxx(), "-std=c++20", "-O2", "-Wall", "-Wextra", "-I" + INCLUDE, main, "-o", BENCH_EXE, "-L" + PKG,
+              "-lbcad_host", "-lbcad_cu", "-Wl,-rpath,$ORIGIN/.."], verbose)
     return HOST_LIB
 
 
 def build_cpp_tests(verbose: bool = False) -> list[str]:
     out = []
     tdir = os.path.join(ROOT, "tests", "cpp")
-    for src in sorted(glob.glob(os.path.join(tdir, "test_*.cpp"))):
+    for src in sorted(glob.glob(os.path.join(tdir, "test_*.cpp")) + glob.glob(os.path.join(tdir, "cpu_*.cpp"))):
         os.makedirs(os.path.join(tdir, "bin"), exist_ok=True)
         exe = os.path.join(tdir, "bin", os.path.splitext(os.path.basename(src))[0])
-        deps = [src] + glob.glob(os.path.join(tdir, "*.hpp")) + glob.glob(os.path.join(INCLUDE, "bcad", "*.hpp")) + [LIB]
+        deps = [src] + glob.glob(os.path.join(tdir, "*.hpp")) + glob.glob(os.path.join(INCLUDE, "bcad", "*.hpp")) + \
+            [LIB, HOST_LIB]
         if _newer(exe, deps):
             _run([cxx(), "-std=c++20", "-O2", "-Wall", "-Wextra", "-I" + INCLUDE, "-I" + tdir, src, "-o", exe,
-                  "-L" + PKG, "-lbcad_cu", "-Wl,-rpath,$ORIGIN/../../../paper_1810_08297_b200"], verbose)
+                  "-L" + PKG, "-lbcad_host", "-lbcad_cu", "-Wl,-rpath,$ORIGIN/../../../paper_1810_08297_b200"], verbose)
         out.append(exe)
     return out
 
