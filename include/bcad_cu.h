@@ -159,6 +159,12 @@ int bcad_cu_host_free(void* ptr);
 /* kind: 0 host->device, 1 device->host, 2 device->device */
 int bcad_cu_memcpy(void* dst, const void* src, size_t bytes, int kind, void* stream);
 int bcad_cu_memset(void* ptr, int value, size_t bytes, void* stream);
+/* n independent copies of one kind (0 host->device, 1 device->host, 2
+ * device->device) enqueued on `stream` with ONE call: host transfers through
+ * cudaMemcpyBatchAsync (a per-copy loop on the legacy NULL stream), device
+ * copies as one multi-buffer copy kernel. The copies must not overlap. */
+int bcad_cu_memcpy_batch(size_t n, void* const* dsts, const void* const* srcs, const size_t* sizes, int kind,
+                         void* stream);
 int bcad_cu_stream_create(void** stream);
 int bcad_cu_stream_destroy(void* stream);
 int bcad_cu_stream_synchronize(void* stream);

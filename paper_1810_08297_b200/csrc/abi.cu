@@ -173,6 +173,28 @@ __global__ void scatter_add_kernel(T* acc, const T* con, ScatterGeom g, bool zer
     }
 }
 
+// Multi-buffer device copy: blockIdx.y selects the buffer, 16-byte vectors
+// when both ends are 16-byte aligned, a byte loop for the rest.
+constexpr int kCopyBatch = 64;
+struct CopyBatchDesc {
+    char* dst[kCopyBatch];
+    const char* src[kCopyBatch];
+    size_t bytes[kCopyBatch];
+};
+
+__global__ void copy_batch_kernel(const __grid_constant__ CopyBatchDesc d) {
+    const int k = blockIdx.y;
+    char* dst = d.dst[k];
+    const char* src = d.src[k];
+    const size_t nb = d.bytes[k];
+    const bool vec = ((reinterpret_cast<uintptr_t>(dst) | reinterpret_cast<uintptr_t>(src)) & 15u) == 0;
+    const size_t n16 = vec ? nb / 16 : 0;
+    const size_t stride = size_t(gridDim.x) * blockDim.x;
+    for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n16; i += stride)
+        reinterpret_cast<int4*>(dst)[i] = __ldcs(reinterpret_cast<const int4*>(src) + i);
+    for (size_t i = n16 * 16 + blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < nb; i += stride) dst[i] = src[i];
+}
+
 int grid_for(int64_t n) {
     const int64_t b = (n + 255) / 256;
     return int(b < 1 ? 1 : (b > 148 * 16 ? 148 * 16 : b));
@@ -458,6 +480,64 @@ int bcad_cu_memcpy(void* dst, const void* src, size_t bytes, int kind, void* str
     if (bytes == 0) return BCAD_CU_OK;
     const cudaMemcpyKind k = kind == 0 ? cudaMemcpyHostToDevice : kind == 1 ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice;
     CU_TRY(cudaMemcpyAsync(dst, src, bytes, k, static_cast<cudaStream_t>(stream)), "cudaMemcpyAsync");
+    return BCAD_CU_OK;
+}
+int bcad_cu_memcpy_batch(size_t n, void* const* dsts, const void* const* srcs, const size_t* sizes, int kind,
+                         void* stream) {
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    if (kind < 0 || kind > 2) return fail(BCAD_CU_ERR_CONFIG, "memcpy kind must be 0, 1 or 2");
+    std::vector<void*> d;
+    std::vector<void*> sr;
+    std::vector<size_t> sz;
+    for (size_t k = 0; k < n; ++k)
+        if (sizes[k]) {
+            d.push_back(dsts[k]);
+            sr.push_back(const_cast<void*>(srcs[k]));
+            sz.push_back(sizes[k]);
+        }
+    if (d.empty()) return BCAD_CU_OK;
+    if (kind == 2) {  // device copies on the SMs, kCopyBatch buffers per launch
+        for (size_t k0 = 0; k0 < d.size(); k0 += kCopyBatch) {
+            CopyBatchDesc desc{};
+            const int m = int(std::min<size_t>(kCopyBatch, d.size() - k0));
+            size_t most = 0;
+            for (int k = 0; k < m; ++k) {
+                desc.dst[k] = static_cast<char*>(d[k0 + k]);
+                desc.src[k] = static_cast<const char*>(sr[k0 + k]);
+                desc.bytes[k] = sz[k0 + k];
+                most = std::max(most, sz[k0 + k]);
+            }
+            const size_t chunks = (most + 16 * 256 - 1) / (16 * 256);
+            const unsigned gx = unsigned(std::max<size_t>(1, std::min<size_t>(chunks, std::max(1, 148 * 8 / m))));
+            copy_batch_kernel<<<dim3(gx, unsigned(m)), 256, 0, s>>>(desc);
+            CU_TRY(cudaGetLastError(), "copy_batch_kernel");
+        }
+        return BCAD_CU_OK;
+    }
+    // The batch path is for pinned host memory; pageable buffers (which the
+    // driver stages, and would otherwise lock page by page) go one by one.
+    bool pinned = true;
+    for (size_t k = 0; k < d.size() && pinned; ++k) {
+        cudaPointerAttributes at{};
+        const void* host = kind == 0 ? sr[k] : d[k];
+        if (cudaPointerGetAttributes(&at, host) != cudaSuccess || at.type != cudaMemoryTypeHost) pinned = false;
+        (void)cudaGetLastError();
+    }
+    if (s == nullptr || d.size() == 1 || !pinned) {  // the batch API rejects the legacy stream
+        for (size_t k = 0; k < d.size(); ++k)
+            CU_TRY(cudaMemcpyAsync(d[k], sr[k], sz[k], kind == 0 ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToHost, s),
+                   "cudaMemcpyAsync");
+        return BCAD_CU_OK;
+    }
+    cudaMemcpyAttributes attr{};
+    attr.srcAccessOrder = cudaMemcpySrcAccessOrderStream;
+    size_t first = 0, fail_idx = 0;
+    if (cudaMemcpyBatchAsync(d.data(), sr.data(), sz.data(), d.size(), &attr, &first, 1, &fail_idx, s) != cudaSuccess) {
+        (void)cudaGetLastError();  // an operand the batch path rejects: one call per copy instead
+        for (size_t k = 0; k < d.size(); ++k)
+            CU_TRY(cudaMemcpyAsync(d[k], sr[k], sz[k], kind == 0 ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToHost, s),
+                   "cudaMemcpyAsync");
+    }
     return BCAD_CU_OK;
 }
 int bcad_cu_memset(void* ptr, int value, size_t bytes, void* stream) {

@@ -42,26 +42,39 @@ int64_t tape_step(const char* name, int n_in, const void* const* host_in, const 
     using namespace bcad;
     Tape<Real> tape;
     std::vector<Var<Real>> vars;
-    for (int j = 0; j < n_in; ++j)
-        vars.push_back(tape.input(Tensor<Real>::from_host(Shape::from_c(shapes[j]), static_cast<const Real*>(host_in[j]))));
+    {
+        CopyBatch up(0);  // the n_in uploads as one runtime call
+        std::vector<Tensor<Real>> x;
+        for (int j = 0; j < n_in; ++j) {
+            x.push_back(Tensor<Real>::uninitialized(Shape::from_c(shapes[j])));
+            up.add(x.back().device_data(), host_in[j], x.back().bytes());
+        }
+        up.submit(current_stream());
+        for (Tensor<Real>& t : x) vars.push_back(tape.input(std::move(t)));
+    }
     const BroadcastKernel<Real> kernel(n_in, m_out, name);
     const std::vector<Var<Real>> outs = mixed_broadcast<Real>(
         tape, kernel, std::span<const Var<Real>>(vars), policy == 0 ? MixedPolicy::CacheForward : MixedPolicy::RecomputeReverse);
     std::vector<std::pair<Var<Real>, Tensor<Real>>> seeds;
+    CopyBatch prim(1), sup(0);
     for (int i = 0; i < m_out; ++i) {
         const Tensor<Real>& v = tape.value(outs[static_cast<std::size_t>(i)]);
-        if (host_primal && host_primal[i])
-            check(bcad_cu_memcpy(host_primal[i], v.device_data(), v.bytes(), 1, current_stream()));
-        if (host_seeds && host_seeds[i])
-            seeds.emplace_back(outs[static_cast<std::size_t>(i)],
-                               Tensor<Real>::from_host(v.shape(), static_cast<const Real*>(host_seeds[i])));
+        if (host_primal && host_primal[i]) prim.add(host_primal[i], v.device_data(), v.bytes());
+        if (host_seeds && host_seeds[i]) {
+            seeds.emplace_back(outs[static_cast<std::size_t>(i)], Tensor<Real>::uninitialized(v.shape()));
+            sup.add(seeds.back().second.device_data(), host_seeds[i], v.bytes());
+        }
     }
+    prim.submit(current_stream());
+    sup.submit(current_stream());
     const Gradients<Real> grads = tape.backward(std::span<const std::pair<Var<Real>, Tensor<Real>>>(seeds));
+    CopyBatch down(1);
     for (int j = 0; j < n_in; ++j) {
         if (!host_grads || !host_grads[j]) continue;
         const Tensor<Real>& g = grads.at(vars[static_cast<std::size_t>(j)]);
-        check(bcad_cu_memcpy(host_grads[j], g.device_data(), g.bytes(), 1, current_stream()));
+        down.add(host_grads[j], g.device_data(), g.bytes());
     }
+    down.submit(current_stream());
     return tape.peak_cached_bytes();
 }
 
@@ -77,10 +90,11 @@ int64_t tape_step(const char* name, int n_in, const void* const* host_in, const 
 
 std::atomic<int> g_pipeline{0};  // 0 auto, 1 off, k > 1 at most k chunks
 
-// Auto chunking: each chunk costs ~7 copy-engine operations per direction
-// plus two launches, so chunks stay large (measured on B200 over PCIe:
-// 2-3 chunks beat both one-shot and finer pipelines at config 2).
-constexpr std::size_t kChunkBytes = std::size_t(16) << 20;  // host<->device bytes per chunk
+// Auto chunking: each chunk costs two batched copy calls, two launches and
+// two events, and the last chunk's download is exposed, so chunks stay
+// large (measured on B200 over PCIe: 3-4 chunks of ~10-13 MB beat both the
+// one-shot step and finer pipelines at configs 2 and 3).
+constexpr std::size_t kChunkBytes = std::size_t(12) << 20;  // host<->device bytes per chunk
 constexpr int kMaxChunks = 16;
 
 struct Pipe {
@@ -188,8 +202,12 @@ int64_t pipelined_step(bcad_cu_kernel k, int n_in, const void* const* host_in, c
         ws.push_back(std::make_unique<detail::DeviceBuffer>(ws_bytes[q], comp));
         check(bcad_cu_memset(ws.back()->ptr, 0, ws_bytes[q], comp));
     }
-    for (int j = 0; j < n_in; ++j)  // batch-broadcast inputs: whole, on the compute stream
-        if (!split[j]) check(bcad_cu_memcpy(x[j].device_data(), host_in[j], x[j].bytes(), 0, comp));
+    {
+        CopyBatch rep(0);  // batch-broadcast inputs: whole, on the compute stream
+        for (int j = 0; j < n_in; ++j)
+            if (!split[j]) rep.add(x[j].device_data(), host_in[j], x[j].bytes());
+        rep.submit(comp);
+    }
     check(bcad_cu_event_record(P.fork, comp));
     check(bcad_cu_stream_wait_event(P.h2d, P.fork));
     check(bcad_cu_stream_wait_event(P.d2h, P.fork));
@@ -203,15 +221,16 @@ int64_t pipelined_step(bcad_cu_kernel k, int n_in, const void* const* host_in, c
         const int64_t b1 = std::min(B, b0 + rows), r = b1 - b0;
         const std::size_t cell0 = static_cast<std::size_t>(b0 * out_row), cells = static_cast<std::size_t>(r * out_row);
         // h2d: this chunk's rows of the batch-sharded inputs and of the seeds
+        CopyBatch up(0);
         for (int j = 0; j < n_in; ++j) {
             if (!split[j]) continue;
             const std::size_t o = static_cast<std::size_t>(b0 * row_elems[j]), cnt = static_cast<std::size_t>(r * row_elems[j]);
-            check(bcad_cu_memcpy(x[j].device_data() + o, static_cast<const Real*>(host_in[j]) + o, cnt * sizeof(Real), 0, P.h2d));
+            up.add(x[j].device_data() + o, static_cast<const Real*>(host_in[j]) + o, cnt * sizeof(Real));
         }
         for (int i = 0; i < m_out; ++i)
             if (has_w[i])
-                check(bcad_cu_memcpy(w[i].device_data() + cell0, static_cast<const Real*>(host_seeds[i]) + cell0,
-                                     cells * sizeof(Real), 0, P.h2d));
+                up.add(w[i].device_data() + cell0, static_cast<const Real*>(host_seeds[i]) + cell0, cells * sizeof(Real));
+        up.submit(P.h2d);
         check(bcad_cu_event_record(P.in_ready[c], P.h2d));
         // compute: K1 then K2 on the chunk (row-offset views of the buffers)
         check(bcad_cu_stream_wait_event(comp, P.in_ready[c]));
@@ -237,20 +256,23 @@ int64_t pipelined_step(bcad_cu_kernel k, int n_in, const void* const* host_in, c
         check(bcad_cu_event_record(P.out_ready[c], comp));
         // d2h: the chunk's primal rows and batch-sharded gradient rows
         check(bcad_cu_stream_wait_event(P.d2h, P.out_ready[c]));
+        CopyBatch down(1);
         for (int i = 0; i < m_out; ++i)
             if (host_primal && host_primal[i])
-                check(bcad_cu_memcpy(static_cast<Real*>(host_primal[i]) + cell0, y[i].device_data() + cell0,
-                                     cells * sizeof(Real), 1, P.d2h));
+                down.add(static_cast<Real*>(host_primal[i]) + cell0, y[i].device_data() + cell0, cells * sizeof(Real));
         for (int j = 0; j < n_in; ++j) {
             if (!split[j] || !has_g[j]) continue;
             const std::size_t o = static_cast<std::size_t>(b0 * row_elems[j]), cnt = static_cast<std::size_t>(r * row_elems[j]);
-            check(bcad_cu_memcpy(static_cast<Real*>(host_grads[j]) + o, g[j].device_data() + o, cnt * sizeof(Real), 1, P.d2h));
+            down.add(static_cast<Real*>(host_grads[j]) + o, g[j].device_data() + o, cnt * sizeof(Real));
         }
+        down.submit(P.d2h);
     }
     check(bcad_cu_event_record(P.join, P.d2h));
     check(bcad_cu_stream_wait_event(comp, P.join));
+    CopyBatch rep(1);
     for (int j = 0; j < n_in; ++j)
-        if (!split[j] && has_g[j]) check(bcad_cu_memcpy(host_grads[j], g[j].device_data(), g[j].bytes(), 1, comp));
+        if (!split[j] && has_g[j]) rep.add(host_grads[j], g[j].device_data(), g[j].bytes());
+    rep.submit(comp);
     check(bcad_cu_stream_synchronize(comp));
     // what the one-shot tape reports (tape.hpp:236-243): inputs + values + cache
     return (in_elems + int64_t(m) * E + (policy == 0 ? int64_t(m * n) * E : 0)) * int64_t(sizeof(Real));
@@ -284,10 +306,17 @@ void cell_grads(int impl, int64_t n, const void* const* dev_in, const void* dev_
                 int64_t* nodes, int64_t* peak) {
     using namespace bcad;
     const Shape mat{n, n}, vec{n};
-    auto dev = [](const Shape& s, const void* p) { return Tensor<Real>::from_device(s, static_cast<const Real*>(p)); };
+    // the caller's device buffers become the CellInputs (copies, one batch)
+    CopyBatch in_copies(2);
+    auto dev = [&](const Shape& s, const void* p) {
+        Tensor<Real> t = Tensor<Real>::uninitialized(s);
+        in_copies.add(t.device_data(), p, t.bytes());
+        return t;
+    };
     const CellInputs<Real> in{dev(mat, dev_in[0]), dev(mat, dev_in[1]), dev(mat, dev_in[2]),
                               dev(mat, dev_in[3]), dev(vec, dev_in[4]), dev(vec, dev_in[5])};
     const Tensor<Real> seed = dev(mat, dev_seed);
+    in_copies.submit(current_stream());
     Tape<Real> tape;
     CellGraph<Real> graph;
     if (impl == 0) graph = cell_update_fused(tape, in, MixedPolicy::CacheForward);
@@ -296,10 +325,12 @@ void cell_grads(int impl, int64_t n, const void* const* dev_in, const void* dev_
     else throw ConfigError("impl must be 0 (mixed-cache), 1 (mixed-recompute) or 2 (reverse-unfused)");
     const Gradients<Real> g = tape.backward(graph.out, seed);
     const Var<Real> leaves[4] = {graph.c_prev, graph.f, graph.i, graph.g};
+    CopyBatch out(2);
     for (int k = 0; k < 4; ++k) {
         const Tensor<Real>& t = g.at(leaves[k]);
-        check(bcad_cu_memcpy(dev_grads[k], t.device_data(), t.bytes(), 2, current_stream()));
+        out.add(dev_grads[k], t.device_data(), t.bytes());
     }
+    out.submit(current_stream());
     if (nodes) *nodes = static_cast<int64_t>(tape.size());
     if (peak) *peak = tape.peak_cached_bytes();
 }

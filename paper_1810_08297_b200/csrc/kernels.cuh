@@ -622,10 +622,15 @@ __global__ void __launch_bounds__(kThreads, kRecompute ? 2 : kCtasPerSm) pull2d_
 
         // ---- cross-CTA completion: the last CTA of a tile row / column /
         // grid (integer ticket) combines the fp64 partials in tile order.
-        __threadfence();
+        // Release: the barrier orders the CTA's partial writes before thread
+        // 0's gpu-scope fence and ticket (fences are cumulative), so only one
+        // thread per CTA waits on the fence.
         __syncthreads();
         if (need_row) {
-            if (tid == 0) s_last = atomicAdd(&p.counters[rt], 1u) == unsigned(p.n_col_tiles - 1);
+            if (tid == 0) {
+                __threadfence();
+                s_last = atomicAdd(&p.counters[rt], 1u) == unsigned(p.n_col_tiles - 1);
+            }
             __syncthreads();
             if (s_last) {
                 __threadfence();
@@ -644,7 +649,10 @@ __global__ void __launch_bounds__(kThreads, kRecompute ? 2 : kCtasPerSm) pull2d_
             __syncthreads();
         }
         if (need_col) {
-            if (tid == 0) s_last = atomicAdd(&p.counters[p.n_row_tiles + ct], 1u) == unsigned(p.n_row_tiles - 1);
+            if (tid == 0) {
+                __threadfence();
+                s_last = atomicAdd(&p.counters[p.n_row_tiles + ct], 1u) == unsigned(p.n_row_tiles - 1);
+            }
             __syncthreads();
             if (s_last) {
                 __threadfence();
@@ -664,7 +672,10 @@ __global__ void __launch_bounds__(kThreads, kRecompute ? 2 : kCtasPerSm) pull2d_
         }
         if (need_scal) {
             unsigned int* cnt = &p.counters[p.n_row_tiles + p.n_col_tiles];
-            if (tid == 0) s_last = atomicAdd(cnt, 1u) == unsigned(n_ctas - 1);
+            if (tid == 0) {
+                __threadfence();
+                s_last = atomicAdd(cnt, 1u) == unsigned(n_ctas - 1);
+            }
             __syncthreads();
             if (s_last) {
                 __threadfence();

@@ -134,6 +134,7 @@ PROTOS = {
     "bcad_cu_host_free": (I, [VP]),
     "bcad_cu_memcpy": (I, [VP, VP, SZ, I, VP]),
     "bcad_cu_memset": (I, [VP, I, SZ, VP]),
+    "bcad_cu_memcpy_batch": (I, [SZ, VP, VP, VP, I, VP]),
     "bcad_cu_stream_create": (I, [C.POINTER(VP)]),
     "bcad_cu_stream_destroy": (I, [VP]),
     "bcad_cu_stream_synchronize": (I, [VP]),

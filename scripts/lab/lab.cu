@@ -372,6 +372,11 @@ int main(int argc, char** argv) {
                                                      {64, 2, 1}, {64, 4, 1}, {128, 2, 1}, {256, 2, 1}};
         k2_sweep<KHmlstmBias, float, SigHmlstmBias>("k2_cfg3", true, 1024, 1024, t3);
     }
+    if (which == "k1c2") {  // default-tiling config-2 forwards, for ncu
+        Problem<float> P(false, 1024, 1024);
+        for (int k = 0; k < 3; ++k) fwd<KHmlstm, float, SigHmlstmCanonical>(P, nullptr);
+        CK(cudaDeviceSynchronize());
+    }
     if (which == "k2c3") {  // one default-tiling config-3 pullback, for ncu
         Problem<float> P(true, 1024, 1024);
         const Tiling fdef = choose_tiling(P.plan, 4, ClassMix{}, true);
