@@ -80,15 +80,20 @@ def main():
              "--import-source on -k regex:\"fwd2d|pull2d\"` on `bench.py --config <cfg>` (cold caches: ncu flushes "
              "between replays, so K2 reads its cached partials from DRAM here while in the timed bench they are still "
              "L2-resident after K1 at config 2). Algorithmic bytes per launch are SURVEY §8(d)'s reference-faithful "
-             "counts (paper_1810_08297_b200/workloads.py).", ""]
+             "counts (paper_1810_08297_b200/workloads.py); peak = MEASURED_PEAKS.json hbm_gbs of this container.", ""]
     traffic = {}
-    for cfg in ("cfg2", "cfg5", "cfg4div"):
+    peak = 6459.0
+    try:
+        peak = float(json.load(open("MEASURED_PEAKS.json"))["hbm_gbs"])
+    except Exception:
+        pass
+    for cfg in ("cfg2", "cfg3", "cfg5", "cfg4div"):
         rep = os.path.join(src, f"full_{cfg}.ncu-rep")
         if not os.path.exists(rep):
             continue
         w = WORKLOADS[cfg]
         lines += [f"## {cfg}: {w.describe}", "",
-                  "| kernel | regs | grid | occ % | warp inst | IPC | SM active/elapsed | dur µs | DRAM read MB | DRAM write MB | algorithmic MB | alg GB/s | frac of 6459 |",
+                  "| kernel | regs | grid | occ % | warp inst | IPC | SM active/elapsed | dur µs | DRAM read MB | DRAM write MB | algorithmic MB | alg GB/s | frac of peak |",
                   "|---|---|---|---|---|---|---|---|---|---|---|---|---|"]
         seen = set()
         for d in raw(rep):
@@ -102,7 +107,7 @@ def main():
             lines.append(f"| {d['kernel']} | {d.get('regs', 0):.0f} | {d.get('grid', 0):.0f} | {d.get('occupancy_pct', 0):.1f} | "
                          f"{d.get('warp_inst', 0):.3g} | {d.get('ipc', 0):.2f} | {act:.2f} | {dur:.1f} | "
                          f"{d.get('dram_read', 0) / 1e6:.1f} | {d.get('dram_write', 0) / 1e6:.1f} | {alg / 1e6:.1f} | "
-                         f"{gbs:.0f} | {gbs / 6459:.2f} |")
+                         f"{gbs:.0f} | {gbs / peak:.2f} |")
             traffic.setdefault(cfg, {})[d["kernel"]] = d.get("dram_read", 0) + d.get("dram_write", 0)
         lines.append("")
     for cfg in ("cfg2", "cfg5"):
