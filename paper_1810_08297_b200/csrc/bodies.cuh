@@ -36,24 +36,70 @@ BCAD_HD S cell_update_scalar(S c, S f, S i, S g, S z1, S z2) {
     return sigmoid(i) * tanh(g);                                                // FLUSH
 }
 
+// Branch-free form of cell_update_scalar for cells whose boundary bits
+// differ across a warp (per-cell z, SURVEY §8(d) config 4 divergence): every
+// lane evaluates sigmoid(f), sigmoid(i) and tanh(g) once and the ordered
+// cases select among the results, so a warp runs three transcendental
+// sequences per cell instead of the five a divergent UPDATE + FLUSH pair
+// costs. Per cell the value and every partial are the branchy form's bit for
+// bit (the same operations in the same order; the selected one is kept).
+template <class S>
+BCAD_HD S cell_update_select(S c, S f, S i, S g, S z1, S z2) {
+    const S flush = sigmoid(i) * tanh(g);
+    const S update = sigmoid(f) * c + flush;
+    const bool upd = z1 == 0.0 && z2 == 1.0, cpy = z1 == 0.0 && z2 == 0.0;
+    return upd ? update : cpy ? c : flush;
+}
+
 // kPredicateArgs: bit j set when argument j feeds a branch predicate of
 // the body (a comparison). The lane-vector evaluation (VDual) is used only
-// when all of them are uniform across a thread's V cells.
+// when all of them are uniform across a thread's V cells. kSelectForm: the
+// body also provides body_select, a branch-free equivalent used when they
+// are not.
 #define BCAD_BODY_P(NAME, STR, NIN, NOUT, RAISES, PRED, ...)                 \
     struct NAME {                                                            \
         static constexpr const char* kName = STR;                            \
         static constexpr int kIn = NIN, kOut = NOUT;                         \
         static constexpr bool kMayRaise = RAISES;                            \
         static constexpr uint32_t kPredicateArgs = PRED;                     \
+        static constexpr bool kSelectForm = false;                           \
         template <class S>                                                   \
         BCAD_HD static void body(const S* in, S* out) { __VA_ARGS__; }       \
+        template <class S>                                                   \
+        BCAD_HD static void body_select(const S* in, S* out) { __VA_ARGS__; } \
     };
 #define BCAD_BODY(NAME, STR, NIN, NOUT, RAISES, ...) BCAD_BODY_P(NAME, STR, NIN, NOUT, RAISES, 0u, __VA_ARGS__)
 
-BCAD_BODY_P(KHmlstm, "hmlstm_update", 6, 1, false, 0x30u,
-          out[0] = cell_update_scalar(in[0], in[1], in[2], in[3], in[4], in[5]))
-BCAD_BODY_P(KHmlstmBias, "hmlstm_update_bias", 9, 1, false, 0x180u,
-          out[0] = cell_update_scalar(in[0], in[1] + in[4], in[2] + in[5], in[3] + in[6], in[7], in[8]))
+struct KHmlstm {  // hmlstm.hpp:56-61
+    static constexpr const char* kName = "hmlstm_update";
+    static constexpr int kIn = 6, kOut = 1;
+    static constexpr bool kMayRaise = false;
+    static constexpr uint32_t kPredicateArgs = 0x30u;  // z1, z2
+    static constexpr bool kSelectForm = true;
+    template <class S>
+    BCAD_HD static void body(const S* in, S* out) {
+        out[0] = cell_update_scalar(in[0], in[1], in[2], in[3], in[4], in[5]);
+    }
+    template <class S>
+    BCAD_HD static void body_select(const S* in, S* out) {
+        out[0] = cell_update_select(in[0], in[1], in[2], in[3], in[4], in[5]);
+    }
+};
+struct KHmlstmBias {  // cell_update(c, f + bf, i + bi, g + bg, z1, z2), SURVEY §8(d) configs 3/5
+    static constexpr const char* kName = "hmlstm_update_bias";
+    static constexpr int kIn = 9, kOut = 1;
+    static constexpr bool kMayRaise = false;
+    static constexpr uint32_t kPredicateArgs = 0x180u;  // z1, z2
+    static constexpr bool kSelectForm = true;
+    template <class S>
+    BCAD_HD static void body(const S* in, S* out) {
+        out[0] = cell_update_scalar(in[0], in[1] + in[4], in[2] + in[5], in[3] + in[6], in[7], in[8]);
+    }
+    template <class S>
+    BCAD_HD static void body_select(const S* in, S* out) {
+        out[0] = cell_update_select(in[0], in[1] + in[4], in[2] + in[5], in[3] + in[6], in[7], in[8]);
+    }
+};
 BCAD_BODY(KIdentity, "identity", 1, 1, false, out[0] = in[0])
 BCAD_BODY_P(KReflect, "reflect", 1, 1, false, 0x1u, out[0] = reflect_below_half(in[0]))
 BCAD_BODY(KTanhSigmoid, "tanh_sigmoid", 1, 1, false, out[0] = tanh(in[0]) * sigmoid(in[0]))
@@ -103,6 +149,9 @@ struct KTanhProduct {  // arity_workload.hpp:19-28
     static constexpr int kIn = A, kOut = 1;
     static constexpr bool kMayRaise = false;
     static constexpr uint32_t kPredicateArgs = A >= 32 ? ~0u : (1u << A) - 1u;  // reflect_below_half on every arg
+    static constexpr bool kSelectForm = false;
+    template <class S>
+    BCAD_HD static void body_select(const S* in, S* out) { body(in, out); }
     template <class S>
     BCAD_HD static void body(const S* in, S* out) {
         S acc = tanh(reflect_below_half(in[0]));

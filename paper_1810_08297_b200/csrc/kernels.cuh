@@ -181,7 +181,10 @@ __device__ __forceinline__ void eval_cells(const Pack<T, V>* x, Pack<T, V>* y, P
         Dual<T, N> xi[N], yo[M];
 #pragma unroll
         for (int j = 0; j < N; ++j) xi[j] = Dual<T, N>::seeded(x[j].x[v], j);
-        Body::template body<Dual<T, N>>(xi, yo);
+        // a static signature whose predicates vary per cell: the branch-free
+        // form, if the body has one
+        if constexpr (Body::kSelectForm && S::kStatic && !vec_eval_ok<Body, S>()) Body::template body_select<Dual<T, N>>(xi, yo);
+        else Body::template body<Dual<T, N>>(xi, yo);
         if constexpr (Body::kMayRaise) report_error(err, off + v);
 #pragma unroll
         for (int i = 0; i < M; ++i) {
@@ -302,7 +305,8 @@ __global__ void __launch_bounds__(kThreads) fwd2d_kernel(const __grid_constant__
                 T xi[N], yo[M];
 #pragma unroll
                 for (int j = 0; j < N; ++j) xi[j] = x[j].x[v];
-                Body::template body<T>(xi, yo);
+                if constexpr (Body::kSelectForm && S::kStatic && !vec_eval_ok<Body, S>()) Body::template body_select<T>(xi, yo);
+                else Body::template body<T>(xi, yo);
 #pragma unroll
                 for (int i = 0; i < M; ++i) y[i].x[v] = yo[i];
             }
