@@ -567,13 +567,15 @@ def measure_tape(device, stream, steps: int):
 
 def measure_arity(device, stream, steps: int):
     """Paper §3.4.1 / Fig. 3 on B200: forward-mode diagonal Jacobian of
-    tanh_product_A (arity_workload.hpp:19-28) at 1024 x 1024 fp32, one fused
-    K1 per call; bytes = (A inputs + primal + A partials) * 4 per cell."""
+    tanh_product_A (arity_workload.hpp:19-28) at 4096 x 4096 fp32 (large
+    enough that launch costs vanish), one fused K1 per call; bytes = (A
+    inputs + primal + A partials) * 4 per cell. Cells per thread drop from 4
+    to 2 (A = 8) and 1 (A >= 16) to keep the A-wide duals in registers."""
     import torch
     from paper_1810_08297_b200 import native
-    n = 1024
+    n = 4096
     peak, _ = hbm_peak()
-    out = {"n": n}
+    out = {"n": n, "cells_per_thread": {"1": 4, "2": 4, "4": 4, "8": 2, "16": 1, "18": 1, "32": 1}}
     g = torch.Generator(device=device)
     g.manual_seed(9)
     for A in (1, 2, 4, 8, 16, 18, 32):

@@ -150,6 +150,9 @@ struct KTanhProduct {  // arity_workload.hpp:19-28
     static constexpr bool kMayRaise = false;
     static constexpr uint32_t kPredicateArgs = A >= 32 ? ~0u : (1u << A) - 1u;  // reflect_below_half on every arg
     static constexpr bool kSelectForm = false;
+    // cells per K1 thread: the product's dual keeps all A partials live, so
+    // wide arities evaluate fewer cells at once (register study, paper Fig. 3)
+    static constexpr int kMaxVec = A >= 16 ? 1 : A >= 8 ? 2 : 4;
     template <class S>
     BCAD_HD static void body_select(const S* in, S* out) { body(in, out); }
     template <class S>

@@ -78,9 +78,20 @@ void fill_generic(bcad_dev::GenParams<N, M, T>& g, const Plan& plan) {
 }
 
 // ---------------------------------------------------------------- forward
+// K1's cells per thread: one 128-bit vector, unless the body caps it
+// (Body::kMaxVec) because its dual state per cell is wide enough that V
+// cells would not fit in registers (tanh_product_<A> for large A: every
+// partial of the product is structurally nonzero).
+template <class Body, class T>
+constexpr int fwd_vec_width() {
+    constexpr int v = vec_width<T>();
+    if constexpr (requires { Body::kMaxVec; }) return Body::kMaxVec < v ? Body::kMaxVec : v;
+    else return v;
+}
+
 template <class Body, class T, class... Sigs>
 int launch_fwd_t(const FwdArgs& a, std::string* err) {
-    constexpr int N = Body::kIn, M = Body::kOut, V = vec_width<T>();
+    constexpr int N = Body::kIn, M = Body::kOut, V = fwd_vec_width<Body, T>();
     const Plan& plan = *a.plan;
     const bool real = a.partials == nullptr;
     bool vec = plan.is2d && plan.cols % V == 0;
