@@ -445,8 +445,10 @@ __global__ void __launch_bounds__(kThreads, kRecompute ? 2 : kCtasPerSm) pull2d_
     double* col_acc = smem;
     double* row_acc = col_acc + size_t(p.n_col_args) * kThreads * V;
     double* scal_acc = row_acc + size_t(p.n_row_args) * trows * wpr;
-    if constexpr (kAnyCol)
-        for (int i = tid; i < p.n_col_args * kThreads * V; i += kThreads) col_acc[i] = 0.0;
+    if constexpr (kAnyCol)  // each thread zeroes exactly the partials it accumulates (no barrier needed)
+        for (int a = 0; a < p.n_col_args; ++a)
+#pragma unroll
+            for (int v = 0; v < V; ++v) col_acc[(size_t(a) * kThreads + tid) * V + v] = 0.0;
     if constexpr (kAnyScal)
         for (int a = 0; a < p.n_scalar_args; ++a) scal_acc[a * kThreads + tid] = 0.0;
 

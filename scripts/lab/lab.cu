@@ -71,6 +71,7 @@ struct Flush {
 };
 
 static Flush* g_flush;
+static bool g_recompute = false;  // pull(): RecomputeReverse (partials re-derived) instead of cached
 static cudaStream_t g_s;
 
 double time_us(const std::function<void()>& fn, int reps = 25) {
@@ -195,7 +196,7 @@ int pull(Problem<T>& P, const Tiling* t) {
     PullArgs a{};
     a.dtype = sizeof(T) == 4 ? BCAD_CU_F32 : BCAD_CU_F64;
     a.out_adj = w;
-    a.partials = parts.data();
+    a.partials = g_recompute ? nullptr : parts.data();
     a.in = in.data();
     a.in_adj = adj.data();
     a.accumulate = nullptr;
@@ -351,7 +352,11 @@ void k2_det(const char* tag, bool bias, int64_t B, int64_t H, int cy_override, i
 }
 
 int main(int argc, char** argv) {
-    const std::string which = argc > 1 ? argv[1] : "all";
+    std::string which = argc > 1 ? argv[1] : "all";
+    if (which.size() > 2 && which.compare(which.size() - 2, 2, ":r") == 0) {
+        g_recompute = true;
+        which = which.substr(0, which.size() - 2);
+    }
     CK(cudaSetDevice(0));
     CK(cudaStreamCreateWithFlags(&g_s, cudaStreamNonBlocking));
     g_flush = new Flush();
@@ -376,6 +381,20 @@ int main(int argc, char** argv) {
         Problem<float> P(false, 1024, 1024);
         for (int k = 0; k < 3; ++k) fwd<KHmlstm, float, SigHmlstmCanonical>(P, nullptr);
         CK(cudaDeviceSynchronize());
+    }
+    if (which == "k2c2") {  // default-tiling config-2 pullbacks (ROW reductions), for sanitizers / ncu
+        Problem<float> P(false, 1024, 1024);
+        fwd<KHmlstm, float, SigHmlstmCanonical>(P, nullptr);
+        for (int k = 0; k < 3; ++k) pull<KHmlstm, float, SigHmlstmCanonical>(P, nullptr);
+        CK(cudaDeviceSynchronize());
+    }
+    if (which == "k2mix") {  // several reduction layouts in one process: small / tall / wide bias problems
+        for (auto [B, H] : {std::pair<int64_t, int64_t>{64, 256}, {4096, 128}, {16, 8192}, {3000, 1024}}) {
+            Problem<float> P(true, B, H);
+            fwd<KHmlstmBias, float, SigHmlstmBias>(P, nullptr);
+            for (int k = 0; k < 2; ++k) pull<KHmlstmBias, float, SigHmlstmBias>(P, nullptr);
+            CK(cudaDeviceSynchronize());
+        }
     }
     if (which == "k2c3") {  // one default-tiling config-3 pullback, for ncu
         Problem<float> P(true, 1024, 1024);
