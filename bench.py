@@ -391,6 +391,8 @@ def run_native(args, w: Workload, rank: int, world: int):
                 continue
             if key == "tape":
                 extra[key] = measure_tape(device, stream, max(5, K // 2))
+            elif key == "shards":
+                extra[key] = measure_shards(device, stream, max(5, K // 2))
             elif key == "arity":
                 extra[key] = measure_arity(device, stream, max(5, K // 2))
             elif key.endswith(":r"):  # RecomputeReverse: K1p primal + fused K2r
@@ -565,6 +567,26 @@ def measure_tape(device, stream, steps: int):
     return out
 
 
+def measure_shards(device, stream, steps: int):
+    """Config 5 strong scaling, the compute side, on one GPU: the step of the
+    batch shard one of G GPUs owns (B = 65536 / G rows of the bias variant,
+    partition.plan) timed here for G = 1, 2, 4, 8. The projected G-GPU step
+    is the shard step plus the NCCL allreduce of the 3 x H reduced (1,H)
+    adjoints (48 KB), which this single-GPU run cannot time; efficiency is
+    reported without it. A projection, not a multi-GPU measurement."""
+    base = WORKLOADS["cfg5"]
+    out = {"workload": base.describe, "note": "per-shard step on one B200; allreduce of 3*H fp32 not included"}
+    t1 = None
+    for G in (1, 2, 4, 8):
+        w = Workload(base.key, base.B // G, base.H, base.dtype, base.variant, base.describe)
+        r = measure_secondary(w, device, stream, steps, 0)
+        t1 = r["ms_per_step"] if G == 1 else t1
+        out[f"G{G}"] = {"B_per_gpu": w.B, "shard_ms_per_step": r["ms_per_step"], "step_frac_hbm": r["step_frac_hbm"],
+                        "projected_value": base.B * base.H / (r["ms_per_step"] * 1e-3),
+                        "projected_efficiency": t1 / (G * r["ms_per_step"])}
+    return out
+
+
 def measure_arity(device, stream, steps: int):
     """Paper §3.4.1 / Fig. 3 on B200: forward-mode diagonal Jacobian of
     tanh_product_A (arity_workload.hpp:19-28) at 4096 x 4096 fp32 (large
@@ -600,9 +622,10 @@ def main():
     ap.add_argument("--policy", type=int, default=0, help="0 CacheForward, 1 RecomputeReverse")
     ap.add_argument("--e2e-steps", type=int, default=10)
     ap.add_argument("--graph", type=int, default=1, help="1: replay the step as a captured CUDA graph")
-    ap.add_argument("--extra", default="cfg3,cfg4,cfg4div,cfg5,cfg2:r,cfg5:r,tape,arity",
+    ap.add_argument("--extra", default="cfg3,cfg4,cfg4div,cfg5,cfg2:r,cfg5:r,tape,arity,shards",
                     help="secondary measurements at N=1 ('none' for none): configs, <cfg>:r = RecomputeReverse, "
-                         "tape = cell_gradients mixed vs reverse-unfused, arity = tanh_product study")
+                         "tape = cell_gradients mixed vs reverse-unfused, arity = tanh_product study, "
+                         "shards = config 5's per-GPU batch shards at G = 2, 4, 8 timed on this GPU")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=12.0)
     args = ap.parse_args()

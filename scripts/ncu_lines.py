@@ -68,8 +68,17 @@ def main():
     name, samples = sass_samples(rep, sub)
     funcs = line_maps(binary)
     n = len(samples)
-    # the function with the same instruction count and first opcode
-    cands = [f for f, m in funcs.items() if len(m) == n]
+    # the function with the same (normalised) demangled name, else the same
+    # instruction count
+    def norm(x):
+        x = re.sub(r"\((int|bool|unsigned int)\)", "", x).replace("false", "0").replace("true", "1")
+        return re.sub(r"\s+", "", x.split("(bcad_dev::")[0].split("(const")[0])
+    names = list(funcs)
+    dem = subprocess.run(["cu++filt"], input="\n".join(names), capture_output=True, text=True).stdout.splitlines()
+    want = norm(name)
+    cands = [f for f, dm in zip(names, dem) if norm(dm) == want and len(funcs[f]) == n]
+    if not cands:
+        cands = [f for f, m in funcs.items() if len(m) == n]
     if not cands:
         sys.exit(f"no function with {n} instructions in {binary}")
     fmap = funcs[cands[0]]
