@@ -113,11 +113,10 @@ int bcad_cu_forward(bcad_cu_kernel k, int dtype, int n_in, const void* const* in
                     const bcad_cu_shape* in_shapes, int m_out, void* const* primal_out,
                     void* const* partials_out, void* stream);
 
-/* Bytes of device workspace bcad_cu_pullback needs for this problem. The
- * workspace must be zero-filled once when first allocated; a pullback leaves
- * it reusable by later pullbacks of the SAME kernel, dtype and shapes (its
- * completion counters return to zero). Problems of different shapes need
- * their own workspaces (or a re-zeroed one): their layouts differ. */
+/* Bytes of device workspace bcad_cu_pullback needs for this problem: the
+ * fp64 per-tile partials of reductions that span several CTAs (combined by a
+ * second, programmatically dependent launch). It needs no initialisation and
+ * carries no state between calls; concurrent pullbacks need separate ones. */
 int bcad_cu_pullback_workspace(bcad_cu_kernel k, int dtype, int n_in, const bcad_cu_shape* in_shapes,
                                int m_out, size_t* bytes);
 

@@ -191,7 +191,7 @@ int64_t pipelined_step(bcad_cu_kernel k, int n_in, const void* const* host_in, c
         g.push_back(alloc(has_g[j] ? volume(shapes[j]) : 1));
     }
     const int64_t rows = (B + chunks - 1) / chunks, last = B - (chunks - 1) * rows;
-    // one zeroed workspace per distinct chunk shape (layouts differ by shape)
+    // one workspace per distinct chunk shape
     std::vector<std::unique_ptr<detail::DeviceBuffer>> ws;
     std::size_t ws_bytes[2] = {0, 0};
     for (int q = 0; q < (last == rows ? 1 : 2); ++q) {
@@ -200,7 +200,6 @@ int64_t pipelined_step(bcad_cu_kernel k, int n_in, const void* const* host_in, c
             if (split[j]) cs[j].dims[0] = q == 0 ? rows : last;
         check(bcad_cu_pullback_workspace(k, dt, n_in, cs.data(), m_out, &ws_bytes[q]));
         ws.push_back(std::make_unique<detail::DeviceBuffer>(ws_bytes[q], comp));
-        check(bcad_cu_memset(ws.back()->ptr, 0, ws_bytes[q], comp));
     }
     {
         CopyBatch rep(0);  // batch-broadcast inputs: whole, on the compute stream

@@ -7,13 +7,15 @@
 //                   stride-0 scalar loads for ROW/SCALAR ones; no expansion.
 //   pull2d      K2  pullback: w (.) D summed over outputs, written elementwise
 //                   for FULL arguments and sum-reduced over broadcast axes
-//                   for ROW (warp shuffles), COL (CTA shared-memory tiles +
-//                   fp64 per-tile partials) and SCALAR arguments; the last
-//                   CTA of a tile row/column (integer ticket) combines the
-//                   partials in fixed order. No floating-point atomics;
-//                   bitwise deterministic run to run. With kRecompute the
-//                   partials are re-derived from the inputs in the same pass
-//                   (RecomputeReverse, mixed.hpp:75-90) instead of read.
+//                   for ROW (warp shuffles), COL (CTA shared-memory tiles)
+//                   and SCALAR arguments; a reduction spanning several CTAs
+//                   leaves fp64 per-tile partials that K2f combines in fixed
+//                   order. No floating-point atomics; bitwise deterministic
+//                   run to run. With kRecompute the partials are re-derived
+//                   from the inputs in the same pass (RecomputeReverse,
+//                   mixed.hpp:75-90) instead of read.
+//   pull_finish K2f the cross-CTA combination, a programmatically dependent
+//                   launch after K2 (only when a reduction spans CTAs).
 //   fwd_generic / pull_generic   rank-N fallbacks (3+ irreducible axis
 //                   groups, odd widths, misaligned pointers).
 #pragma once
@@ -352,54 +354,8 @@ struct Pull2DParams {
     double* ws_row;       // [n_row_args][n_col_tiles][rows]
     double* ws_col;       // [n_col_args][n_row_tiles][cols]
     double* ws_scalar;    // [n_scalar_args][n_ctas]
-    unsigned int* counters;  // [n_row_tiles] [n_col_tiles] [1]
     unsigned long long* err;
 };
-
-// Last-CTA combination of cross-CTA fp64 partials, all threads of the CTA:
-// item `it` needs sum_{q < n} part(it)[q * stride]. Each item's n partials
-// are cut into G contiguous groups (G chosen so items x G covers the CTA a
-// few times); a thread sums one (item, group) unit with its loads issued 16
-// at a time from L2 (__ldcg: written by other CTAs), the group sums land in
-// shared memory, and the item's result adds them in group order. The
-// association is fixed by (n, n_items), so results are bitwise run-to-run
-// deterministic. `scratch` holds at least n_items * G doubles (G <= 8).
-template <class Base, class Fin>
-__device__ __forceinline__ void cta_combine(int n_items, int n, size_t stride, double* scratch, int scratch_cap,
-                                            Base base, Fin fin) {
-    // G minimises the per-thread count of dependent 16-load batches
-    int G = 1, best = 0x7fffffff;
-    for (int g = 1; g <= 8; g *= 2) {
-        if (g > 1 && n_items * g > scratch_cap) break;
-        const int batches = ((n_items * g + kThreads - 1) / kThreads) * (((n + g - 1) / g + 15) / 16);
-        if (batches < best) best = batches, G = g;
-    }
-    const int per = (n + G - 1) / G;
-    for (int u = threadIdx.x; u < n_items * G; u += kThreads) {
-        const int it = u / G, grp = u % G;
-        const double* b = base(it);
-        const int q0 = grp * per, q1 = min(n, q0 + per);
-        double acc = 0.0;
-        int q = q0;
-        for (; q + 16 <= q1; q += 16) {
-            double v[16];
-#pragma unroll
-            for (int k = 0; k < 16; ++k) v[k] = __ldcg(b + size_t(q + k) * stride);
-#pragma unroll
-            for (int k = 0; k < 16; ++k) acc += v[k];
-        }
-        for (; q < q1; ++q) acc += __ldcg(b + size_t(q) * stride);
-        if (G == 1) fin(it, acc);
-        else scratch[u] = acc;
-    }
-    if (G == 1) return;
-    __syncthreads();
-    for (int it = threadIdx.x; it < n_items; it += kThreads) {
-        double acc = 0.0;
-        for (int grp = 0; grp < G; ++grp) acc += scratch[it * G + grp];
-        fin(it, acc);
-    }
-}
 
 template <class T>
 __device__ __forceinline__ T finish(double s, const T* slot_ptr, bool accumulate) {
@@ -424,8 +380,8 @@ __global__ void __launch_bounds__(kThreads, kRecompute ? 2 : kCtasPerSm) pull2d_
     constexpr bool kAnyCol = !S::kStatic || S::has(kCol);
     constexpr bool kAnyScal = !S::kStatic || S::has(kScalar);
     extern __shared__ double smem[];
-    __shared__ unsigned int s_last;
     pdl_wait();
+    pdl_trigger();  // lets the finisher (if any) be scheduled; it waits for this grid to complete
     if constexpr (Body::kMayRaise && kRecompute) s_err_flag[threadIdx.x] = 0;
 
     const int tid = threadIdx.x;
@@ -620,90 +576,81 @@ __global__ void __launch_bounds__(kThreads, kRecompute ? 2 : kCtasPerSm) pull2d_
                 }
             }
         }
-        const int smem_cap = int(pull_smem_doubles(p.n_col_args, p.n_row_args, p.n_scalar_args, V, p.rpt, p.ty, wpr));
-        const bool need_row = kAnyRow && p.n_row_args > 0 && p.n_col_tiles > 1;
-        const bool need_col = kAnyCol && p.n_col_args > 0 && p.n_row_tiles > 1;
-        const bool need_scal = kAnyScal && p.n_scalar_args > 0 && n_ctas > 1;
-        if (!(need_row || need_col || need_scal)) return;
-
-        // ---- cross-CTA completion: the last CTA of a tile row / column /
-        // grid (integer ticket) combines the fp64 partials in tile order.
-        // Release: the barrier orders the CTA's partial writes before thread
-        // 0's gpu-scope fence and ticket (fences are cumulative), so only one
-        // thread per CTA waits on the fence.
-        __syncthreads();
-        if (need_row) {
-            if (tid == 0) {
-                __threadfence();
-                s_last = atomicAdd(&p.counters[rt], 1u) == unsigned(p.n_col_tiles - 1);
-            }
-            __syncthreads();
-            if (s_last) {
-                __threadfence();
-                const int64_t rb = int64_t(rt) * p.tile_rows;
-                const int nr = int(min(p.tile_rows, p.rows - rb));
-                cta_combine(
-                    p.n_row_args * nr, p.n_col_tiles, size_t(p.rows), smem, smem_cap,
-                    [&](int it) { return p.ws_row + size_t(it / nr) * p.n_col_tiles * p.rows + rb + it % nr; },
-                    [&](int it, double sacc) {
-                        const int j = p.row_j[it / nr];
-                        const int64_t r = rb + it % nr;
-                        p.adj[j][r] = finish<T>(sacc, p.adj[j] + r, (p.acc_mask >> j) & 1u);
-                    });
-                if (tid == 0) p.counters[rt] = 0;
-            }
-            __syncthreads();
-        }
-        if (need_col) {
-            if (tid == 0) {
-                __threadfence();
-                s_last = atomicAdd(&p.counters[p.n_row_tiles + ct], 1u) == unsigned(p.n_row_tiles - 1);
-            }
-            __syncthreads();
-            if (s_last) {
-                __threadfence();
-                const int64_t cb = int64_t(ct) * ccols;
-                const int nc = int(min(int64_t(ccols), p.cols - cb));
-                cta_combine(
-                    p.n_col_args * nc, p.n_row_tiles, size_t(p.cols), smem, smem_cap,
-                    [&](int it) { return p.ws_col + size_t(it / nc) * p.n_row_tiles * p.cols + cb + it % nc; },
-                    [&](int it, double sacc) {
-                        const int j = p.col_j[it / nc];
-                        const int64_t c = cb + it % nc;
-                        p.adj[j][c] = finish<T>(sacc, p.adj[j] + c, (p.acc_mask >> j) & 1u);
-                    });
-                if (tid == 0) p.counters[p.n_row_tiles + ct] = 0;
-            }
-            __syncthreads();
-        }
-        if (need_scal) {
-            unsigned int* cnt = &p.counters[p.n_row_tiles + p.n_col_tiles];
-            if (tid == 0) {
-                __threadfence();
-                s_last = atomicAdd(cnt, 1u) == unsigned(n_ctas - 1);
-            }
-            __syncthreads();
-            if (s_last) {
-                __threadfence();
-                for (int a = 0; a < p.n_scalar_args; ++a) {
-                    double sacc = 0.0;
-                    for (int64_t q = tid; q < n_ctas; q += kThreads) sacc += __ldcg(&p.ws_scalar[size_t(a) * n_ctas + q]);
-                    scal_acc[a * kThreads + tid] = sacc;
-                    __syncthreads();
-                    for (int stride = kThreads / 2; stride > 0; stride >>= 1) {
-                        if (tid < stride) scal_acc[a * kThreads + tid] += scal_acc[a * kThreads + tid + stride];
-                        __syncthreads();
-                    }
-                    if (tid == 0) {
-                        const int j = p.scal_j[a];
-                        p.adj[j][0] = finish<T>(scal_acc[a * kThreads], p.adj[j], (p.acc_mask >> j) & 1u);
-                    }
-                    __syncthreads();
-                }
-                if (tid == 0) *cnt = 0;
-            }
-        }
     }
+}
+
+// K2f: the cross-CTA combination of K2's fp64 tile partials as a separate,
+// programmatically dependent launch (it waits for K2's grid, so no fences or
+// tickets in K2 itself). A CTA owns 32 consecutive reduced output elements
+// (lane = element, so every load is coalesced across the warp); its 8 warps
+// split the tile partials into 8 contiguous groups, and the group sums are
+// added in group order. Scalar arguments get one CTA each (strided sums, a
+// fixed-shape tree). Fixed association: bitwise run-to-run deterministic.
+template <int N, int M, class T>
+__global__ void __launch_bounds__(kThreads) pull_finish_kernel(const __grid_constant__ Pull2DParams<N, M, T> p) {
+    pdl_wait();
+    __shared__ double part[kThreads];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t n_ctas = int64_t(p.n_row_tiles) * p.n_col_tiles;
+    const int64_t row_items = p.n_col_tiles > 1 ? int64_t(p.n_row_args) * p.rows : 0;
+    const int64_t col_items = p.n_row_tiles > 1 ? int64_t(p.n_col_args) * p.cols : 0;
+    const int64_t row_blocks = (row_items + 31) / 32, col_blocks = (col_items + 31) / 32;
+    const int64_t b = blockIdx.x;
+    if (b >= row_blocks + col_blocks) {  // one scalar argument
+        const int a = int(b - row_blocks - col_blocks);
+        double acc = 0.0;
+        for (int64_t q = threadIdx.x; q < n_ctas; q += kThreads) acc += p.ws_scalar[size_t(a) * n_ctas + q];
+        part[threadIdx.x] = acc;
+        __syncthreads();
+        for (int stride = kThreads / 2; stride > 0; stride >>= 1) {
+            if (threadIdx.x < stride) part[threadIdx.x] += part[threadIdx.x + stride];
+            __syncthreads();
+        }
+        if (threadIdx.x == 0) {
+            const int j = p.scal_j[a];
+            p.adj[j][0] = finish<T>(part[0], p.adj[j], (p.acc_mask >> j) & 1u);
+        }
+        return;
+    }
+    const bool is_row = b < row_blocks;
+    const int64_t it = (is_row ? b : b - row_blocks) * 32 + lane;
+    const int64_t items = is_row ? row_items : col_items, len = is_row ? p.rows : p.cols;
+    const int n = is_row ? p.n_col_tiles : p.n_row_tiles;
+    const bool valid = it < items;
+    const int a = valid ? int(it / len) : 0;
+    const int64_t e = valid ? it % len : 0;
+    const double* base = (is_row ? p.ws_row : p.ws_col) + size_t(a) * n * len + e;
+    const int per = (n + 7) / 8, q0 = warp * per, q1 = min(n, q0 + per);
+    double acc = 0.0;
+    if (valid) {
+        int q = q0;
+        for (; q + 8 <= q1; q += 8) {
+            double v[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) v[u] = base[size_t(q + u) * len];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) acc += v[u];
+        }
+        for (; q < q1; ++q) acc += base[size_t(q) * len];
+    }
+    part[warp * 32 + lane] = acc;
+    __syncthreads();
+    if (warp == 0 && valid) {
+        double s = 0.0;
+#pragma unroll
+        for (int g = 0; g < 8; ++g) s += part[g * 32 + lane];
+        const int j = is_row ? p.row_j[a] : p.col_j[a];
+        p.adj[j][e] = finish<T>(s, p.adj[j] + e, (p.acc_mask >> j) & 1u);
+    }
+}
+
+// Blocks of pull_finish_kernel for a tiling (0 = nothing to combine).
+inline int64_t pull_finish_blocks(int64_t rows, int64_t cols, int n_row_tiles, int n_col_tiles, int n_row_args,
+                                  int n_col_args, int n_scalar_args) {
+    const int64_t ri = n_col_tiles > 1 ? int64_t(n_row_args) * rows : 0;
+    const int64_t ci = n_row_tiles > 1 ? int64_t(n_col_args) * cols : 0;
+    const int64_t si = int64_t(n_row_tiles) * n_col_tiles > 1 ? n_scalar_args : 0;
+    return (ri + 31) / 32 + (ci + 31) / 32 + si;
 }
 
 // ------------------------------------------------------- generic kernels

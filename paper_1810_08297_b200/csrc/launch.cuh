@@ -211,8 +211,8 @@ int launch_pull_t(const PullArgs& a, std::string* err) {
         p.ws_row = reinterpret_cast<double*>(ws + L.ws_row);
         p.ws_col = reinterpret_cast<double*>(ws + L.ws_col);
         p.ws_scalar = reinterpret_cast<double*>(ws + L.ws_scalar);
-        p.counters = reinterpret_cast<unsigned int*>(ws + L.counters);
         p.err = a.err;
+        const int64_t fin_blocks = bcad_dev::pull_finish_blocks(plan.rows, plan.cols, p.n_row_tiles, p.n_col_tiles, nr, nc, ns);
         const size_t smem = pull_smem_bytes(nc, nr, ns, t);
         const dim3 grid(unsigned(t.n_col_tiles), unsigned(t.n_row_tiles));
         bool dense = p.acc_mask == 0;  // every w and adjoint present, nothing accumulated
@@ -231,7 +231,10 @@ int launch_pull_t(const PullArgs& a, std::string* err) {
                 const cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
                 if (e != cudaSuccess) return cuda_status(e, err);
             }
-            return cuda_status(launch_pdl(kern, grid, smem, a.stream, p), err);
+            int rc = cuda_status(launch_pdl(kern, grid, smem, a.stream, p), err);
+            if (rc || fin_blocks == 0) return rc;
+            return cuda_status(launch_pdl(&bcad_dev::pull_finish_kernel<N, M, T>, dim3(unsigned(fin_blocks)), 0,
+                                          a.stream, p), err);
         });
     }
     bcad_dev::GenParams<N, M, T> g{};

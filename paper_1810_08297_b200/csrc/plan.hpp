@@ -213,12 +213,14 @@ inline Tiling choose_tiling(const Plan& p, int V, const ClassMix& mix, bool fine
     return t;
 }
 
-// Workspace (global, fp64 tile partials + tickets) and dynamic shared memory
-// of the 2-D pullback. Offsets are sized for every argument of a class, so a
-// workspace queried once serves any subset of wanted adjoints.
+// Workspace (global, fp64 tile partials read by the finisher K2f) and
+// dynamic shared memory of the 2-D pullback. Offsets are sized for every
+// argument of a class, so a workspace queried once serves any subset of
+// wanted adjoints. Every partial is written before it is read: no
+// initialisation and no state carried between pullbacks.
 struct PullLayout {
     int n_row_args = 0, n_col_args = 0, n_scalar_args = 0;
-    size_t ws_row = 0, ws_col = 0, ws_scalar = 0, counters = 0, total = 0;
+    size_t ws_row = 0, ws_col = 0, ws_scalar = 0, total = 0;
     size_t smem = 0;
 };
 
@@ -243,8 +245,6 @@ inline PullLayout pull_layout(const Plan& p, const Tiling& t) {
     if (t.n_row_tiles > 1) off += align256(size_t(L.n_col_args) * t.n_row_tiles * p.cols * 8);
     L.ws_scalar = off;
     if (t.n_ctas > 1) off += align256(size_t(L.n_scalar_args) * t.n_ctas * 8);
-    L.counters = off;
-    off += align256(size_t(t.n_row_tiles + t.n_col_tiles + 1) * 4);
     L.total = off;
     L.smem = pull_smem_bytes(L.n_col_args, L.n_row_args, L.n_scalar_args, t);
     return L;

@@ -290,7 +290,8 @@ def fill(t, value: float, stream=None):
 
 
 def new_workspace(kernel: Kernel, shapes, dtype, device="cuda"):
-    """Zero-filled workspace of the size bcad_cu_pullback_workspace reports."""
+    """Workspace of the size bcad_cu_pullback_workspace reports (zero-filled,
+    though the kernels need no initialisation)."""
     import torch
     code = F32 if dtype == torch.float32 else F64
     nbytes = pullback_workspace(kernel, shapes, code)

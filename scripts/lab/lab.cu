@@ -374,7 +374,8 @@ int main(int argc, char** argv) {
         const std::vector<std::array<int, 3>> t3 = {{32, 1, 1}, {32, 2, 1}, {32, 4, 1}, {32, 8, 1},
                                                      {16, 1, 1}, {16, 2, 1}, {16, 4, 1}, {16, 8, 1},
                                                      {8, 1, 1}, {8, 2, 1}, {8, 4, 1}, {8, 8, 1},
-                                                     {64, 2, 1}, {64, 4, 1}, {128, 2, 1}, {256, 2, 1}};
+                                                     {64, 2, 1}, {64, 4, 1}, {128, 1, 1}, {128, 2, 1}, {256, 1, 1},
+                                                     {256, 2, 1}};
         k2_sweep<KHmlstmBias, float, SigHmlstmBias>("k2_cfg3", true, 1024, 1024, t3);
     }
     if (which == "k1c2") {  // default-tiling config-2 forwards, for ncu
