@@ -246,6 +246,10 @@ class Case:
             else:
                 self.adj.append(torch.empty(s, device=device, dtype=dt))
         self.ws = native.new_workspace(self.k, shapes, dt, device)
+        # K1 + K2, plus the finisher K2f when a reduction spans CTAs (its
+        # tile partials are what the workspace holds)
+        code = native.F32 if dt == torch.float32 else native.F64
+        self.launches = 3 if native.pullback_workspace(self.k, shapes, code) > 0 else 2
         self.step = native.PreparedStep(self.k, ins, self.primal, self.partials, [self.seed], self.adj, self.ws,
                                         policy=policy)
 
@@ -425,7 +429,7 @@ def run_native(args, w: Workload, rank: int, world: int):
                 "d2h_bytes_per_step": e2e["d2h"], "ms_per_step": e2e["ms_per_step"],
                 "schedule": "row-chunk pipelined host step (bcad_host_set_pipeline auto)",
                 "one_shot_ms_per_step": e2e["one_shot_ms_per_step"], "pcie": e2e["pcie"]},
-        "gpu_launches": 2 * K,
+        "gpu_launches": case.launches * K,
         "clocks": clock_info,
     }
     if cpu:

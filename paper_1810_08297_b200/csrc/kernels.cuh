@@ -35,6 +35,7 @@ using bcad_cu_impl::kRow;
 using bcad_cu_impl::kScalar;
 using bcad_cu_impl::kThreads;
 using bcad_cu_impl::kCtasPerSm;
+using bcad_cu_impl::kRecomputeCtasPerSm;
 
 // ----------------------------------------------------------- vector I/O
 template <class T, int V> struct alignas(sizeof(T) * V) Pack { T x[V]; };
@@ -47,6 +48,9 @@ __device__ __forceinline__ Pack<T, V> ld_stream(const T* p) {
         r.x[0] = v.x; r.x[1] = v.y; r.x[2] = v.z; r.x[3] = v.w;
     } else if constexpr (V == 2 && sizeof(T) == 8) {
         const double2 v = __ldcs(reinterpret_cast<const double2*>(p));
+        r.x[0] = v.x; r.x[1] = v.y;
+    } else if constexpr (V == 2 && sizeof(T) == 4) {
+        const float2 v = __ldcs(reinterpret_cast<const float2*>(p));
         r.x[0] = v.x; r.x[1] = v.y;
     } else {
 #pragma unroll
@@ -64,6 +68,9 @@ __device__ __forceinline__ Pack<T, V> ld_ro(const T* p) {  // read-only, may be 
     } else if constexpr (V == 2 && sizeof(T) == 8) {
         const double2 v = __ldg(reinterpret_cast<const double2*>(p));
         r.x[0] = v.x; r.x[1] = v.y;
+    } else if constexpr (V == 2 && sizeof(T) == 4) {
+        const float2 v = __ldg(reinterpret_cast<const float2*>(p));
+        r.x[0] = v.x; r.x[1] = v.y;
     } else {
 #pragma unroll
         for (int v = 0; v < V; ++v) r.x[v] = __ldg(p + v);
@@ -77,6 +84,8 @@ __device__ __forceinline__ void st_vec(T* p, const Pack<T, V>& r) {
         *reinterpret_cast<float4*>(p) = make_float4(r.x[0], r.x[1], r.x[2], r.x[3]);
     } else if constexpr (V == 2 && sizeof(T) == 8) {
         *reinterpret_cast<double2*>(p) = make_double2(r.x[0], r.x[1]);
+    } else if constexpr (V == 2 && sizeof(T) == 4) {
+        *reinterpret_cast<float2*>(p) = make_float2(r.x[0], r.x[1]);
     } else {
 #pragma unroll
         for (int v = 0; v < V; ++v) p[v] = r.x[v];
@@ -374,7 +383,7 @@ __host__ __device__ inline size_t pull_smem_doubles(int n_col, int n_row, int n_
 // (mixed.hpp:34-38); FULL slots get the reference's element arithmetic,
 // reduced slots an fp64 sum of those terms in a fixed order.
 template <class Body, class T, int V, bool kRecompute, class S, bool kDense>
-__global__ void __launch_bounds__(kThreads, kRecompute ? 2 : kCtasPerSm) pull2d_kernel(const __grid_constant__ Pull2DParams<Body::kIn, Body::kOut, T> p) {
+__global__ void __launch_bounds__(kThreads, kRecompute ? kRecomputeCtasPerSm : kCtasPerSm) pull2d_kernel(const __grid_constant__ Pull2DParams<Body::kIn, Body::kOut, T> p) {
     constexpr int N = Body::kIn, M = Body::kOut;
     constexpr bool kAnyRow = !S::kStatic || S::has(kRow);
     constexpr bool kAnyCol = !S::kStatic || S::has(kCol);

@@ -149,6 +149,11 @@ struct Tiling {
 
 constexpr int kSmCount = 148;
 constexpr int kCtasPerSm = 4;  // 256-thread CTAs at <= 64 registers per thread
+// RecomputeReverse pullback (duals re-derived in registers): three CTAs per
+// SM (<= 80 registers; the registered HM-LSTM signatures fit without spills).
+// Same cells per thread and tiling as the cached pullback, so both policies
+// reduce in the same order and agree bit for bit (mixed.hpp:103-130).
+constexpr int kRecomputeCtasPerSm = 3;
 constexpr int64_t kMaxGridY = 65535;
 
 inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }

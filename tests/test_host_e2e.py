@@ -133,3 +133,29 @@ def test_host_set_pipeline_rejects_negative(host):
     from paper_1810_08297_b200 import native
     with pytest.raises(native.ConfigError):
         H.set_pipeline(-1)
+
+
+@pytest.mark.parametrize("dtype", [np.float32, np.float64])
+def test_host_step_pipelined_scalar_and_two_outputs(host, oracle_lib, dtype):
+    """Pipelining with a scalar (batch-broadcast) argument, a (B, 1)-shaped
+    argument and a two-output kernel (prod_diff: a*b, a-b): the scalar's
+    gradient is summed over chunks, both seeds are chunked."""
+    from paper_1810_08297_b200 import host as H
+    rng = np.random.default_rng(7)
+    B, W = 37, 48
+    for shapes in ([(B, W), ()], [(B, W), (B, 1)], [(B, 1), (1, W)]):
+        ins = [rng.uniform(-1, 1, s).astype(dtype) for s in shapes]
+        out_shape = O.broadcast_shape_py(shapes)
+        seeds = [rng.uniform(-1, 1, out_shape).astype(dtype) for _ in range(2)]
+        try:
+            H.set_pipeline(1)
+            p1, g1, peak1 = host_step(host, "prod_diff", ins, seeds, 0)
+            H.set_pipeline(5)
+            pk, gk, peakk = host_step(host, "prod_diff", ins, seeds, 0)
+        finally:
+            H.set_pipeline(0)
+        for a, b in zip(p1, pk):
+            assert np.array_equal(a, b)
+        assert peak1 == peakk
+        _, want_g, want_a64 = oracle_lib.mixed_step("prod_diff", ins, 0, seeds)
+        assert_grads(gk, want_g, want_a64, shapes, out_shape, dtype, f"pipelined prod_diff {shapes}")
