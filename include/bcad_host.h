@@ -46,7 +46,7 @@ int bcad_host_cell_gradients(int impl, int dtype, int64_t n, const void* const* 
  * of the next and the device->host copy of the previous overlap. Rows are
  * independent under first-axis broadcasting (shape.hpp:13-16); gradients of
  * batch-broadcast arguments (axis 0 of length 1, or scalars) are summed over
- * chunks in chunk order on the device. max_chunks: 0 = automatic (about 12 MiB
+ * chunks in chunk order on the device. max_chunks: 0 = automatic (about 9 MiB
  * of host<->device traffic per chunk, at most 16 chunks), 1 = off (one tape
  * over the whole batch), k > 1 = at most k chunks. Kernels that may raise
  * always run one-shot so error indices match the reference. Process-wide. */

@@ -92,9 +92,9 @@ std::atomic<int> g_pipeline{0};  // 0 auto, 1 off, k > 1 at most k chunks
 
 // Auto chunking: each chunk costs two batched copy calls, two launches and
 // two events, and the last chunk's download is exposed, so chunks stay
-// large (measured on B200 over PCIe: 3-4 chunks of ~10-13 MB beat both the
+// large (measured on B200 over PCIe: ~4 chunks of ~9-10 MB beat both the
 // one-shot step and finer pipelines at configs 2 and 3).
-constexpr std::size_t kChunkBytes = std::size_t(12) << 20;  // host<->device bytes per chunk
+constexpr std::size_t kChunkBytes = std::size_t(9) << 20;  // host<->device bytes per chunk
 constexpr int kMaxChunks = 16;
 
 struct Pipe {
@@ -190,17 +190,36 @@ int64_t pipelined_step(bcad_cu_kernel k, int n_in, const void* const* host_in, c
         has_g[j] = host_grads && host_grads[j];
         g.push_back(alloc(has_g[j] ? volume(shapes[j]) : 1));
     }
-    const int64_t rows = (B + chunks - 1) / chunks, last = B - (chunks - 1) * rows;
-    // one workspace per distinct chunk shape
-    std::vector<std::unique_ptr<detail::DeviceBuffer>> ws;
-    std::size_t ws_bytes[2] = {0, 0};
-    for (int q = 0; q < (last == rows ? 1 : 2); ++q) {
+    // Chunk boundaries: the first and last chunks get half the rows of the
+    // others, so the pipeline fills and drains faster (the exposed head is
+    // the first chunk's upload, the exposed tail the last chunk's download).
+    std::vector<int64_t> bound(static_cast<std::size_t>(chunks) + 1, 0);
+    {
+        const double units = chunks > 2 ? double(chunks) - 1.0 : double(chunks);
+        double acc = 0.0;
+        for (int c = 0; c < chunks; ++c) {
+            acc += (chunks > 2 && (c == 0 || c == chunks - 1)) ? 0.5 : 1.0;
+            bound[c + 1] = c + 1 == chunks ? B
+                                           : std::min(B - (chunks - c - 1),
+                                                      std::max(bound[c] + 1, int64_t(double(B) * acc / units + 0.5)));
+        }
+    }
+    // one workspace per distinct chunk height
+    std::vector<std::pair<int64_t, std::unique_ptr<detail::DeviceBuffer>>> ws;
+    std::vector<std::size_t> ws_bytes;
+    auto ws_for = [&](int64_t r) -> std::size_t {
+        for (std::size_t q = 0; q < ws.size(); ++q)
+            if (ws[q].first == r) return q;
         std::vector<bcad_cu_shape> cs(shapes, shapes + n_in);
         for (int j = 0; j < n_in; ++j)
-            if (split[j]) cs[j].dims[0] = q == 0 ? rows : last;
-        check(bcad_cu_pullback_workspace(k, dt, n_in, cs.data(), m_out, &ws_bytes[q]));
-        ws.push_back(std::make_unique<detail::DeviceBuffer>(ws_bytes[q], comp));
-    }
+            if (split[j]) cs[j].dims[0] = r;
+        std::size_t b = 0;
+        check(bcad_cu_pullback_workspace(k, dt, n_in, cs.data(), m_out, &b));
+        ws.emplace_back(r, std::make_unique<detail::DeviceBuffer>(b, comp));
+        ws_bytes.push_back(b);
+        return ws.size() - 1;
+    };
+    for (int c = 0; c < chunks; ++c) (void)ws_for(bound[c + 1] - bound[c]);
     {
         CopyBatch rep(0);  // batch-broadcast inputs: whole, on the compute stream
         for (int j = 0; j < n_in; ++j)
@@ -216,8 +235,8 @@ int64_t pipelined_step(bcad_cu_kernel k, int n_in, const void* const* host_in, c
     std::vector<void*> yp(m), Dw(m * n), gp(n);
     std::vector<unsigned char> acc(n, 0);
     int c = 0;
-    for (int64_t b0 = 0; b0 < B; b0 += rows, ++c) {
-        const int64_t b1 = std::min(B, b0 + rows), r = b1 - b0;
+    for (; c < chunks; ++c) {
+        const int64_t b0 = bound[c], b1 = bound[c + 1], r = b1 - b0;
         const std::size_t cell0 = static_cast<std::size_t>(b0 * out_row), cells = static_cast<std::size_t>(r * out_row);
         // h2d: this chunk's rows of the batch-sharded inputs and of the seeds
         CopyBatch up(0);
@@ -251,7 +270,7 @@ int64_t pipelined_step(bcad_cu_kernel k, int n_in, const void* const* host_in, c
         }
         check(bcad_cu_forward(k, dt, n_in, xin.data(), cs.data(), m_out, yp.data(), policy == 0 ? Dw.data() : nullptr, comp));
         check(bcad_cu_pullback(k, dt, n_in, cs.data(), m_out, wp.data(), policy == 0 ? Dp.data() : nullptr, xin.data(),
-                               gp.data(), acc.data(), ws[r == rows ? 0 : 1]->ptr, ws_bytes[r == rows ? 0 : 1], comp));
+                               gp.data(), acc.data(), ws[ws_for(r)].second->ptr, ws_bytes[ws_for(r)], comp));
         check(bcad_cu_event_record(P.out_ready[c], comp));
         // d2h: the chunk's primal rows and batch-sharded gradient rows
         check(bcad_cu_stream_wait_event(P.d2h, P.out_ready[c]));

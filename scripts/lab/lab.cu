@@ -378,6 +378,30 @@ int main(int argc, char** argv) {
                                                      {256, 2, 1}};
         k2_sweep<KHmlstmBias, float, SigHmlstmBias>("k2_cfg3", true, 1024, 1024, t3);
     }
+    if (which == "k1c2time") {  // config-2 K1 alone, repeated (A/B runs)
+        Problem<float> P(false, 1024, 1024);
+        for (int rep = 0; rep < 5; ++rep) {
+            const double us = time_us([&] { fwd<KHmlstm, float, SigHmlstmCanonical>(P, nullptr); }, 41);
+            std::printf("{\"exp\": \"k1c2time\", \"rep\": %d, \"us\": %.3f}\n", rep, us);
+        }
+    }
+    if (which == "k1time") {  // default-tiling K1 timings: cfg2, cfg3, cfg5-per-G8-shard, cfg5 sizes
+        for (auto [bias, B, H] : {std::tuple<bool, int64_t, int64_t>{false, 1024, 1024}, {true, 1024, 1024},
+                                  {true, 8192, 4096}, {true, 65536, 4096}, {false, 8192, 4096}}) {
+            if (bias) {
+                Problem<float> P(true, B, H);
+                const double us = time_us([&] { fwd<KHmlstmBias, float, SigHmlstmBias>(P, nullptr); }, 15);
+                std::printf("{\"exp\": \"k1time\", \"bias\": 1, \"B\": %lld, \"H\": %lld, \"us\": %.3f, \"GBps\": %.1f}\n",
+                            (long long)B, (long long)H, us, double(P.k1_bytes) / (us * 1e-6) / 1e9);
+            } else {
+                Problem<float> P(false, B, H);
+                const double us = time_us([&] { fwd<KHmlstm, float, SigHmlstmCanonical>(P, nullptr); }, 15);
+                std::printf("{\"exp\": \"k1time\", \"bias\": 0, \"B\": %lld, \"H\": %lld, \"us\": %.3f, \"GBps\": %.1f}\n",
+                            (long long)B, (long long)H, us, double(P.k1_bytes) / (us * 1e-6) / 1e9);
+            }
+            std::fflush(stdout);
+        }
+    }
     if (which == "k1c2") {  // default-tiling config-2 forwards, for ncu
         Problem<float> P(false, 1024, 1024);
         for (int k = 0; k < 3; ++k) fwd<KHmlstm, float, SigHmlstmCanonical>(P, nullptr);
