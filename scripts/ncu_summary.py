@@ -50,7 +50,8 @@ def raw(report):
                     continue
                 d[METRICS[k]] = x * UNIT_SCALE.get(u, 1)
         name = r[head.index("Kernel Name")]
-        d["kernel"] = "K1_forward" if "fwd2d" in name else "K2_pullback" if "pull2d" in name else name[:40]
+        d["kernel"] = ("K1_forward" if "fwd2d" in name else "K2_pullback" if "pull2d" in name
+                       else "K2f_finish" if "pull_finish" in name else name[:40])
         d["name"] = name.split("(")[0][:110]
         res.append(d)
     return res
@@ -65,7 +66,8 @@ def launch_shares(path):
         if r[mi] != "gpu__time_duration.sum":
             continue
         name = r[ki]
-        key = "K1 fwd2d" if "fwd2d" in name else "K2 pull2d" if "pull2d" in name else ("nccl" if "nccl" in name.lower() else "other (torch flush/fill/copy)")
+        key = ("K1 fwd2d" if "fwd2d" in name else "K2 pull2d" if "pull2d" in name else "K2f pull_finish"
+               if "pull_finish" in name else ("nccl" if "nccl" in name.lower() else "other (torch flush/fill/copy)"))
         t = float(r[vi].replace(",", "")) * UNIT_SCALE.get(r[ui], 1)
         per.setdefault(key, []).append(t)
     return per
@@ -100,7 +102,10 @@ def main():
             if d["kernel"] in seen:
                 continue
             seen.add(d["kernel"])
-            alg = w.k1_bytes() if d["kernel"] == "K1_forward" else w.k2_bytes()
+            if d["kernel"] == "K2f_finish":  # reads the fp64 tile partials, writes the reduced adjoints
+                alg = d.get("dram_read", 0) + d.get("dram_write", 0)
+            else:
+                alg = w.k1_bytes() if d["kernel"] == "K1_forward" else w.k2_bytes()
             dur = d.get("duration_us", float("nan"))
             gbs = alg / (dur * 1e-6) / 1e9
             act = d.get("sm_active_cycles", 0) / max(1, d.get("sm_elapsed_cycles", 1))
