@@ -155,6 +155,8 @@ int bcad_cu_malloc(void** ptr, size_t bytes, void* stream);
 int bcad_cu_free(void* ptr, void* stream);
 int bcad_cu_host_alloc(void** ptr, size_t bytes); /* pinned host memory */
 int bcad_cu_host_free(void* ptr);
+/* 1 if `ptr` is page-locked (pinned / registered) host memory, else 0. */
+int bcad_cu_host_is_pinned(const void* ptr);
 /* kind: 0 host->device, 1 device->host, 2 device->device */
 int bcad_cu_memcpy(void* dst, const void* src, size_t bytes, int kind, void* stream);
 int bcad_cu_memset(void* ptr, int value, size_t bytes, void* stream);
@@ -174,6 +176,13 @@ int bcad_cu_event_create(void** event);
 int bcad_cu_event_destroy(void* event);
 int bcad_cu_event_record(void* event, void* stream);
 int bcad_cu_stream_wait_event(void* stream, void* event);
+/* CUDA graphs of enqueued work: capture everything enqueued on `stream` (and
+ * on streams joined to it through events) between begin and end into an
+ * executable graph; replay it with one launch. Capture is thread-local. */
+int bcad_cu_graph_capture_begin(void* stream);
+int bcad_cu_graph_capture_end(void* stream, void** graph_exec);
+int bcad_cu_graph_launch(void* graph_exec, void* stream);
+int bcad_cu_graph_destroy(void* graph_exec);
 
 /* ------------------------------------------------------ multi-GPU (NCCL) */
 /* NCCL is loaded at run time (dlopen libnccl.so.2); without it these return

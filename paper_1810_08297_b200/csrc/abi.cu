@@ -476,6 +476,12 @@ int bcad_cu_host_free(void* ptr) {
     CU_TRY(cudaFreeHost(ptr), "cudaFreeHost");
     return BCAD_CU_OK;
 }
+int bcad_cu_host_is_pinned(const void* ptr) {
+    cudaPointerAttributes at{};
+    const bool pinned = cudaPointerGetAttributes(&at, ptr) == cudaSuccess && at.type == cudaMemoryTypeHost;
+    (void)cudaGetLastError();
+    return pinned ? 1 : 0;
+}
 int bcad_cu_memcpy(void* dst, const void* src, size_t bytes, int kind, void* stream) {
     if (bytes == 0) return BCAD_CU_OK;
     const cudaMemcpyKind k = kind == 0 ? cudaMemcpyHostToDevice : kind == 1 ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice;
@@ -514,16 +520,20 @@ int bcad_cu_memcpy_batch(size_t n, void* const* dsts, const void* const* srcs, c
         }
         return BCAD_CU_OK;
     }
+    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+    if (s != nullptr && cudaStreamIsCapturing(s, &cap) != cudaSuccess) (void)cudaGetLastError();
     // The batch path is for pinned host memory; pageable buffers (which the
     // driver stages, and would otherwise lock page by page) go one by one.
-    bool pinned = true;
+    bool pinned = cap == cudaStreamCaptureStatusNone;
     for (size_t k = 0; k < d.size() && pinned; ++k) {
         cudaPointerAttributes at{};
         const void* host = kind == 0 ? sr[k] : d[k];
         if (cudaPointerGetAttributes(&at, host) != cudaSuccess || at.type != cudaMemoryTypeHost) pinned = false;
         (void)cudaGetLastError();
     }
-    if (s == nullptr || d.size() == 1 || !pinned) {  // the batch API rejects the legacy stream
+    // legacy stream (rejected by the batch API), pageable memory, or a graph
+    // capture (plain copy nodes; the per-call host cost is paid once)
+    if (s == nullptr || d.size() == 1 || !pinned || cap != cudaStreamCaptureStatusNone) {
         for (size_t k = 0; k < d.size(); ++k)
             CU_TRY(cudaMemcpyAsync(d[k], sr[k], sz[k], kind == 0 ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToHost, s),
                    "cudaMemcpyAsync");
@@ -577,6 +587,31 @@ int bcad_cu_event_destroy(void* event) {
 }
 int bcad_cu_event_record(void* event, void* stream) {
     CU_TRY(cudaEventRecord(static_cast<cudaEvent_t>(event), static_cast<cudaStream_t>(stream)), "cudaEventRecord");
+    return BCAD_CU_OK;
+}
+int bcad_cu_graph_capture_begin(void* stream) {
+    CU_TRY(cudaStreamBeginCapture(static_cast<cudaStream_t>(stream), cudaStreamCaptureModeThreadLocal),
+           "cudaStreamBeginCapture");
+    return BCAD_CU_OK;
+}
+int bcad_cu_graph_capture_end(void* stream, void** graph_exec) {
+    cudaGraph_t g = nullptr;
+    CU_TRY(cudaStreamEndCapture(static_cast<cudaStream_t>(stream), &g), "cudaStreamEndCapture");
+    cudaGraphExec_t e = nullptr;
+    const cudaError_t rc = cudaGraphInstantiate(&e, g, 0);
+    cudaGraphDestroy(g);
+    CU_TRY(rc, "cudaGraphInstantiate");
+    *graph_exec = e;
+    return BCAD_CU_OK;
+}
+int bcad_cu_graph_launch(void* graph_exec, void* stream) {
+    CU_TRY(cudaGraphLaunch(static_cast<cudaGraphExec_t>(graph_exec), static_cast<cudaStream_t>(stream)),
+           "cudaGraphLaunch");
+    return BCAD_CU_OK;
+}
+int bcad_cu_graph_destroy(void* graph_exec) {
+    if (!graph_exec) return BCAD_CU_OK;
+    CU_TRY(cudaGraphExecDestroy(static_cast<cudaGraphExec_t>(graph_exec)), "cudaGraphExecDestroy");
     return BCAD_CU_OK;
 }
 int bcad_cu_stream_wait_event(void* stream, void* event) {

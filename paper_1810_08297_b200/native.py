@@ -132,6 +132,7 @@ PROTOS = {
     "bcad_cu_free": (I, [VP, VP]),
     "bcad_cu_host_alloc": (I, [C.POINTER(VP), SZ]),
     "bcad_cu_host_free": (I, [VP]),
+    "bcad_cu_host_is_pinned": (I, [VP]),
     "bcad_cu_memcpy": (I, [VP, VP, SZ, I, VP]),
     "bcad_cu_memset": (I, [VP, I, SZ, VP]),
     "bcad_cu_memcpy_batch": (I, [SZ, VP, VP, VP, I, VP]),
@@ -143,6 +144,10 @@ PROTOS = {
     "bcad_cu_event_destroy": (I, [VP]),
     "bcad_cu_event_record": (I, [VP, VP]),
     "bcad_cu_stream_wait_event": (I, [VP, VP]),
+    "bcad_cu_graph_capture_begin": (I, [VP]),
+    "bcad_cu_graph_capture_end": (I, [VP, C.POINTER(VP)]),
+    "bcad_cu_graph_launch": (I, [VP, VP]),
+    "bcad_cu_graph_destroy": (I, [VP]),
     "bcad_cu_nccl_unique_id": (I, [C.c_char_p]),
     "bcad_cu_comm_init": (I, [C.POINTER(VP), I, C.c_char_p, I]),
     "bcad_cu_comm_destroy": (I, [VP]),

@@ -230,3 +230,42 @@ def test_device_errors_report_output_index(gpu, oracle_lib, name, ins, exc, wher
     assert f"at output index {where}" in str(ge.value)
     # the real body never raises (broadcast_apply uses plain reals)
     gpu.forward(name, ins, want_partials=False)
+
+
+def test_graph_capture_replays_the_step_bit_exact(oracle_lib):
+    """bcad_cu_graph_capture_begin/_end/_launch: K1 -> K2 -> K2f of the bias
+    variant (programmatic-dependent launches, a finisher, stream-ordered
+    workspace) captured once and replayed equals the direct launches bit for
+    bit — the kernels are graph-capturable as the bench's replay needs."""
+    import ctypes as C
+    import torch
+    from paper_1810_08297_b200 import native
+    ins = O.hmlstm_inputs(oracle_lib, 1024, 1024, np.float32, "bias")
+    dins = [torch.from_numpy(a).cuda() for a in ins]
+    shapes = [a.shape for a in ins]
+    k = native.Kernel("hmlstm_update_bias")
+    prim = [torch.empty((1024, 1024), device="cuda")]
+    parts = [torch.empty((1024, 1024), device="cuda") for _ in range(9)]
+    seed = [torch.rand((1024, 1024), device="cuda")]
+    ws = native.new_workspace(k, shapes, torch.float32)
+    adj_direct = [torch.empty(s, device="cuda") for s in shapes]
+    adj_graph = [torch.empty(s, device="cuda") for s in shapes]
+    stream = torch.cuda.Stream()
+    sp = C.c_void_p(stream.cuda_stream)
+
+    def step(adj):
+        native.forward(k, dins, prim, parts, stream=stream)
+        native.pullback(k, shapes, seed, parts, dins, adj, workspace=ws, stream=stream)
+
+    step(adj_direct)
+    torch.cuda.synchronize()
+    native.check(native.LIB.bcad_cu_graph_capture_begin(sp))
+    step(adj_graph)
+    exe = C.c_void_p()
+    native.check(native.LIB.bcad_cu_graph_capture_end(sp, C.byref(exe)))
+    for _ in range(3):
+        native.check(native.LIB.bcad_cu_graph_launch(exe, sp))
+    torch.cuda.synchronize()
+    native.check(native.LIB.bcad_cu_graph_destroy(exe))
+    for a, b in zip(adj_direct, adj_graph):
+        assert torch.equal(a, b)
