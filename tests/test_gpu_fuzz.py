@@ -1,0 +1,73 @@
+"""Randomised parity of the tiled 2-D kernels against the oracle at sizes that
+exercise their machinery: multi-tile ROW / COL / SCALAR reductions (the
+finisher K2f), small-problem and large-problem tilings, odd widths (generic
+rank-N fallback), accumulate flags, outputs without an adjoint, both
+policies. Shapes follow the reference's first-axis broadcasting
+(shape.hpp:13-16): each argument is full, length-1 on the batch axis (COL),
+length-1 on the trailing axis / dropped (ROW) or a scalar."""
+import numpy as np
+import pytest
+
+import oracle as O
+from helpers import GpuRunner, assert_close, assert_grads, tol_for
+
+pytestmark = pytest.mark.gpu
+
+KERNELS = ["mul", "plus", "gate", "sig_tanh", "square_gate", "blend", "fiveway", "prod_diff", "two", "fanout",
+           "curl", "hmlstm_update_bias", "hmlstm_update"]
+
+
+def arg_shape(rng, kind, rows, cols):
+    if kind == "full":
+        return (rows, cols)
+    if kind == "col":
+        return (1, cols)
+    if kind == "row":
+        return (rows,) if rng.integers(0, 2) else (rows, 1)
+    return ()
+
+
+@pytest.fixture(scope="module")
+def gpu():
+    return GpuRunner("cuda")
+
+
+@pytest.mark.parametrize("dtype", [np.float32, np.float64])
+def test_fuzz_tiled_kernels(gpu, oracle_lib, dtype):
+    rng = np.random.default_rng(2024 if dtype == np.float32 else 2025)
+    rtol, atol = tol_for(dtype)
+    widths = [4, 8, 12, 64, 100, 128, 256, 1000, 1024, 2048, 4096, 6]
+    for case in range(64):
+        name = KERNELS[case % len(KERNELS)]
+        n, m = oracle_lib.arity(name)
+        cols = int(rng.choice(widths))
+        rows = int(rng.integers(1, max(2, min(3000, 600_000 // cols))))
+        if name.startswith("hmlstm"):
+            kinds = ["full"] * 4 + (["col"] * 3 if n == 9 else []) + ["row", "row"]
+        else:
+            kinds = [str(rng.choice(["full", "full", "col", "row", "scalar"])) for _ in range(n)]
+            kinds[int(rng.integers(0, n))] = "full"  # keep the output (rows, cols)
+        shapes = [arg_shape(rng, k, rows, cols) for k in kinds]
+        ins = [rng.uniform(-1, 1, s).astype(dtype) for s in shapes]
+        if name.startswith("hmlstm"):
+            for z in (n - 2, n - 1):
+                ins[z] = (rng.uniform(0, 1, shapes[z]) < 0.5).astype(dtype)
+        out_shape = O.broadcast_shape_py(shapes)
+        seeds = [rng.uniform(-1, 1, out_shape).astype(dtype) for _ in range(m)]
+        if m > 1 and case % 3 == 0:
+            seeds[int(rng.integers(0, m))] = None
+        existing = [rng.uniform(-1, 1, s).astype(dtype) if rng.integers(0, 4) == 0 else None for s in shapes]
+        policy = int(rng.integers(0, 2))
+        tag = f"case {case} {name} {shapes} p{policy}"
+        got_p, got_d, got_g = gpu.step(name, ins, seeds=seeds, policy=policy, existing=existing)
+        want_p, want_d = oracle_lib.forward(name, ins)
+        _, want_g, want_a64 = oracle_lib.mixed_step(name, ins, O.CACHE_FORWARD, seeds)
+        for i in range(m):
+            assert_close(got_p[i], want_p[i], rtol, atol, tag + f" primal{i}")
+        if got_d is not None:
+            for k, (g, w) in enumerate(zip(got_d, want_d)):
+                assert_close(g, w, rtol, atol, tag + f" D{k}")
+        # accumulate: the device adds into the existing slot
+        want_g = [w if e is None else (e.astype(np.float64) + w).astype(dtype) for w, e in zip(want_g, existing)]
+        want_a64 = [w if e is None else e.astype(np.float64) + w for w, e in zip(want_a64, existing)]
+        assert_grads(got_g, want_g, want_a64, shapes, out_shape, dtype, tag)
