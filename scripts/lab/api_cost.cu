@@ -54,6 +54,10 @@ int main() {
             cudaMemcpyBatchAsync(d.data(), sr.data(), sz.data(), 7, &at, &idx, 1, &fail, s); }, 200));
         printf(" \"memcpyAsync_7xH2D_1MB_us_total\": %.2f,\n", per_call_us([&] {
             for (int k = 0; k < 7; ++k) cudaMemcpyAsync(d[k], sr[k], 1 << 20, cudaMemcpyHostToDevice, s); }, 200));
+        printf(" \"pointerGetAttributes_us\": %.2f,\n", per_call_us([&] {
+            cudaPointerAttributes at; cudaPointerGetAttributes(&at, sr[3]); }, 5000));
+        printf(" \"streamIsCapturing_us\": %.2f,\n", per_call_us([&] {
+            cudaStreamCaptureStatus st; cudaStreamIsCapturing(s, &st); }, 5000));
         printf(" \"memcpyAsync_H2D_64B_pinned_us\": %.2f,\n", per_call_us([&] {
             cudaMemcpyAsync(d[0], sr[0], 64, cudaMemcpyHostToDevice, s); }, 2000));
     }
