@@ -191,20 +191,24 @@ inline Tiling choose_tiling(const Plan& p, int V, const ClassMix& mix, bool fine
     int txv = 1;
     while (txv < cap && txv < t.vcols) txv <<= 1;
     const int64_t slots = int64_t(kSmCount) * kCtasPerSm;
-    // Small problems with column reductions: 16-lane column tiles and about
-    // two CTAs per SM, which balances the fp64 partials per column (one per
-    // row tile) against those per row (one per column tile) that the last
-    // CTAs combine (measured at config 3: -18% against 32 lanes x 2 rows).
-    const bool small_col = mix.col && !fine && txv == 32 && t.vcols >= 256 &&
+    // Column reductions ((1,H) arguments): at least 4 rows per thread, which
+    // amortises each CTA's shared-memory setup and combine; small problems
+    // also take 16-lane column tiles (64 fp32 columns) and about two CTAs per
+    // SM, balancing the fp64 tile partials per column against those per row.
+    // Measured (lab, bias variant) against the former 32 lanes x 1..6 rows:
+    // B x H = 1024 x 1024 -18%, 4096 x 1024 -14%, 16384 x 1024 -4%; larger
+    // problems keep 32 lanes (half the per-row partials, within 2%).
+    const bool col_small = mix.col && !fine && txv == 32 && t.vcols >= 256 &&
                            ceil_div(p.rows, kThreads / 32) * ceil_div(t.vcols, 32) <= 2 * slots;
-    if (small_col) txv = 16;
+    if (col_small) txv = 16;
     t.txv = txv;
     t.ty = kThreads / txv;
     t.n_col_tiles = ceil_div(t.vcols, txv);
     const int64_t tiles1 = ceil_div(p.rows, t.ty);  // row tiles at rpt = 1
     const int64_t work = tiles1 * t.n_col_tiles;     // CTAs at rpt = 1
-    int64_t rpt = small_col ? ceil_div(work, 2 * kSmCount)
-                            : work <= 2 * slots ? (fine ? 1 : ceil_div(work, slots)) : work / (8 * slots);
+    int64_t rpt = work <= 2 * slots ? (fine ? 1 : ceil_div(work, slots)) : work / (8 * slots);
+    if (col_small) rpt = ceil_div(work, 2 * kSmCount);
+    else if (mix.col && !fine && rpt < 4) rpt = 4;
     if (rpt < 1) rpt = 1;
     if (rpt > 512) rpt = 512;
     // keep the per-tile row partials in shared memory small

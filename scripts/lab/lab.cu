@@ -378,6 +378,14 @@ int main(int argc, char** argv) {
                                                      {256, 2, 1}};
         k2_sweep<KHmlstmBias, float, SigHmlstmBias>("k2_cfg3", true, 1024, 1024, t3);
     }
+    if (which == "k2b") {  // bias pullback tilings at medium and large batch
+        std::vector<std::array<int, 3>> t;
+        for (int txv : {8, 16, 32, 64})
+            for (int rpt : {1, 2, 4, 8, 16, 32, 64}) t.push_back({txv, rpt, 1});
+        k2_sweep<KHmlstmBias, float, SigHmlstmBias>("k2b_4096", true, 4096, 1024, t);
+        k2_sweep<KHmlstmBias, float, SigHmlstmBias>("k2b_16384", true, 16384, 1024, t);
+        k2_sweep<KHmlstmBias, float, SigHmlstmBias>("k2b_8192x4096", true, 8192, 4096, t);
+    }
     if (which == "k1c2time") {  // config-2 K1 alone, repeated (A/B runs)
         Problem<float> P(false, 1024, 1024);
         for (int rep = 0; rep < 5; ++rep) {
