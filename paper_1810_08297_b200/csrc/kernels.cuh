@@ -17,7 +17,8 @@
 //   pull_finish K2f the cross-CTA combination, a programmatically dependent
 //                   launch after K2 (only when a reduction spans CTAs).
 //   fwd_generic / pull_generic   rank-N fallbacks (3+ irreducible axis
-//                   groups, odd widths, misaligned pointers).
+//                   groups; odd widths and unaligned views run fwd2d /
+//                   pull2d at one cell per thread instead).
 #pragma once
 
 #include <cstdint>

@@ -89,6 +89,50 @@ constexpr int fwd_vec_width() {
     else return v;
 }
 
+// The tiled 2-D forward at VV cells per thread (the body's vector width, or
+// 1 for widths / pointers that do not allow vectors).
+template <class Body, class T, int VV, class... Sigs>
+int launch_fwd2d(const FwdArgs& a, std::string* err) {
+    constexpr int N = Body::kIn, M = Body::kOut;
+    const Plan& plan = *a.plan;
+    const bool real = a.partials == nullptr;
+    const Tiling t = a.tiling ? *a.tiling : choose_tiling(plan, VV, ClassMix{}, /*fine=*/true);  // no reductions in K1: wide row tiles
+    bcad_dev::Fwd2DParams<N, M, T> p{};
+    for (int j = 0; j < N; ++j) {
+        p.in[j] = static_cast<const T*>(a.in[j]);
+        p.cls[j] = plan.cls[j];
+    }
+    for (int i = 0; i < M; ++i) {
+        p.primal[i] = a.primal ? static_cast<T*>(a.primal[i]) : nullptr;
+        for (int j = 0; j < N; ++j) p.partials[i * N + j] = a.partials ? static_cast<T*>(a.partials[i * N + j]) : nullptr;
+    }
+    p.rows = plan.rows;
+    p.cols = plan.cols;
+    p.vcols = int(t.vcols);
+    p.txv_shift = __builtin_ctz(unsigned(t.txv));
+    p.ty = t.ty;
+    p.rpt = t.rpt;
+    p.tile_rows = t.tile_rows;
+    p.err = a.err;
+    const dim3 grid(unsigned(t.n_col_tiles), unsigned(t.n_row_tiles));
+    bool dense = true;  // every output pointer present: no per-store checks
+    for (int i = 0; i < M; ++i) {
+        dense = dense && p.primal[i];
+        for (int j = 0; j < N && !real; ++j) dense = dense && p.partials[i * N + j];
+    }
+    return with_sig<Sigs...>(plan, [&](auto sig) {
+        using S = decltype(sig);
+        void (*kern)(bcad_dev::Fwd2DParams<N, M, T>);
+        if constexpr (S::kStatic) {
+            if (dense) kern = real ? &bcad_dev::fwd2d_kernel<Body, T, VV, true, S, true> : &bcad_dev::fwd2d_kernel<Body, T, VV, false, S, true>;
+            else kern = real ? &bcad_dev::fwd2d_kernel<Body, T, VV, true, S, false> : &bcad_dev::fwd2d_kernel<Body, T, VV, false, S, false>;
+        } else {
+            kern = real ? &bcad_dev::fwd2d_kernel<Body, T, VV, true, S, false> : &bcad_dev::fwd2d_kernel<Body, T, VV, false, S, false>;
+        }
+        return cuda_status(launch_pdl(kern, grid, 0, a.stream, p), err);
+    });
+}
+
 template <class Body, class T, class... Sigs>
 int launch_fwd_t(const FwdArgs& a, std::string* err) {
     constexpr int N = Body::kIn, M = Body::kOut, V = fwd_vec_width<Body, T>();
@@ -102,43 +146,10 @@ int launch_fwd_t(const FwdArgs& a, std::string* err) {
         for (int j = 0; j < N && a.partials && vec; ++j)
             if (a.partials[i * N + j] && !aligned16(a.partials[i * N + j])) vec = false;
     }
-    if (vec) {
-        const Tiling t = a.tiling ? *a.tiling : choose_tiling(plan, V, ClassMix{}, /*fine=*/true);  // no reductions in K1: wide row tiles
-        bcad_dev::Fwd2DParams<N, M, T> p{};
-        for (int j = 0; j < N; ++j) {
-            p.in[j] = static_cast<const T*>(a.in[j]);
-            p.cls[j] = plan.cls[j];
-        }
-        for (int i = 0; i < M; ++i) {
-            p.primal[i] = a.primal ? static_cast<T*>(a.primal[i]) : nullptr;
-            for (int j = 0; j < N; ++j) p.partials[i * N + j] = a.partials ? static_cast<T*>(a.partials[i * N + j]) : nullptr;
-        }
-        p.rows = plan.rows;
-        p.cols = plan.cols;
-        p.vcols = int(t.vcols);
-        p.txv_shift = __builtin_ctz(unsigned(t.txv));
-        p.ty = t.ty;
-        p.rpt = t.rpt;
-        p.tile_rows = t.tile_rows;
-        p.err = a.err;
-        const dim3 grid(unsigned(t.n_col_tiles), unsigned(t.n_row_tiles));
-        bool dense = true;  // every output pointer present: no per-store checks
-        for (int i = 0; i < M; ++i) {
-            dense = dense && p.primal[i];
-            for (int j = 0; j < N && !real; ++j) dense = dense && p.partials[i * N + j];
-        }
-        return with_sig<Sigs...>(plan, [&](auto sig) {
-            using S = decltype(sig);
-            void (*kern)(bcad_dev::Fwd2DParams<N, M, T>);
-            if constexpr (S::kStatic) {
-                if (dense) kern = real ? &bcad_dev::fwd2d_kernel<Body, T, V, true, S, true> : &bcad_dev::fwd2d_kernel<Body, T, V, false, S, true>;
-                else kern = real ? &bcad_dev::fwd2d_kernel<Body, T, V, true, S, false> : &bcad_dev::fwd2d_kernel<Body, T, V, false, S, false>;
-            } else {
-                kern = real ? &bcad_dev::fwd2d_kernel<Body, T, V, true, S, false> : &bcad_dev::fwd2d_kernel<Body, T, V, false, S, false>;
-            }
-            return cuda_status(launch_pdl(kern, grid, 0, a.stream, p), err);
-        });
-    }
+    if (vec) return launch_fwd2d<Body, T, V, Sigs...>(a, err);
+    // odd widths / unaligned views of a 2-D problem: the same tiled kernel, one cell per thread
+    if constexpr (V > 1)
+        if (plan.is2d) return launch_fwd2d<Body, T, 1>(a, err);
     bcad_dev::GenParams<N, M, T> g{};
     fill_generic(g, plan);
     for (int j = 0; j < N; ++j) g.in[j] = static_cast<const T*>(a.in[j]);
@@ -154,6 +165,80 @@ int launch_fwd_t(const FwdArgs& a, std::string* err) {
 }
 
 // --------------------------------------------------------------- pullback
+// The tiled 2-D pullback at VV cells per thread (VV = the 128-bit width, or
+// 1 for widths / pointers that do not allow vectors) with signature
+// dispatch over Sigs (none: runtime classes only).
+template <class Body, class T, int VV, class... Sigs>
+int launch_pull2d(const PullArgs& a, std::string* err) {
+    constexpr int N = Body::kIn, M = Body::kOut;
+    const Plan& plan = *a.plan;
+    const bool recompute = a.partials == nullptr;
+    const Tiling t = a.tiling ? *a.tiling : choose_tiling(plan, VV, class_mix(plan));
+    const PullLayout L = pull_layout(plan, t);  // offsets sized for every argument
+    if (a.ws_bytes < L.total || (L.total > 0 && !a.workspace)) {
+        *err = "pullback workspace too small: need " + std::to_string(L.total) + " bytes";
+        return BCAD_CU_ERR_CONFIG;
+    }
+    bcad_dev::Pull2DParams<N, M, T> p{};
+    int nr = 0, nc = 0, ns = 0;
+    for (int j = 0; j < N; ++j) {
+        p.in[j] = a.in ? static_cast<const T*>(a.in[j]) : nullptr;
+        p.adj[j] = static_cast<T*>(a.in_adj[j]);
+        p.cls[j] = plan.cls[j];
+        p.slot[j] = -1;
+        if (a.accumulate && a.accumulate[j]) p.acc_mask |= 1u << j;
+        if (!p.adj[j]) continue;
+        if (plan.cls[j] == kRow) { p.row_j[nr] = j; p.slot[j] = nr++; }
+        if (plan.cls[j] == kCol) { p.col_j[nc] = j; p.slot[j] = nc++; }
+        if (plan.cls[j] == kScalar) { p.scal_j[ns] = j; p.slot[j] = ns++; }
+    }
+    for (int i = 0; i < M; ++i) {
+        p.w[i] = static_cast<const T*>(a.out_adj[i]);
+        for (int j = 0; j < N; ++j) p.D[i * N + j] = recompute ? nullptr : static_cast<const T*>(a.partials[i * N + j]);
+    }
+    p.rows = plan.rows;
+    p.cols = plan.cols;
+    p.vcols = int(t.vcols);
+    p.txv_shift = __builtin_ctz(unsigned(t.txv));
+    p.ty = t.ty;
+    p.rpt = t.rpt;
+    p.tile_rows = t.tile_rows;
+    p.n_col_tiles = int(t.n_col_tiles);
+    p.n_row_tiles = int(t.n_row_tiles);
+    p.n_row_args = nr;
+    p.n_col_args = nc;
+    p.n_scalar_args = ns;
+    char* ws = static_cast<char*>(a.workspace);
+    p.ws_row = reinterpret_cast<double*>(ws + L.ws_row);
+    p.ws_col = reinterpret_cast<double*>(ws + L.ws_col);
+    p.ws_scalar = reinterpret_cast<double*>(ws + L.ws_scalar);
+    p.err = a.err;
+    const int64_t fin_blocks = bcad_dev::pull_finish_blocks(plan.rows, plan.cols, p.n_row_tiles, p.n_col_tiles, nr, nc, ns);
+    const size_t smem = pull_smem_bytes(nc, nr, ns, t);
+    const dim3 grid(unsigned(t.n_col_tiles), unsigned(t.n_row_tiles));
+    bool dense = p.acc_mask == 0;  // every w and adjoint present, nothing accumulated
+    for (int i = 0; i < M; ++i) dense = dense && p.w[i];
+    for (int j = 0; j < N; ++j) dense = dense && p.adj[j];
+    return with_sig<Sigs...>(plan, [&](auto sig) {
+        using S = decltype(sig);
+        void (*kern)(bcad_dev::Pull2DParams<N, M, T>);
+        if constexpr (S::kStatic) {
+            if (dense) kern = recompute ? &bcad_dev::pull2d_kernel<Body, T, VV, true, S, true> : &bcad_dev::pull2d_kernel<Body, T, VV, false, S, true>;
+            else kern = recompute ? &bcad_dev::pull2d_kernel<Body, T, VV, true, S, false> : &bcad_dev::pull2d_kernel<Body, T, VV, false, S, false>;
+        } else {
+            kern = recompute ? &bcad_dev::pull2d_kernel<Body, T, VV, true, S, false> : &bcad_dev::pull2d_kernel<Body, T, VV, false, S, false>;
+        }
+        if (smem > 48 * 1024) {
+            const cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+            if (e != cudaSuccess) return cuda_status(e, err);
+        }
+        int rc = cuda_status(launch_pdl(kern, grid, smem, a.stream, p), err);
+        if (rc || fin_blocks == 0) return rc;
+        return cuda_status(launch_pdl(&bcad_dev::pull_finish_kernel<N, M, T>, dim3(unsigned(fin_blocks)), 0,
+                                      a.stream, p), err);
+    });
+}
+
 template <class Body, class T, class... Sigs>
 int launch_pull_t(const PullArgs& a, std::string* err) {
     constexpr int N = Body::kIn, M = Body::kOut, V = vec_width<T>();
@@ -170,73 +255,12 @@ int launch_pull_t(const PullArgs& a, std::string* err) {
     }
     for (int j = 0; j < N && recompute && vec; ++j)
         if ((plan.cls[j] == kFull || plan.cls[j] == kCol) && !aligned16(a.in[j])) vec = false;
-
-    if (vec) {
-        const Tiling t = a.tiling ? *a.tiling : choose_tiling(plan, V, class_mix(plan));
-        const PullLayout L = pull_layout(plan, t);  // offsets sized for every argument
-        if (a.ws_bytes < L.total || (L.total > 0 && !a.workspace)) {
-            *err = "pullback workspace too small: need " + std::to_string(L.total) + " bytes";
-            return BCAD_CU_ERR_CONFIG;
-        }
-        bcad_dev::Pull2DParams<N, M, T> p{};
-        int nr = 0, nc = 0, ns = 0;
-        for (int j = 0; j < N; ++j) {
-            p.in[j] = a.in ? static_cast<const T*>(a.in[j]) : nullptr;
-            p.adj[j] = static_cast<T*>(a.in_adj[j]);
-            p.cls[j] = plan.cls[j];
-            p.slot[j] = -1;
-            if (a.accumulate && a.accumulate[j]) p.acc_mask |= 1u << j;
-            if (!p.adj[j]) continue;
-            if (plan.cls[j] == kRow) { p.row_j[nr] = j; p.slot[j] = nr++; }
-            if (plan.cls[j] == kCol) { p.col_j[nc] = j; p.slot[j] = nc++; }
-            if (plan.cls[j] == kScalar) { p.scal_j[ns] = j; p.slot[j] = ns++; }
-        }
-        for (int i = 0; i < M; ++i) {
-            p.w[i] = static_cast<const T*>(a.out_adj[i]);
-            for (int j = 0; j < N; ++j) p.D[i * N + j] = recompute ? nullptr : static_cast<const T*>(a.partials[i * N + j]);
-        }
-        p.rows = plan.rows;
-        p.cols = plan.cols;
-        p.vcols = int(t.vcols);
-        p.txv_shift = __builtin_ctz(unsigned(t.txv));
-        p.ty = t.ty;
-        p.rpt = t.rpt;
-        p.tile_rows = t.tile_rows;
-        p.n_col_tiles = int(t.n_col_tiles);
-        p.n_row_tiles = int(t.n_row_tiles);
-        p.n_row_args = nr;
-        p.n_col_args = nc;
-        p.n_scalar_args = ns;
-        char* ws = static_cast<char*>(a.workspace);
-        p.ws_row = reinterpret_cast<double*>(ws + L.ws_row);
-        p.ws_col = reinterpret_cast<double*>(ws + L.ws_col);
-        p.ws_scalar = reinterpret_cast<double*>(ws + L.ws_scalar);
-        p.err = a.err;
-        const int64_t fin_blocks = bcad_dev::pull_finish_blocks(plan.rows, plan.cols, p.n_row_tiles, p.n_col_tiles, nr, nc, ns);
-        const size_t smem = pull_smem_bytes(nc, nr, ns, t);
-        const dim3 grid(unsigned(t.n_col_tiles), unsigned(t.n_row_tiles));
-        bool dense = p.acc_mask == 0;  // every w and adjoint present, nothing accumulated
-        for (int i = 0; i < M; ++i) dense = dense && p.w[i];
-        for (int j = 0; j < N; ++j) dense = dense && p.adj[j];
-        return with_sig<Sigs...>(plan, [&](auto sig) {
-            using S = decltype(sig);
-            void (*kern)(bcad_dev::Pull2DParams<N, M, T>);
-            if constexpr (S::kStatic) {
-                if (dense) kern = recompute ? &bcad_dev::pull2d_kernel<Body, T, V, true, S, true> : &bcad_dev::pull2d_kernel<Body, T, V, false, S, true>;
-                else kern = recompute ? &bcad_dev::pull2d_kernel<Body, T, V, true, S, false> : &bcad_dev::pull2d_kernel<Body, T, V, false, S, false>;
-            } else {
-                kern = recompute ? &bcad_dev::pull2d_kernel<Body, T, V, true, S, false> : &bcad_dev::pull2d_kernel<Body, T, V, false, S, false>;
-            }
-            if (smem > 48 * 1024) {
-                const cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-                if (e != cudaSuccess) return cuda_status(e, err);
-            }
-            int rc = cuda_status(launch_pdl(kern, grid, smem, a.stream, p), err);
-            if (rc || fin_blocks == 0) return rc;
-            return cuda_status(launch_pdl(&bcad_dev::pull_finish_kernel<N, M, T>, dim3(unsigned(fin_blocks)), 0,
-                                          a.stream, p), err);
-        });
-    }
+    if (vec) return launch_pull2d<Body, T, V, Sigs...>(a, err);
+    // odd widths / unaligned views of a 2-D problem: the same tiled kernel, one
+    // cell per thread (when the caller's workspace fits that layout)
+    if (pull_scalar2d_ok<T>(plan) &&
+        a.ws_bytes >= pull_layout(plan, choose_tiling(plan, 1, class_mix(plan))).total)
+        return launch_pull2d<Body, T, 1>(a, err);
     bcad_dev::GenParams<N, M, T> g{};
     fill_generic(g, plan);
     int64_t off = 0;

@@ -11,6 +11,7 @@
 // or more irreducible axis groups uses the generic rank-N kernels.
 #pragma once
 
+#include <algorithm>
 #include <cstdint>
 #include <cstring>
 #include <string>
@@ -271,11 +272,23 @@ bool pull_vec_shape_ok(const Plan& plan) {
     return pull_layout(plan, choose_tiling(plan, V, class_mix(plan))).smem <= kMaxPullSmem;
 }
 
+// The tiled pullback at one cell per thread (odd widths, unaligned views).
+template <class T>
+bool pull_scalar2d_ok(const Plan& plan) {
+    return plan.is2d && pull_layout(plan, choose_tiling(plan, 1, class_mix(plan))).smem <= kMaxPullSmem;
+}
+
+// Workspace of the tiled variant the width selects: vectors when the width
+// allows them, else one cell per thread. (A vector-width problem handed
+// unaligned views at launch uses the one-cell variant only if this
+// workspace also fits its layout, else the generic kernel.)
 template <class T>
 size_t pull_ws_t(const Plan& plan) {
     constexpr int V = vec_width<T>();
-    if (!pull_vec_shape_ok<T>(plan)) return 256;
-    return pull_layout(plan, choose_tiling(plan, V, class_mix(plan))).total;
+    size_t ws = 256;
+    if (pull_vec_shape_ok<T>(plan)) ws = std::max(ws, pull_layout(plan, choose_tiling(plan, V, class_mix(plan))).total);
+    else if (pull_scalar2d_ok<T>(plan)) ws = std::max(ws, pull_layout(plan, choose_tiling(plan, 1, class_mix(plan))).total);
+    return ws;
 }
 
 }  // namespace bcad_cu_impl

@@ -76,8 +76,11 @@ def test_workspace_sizing_is_host_only():
     small = native.pullback_workspace(kb, [(32, 256)] * 4 + [(1, 256)] * 3 + [(32,)] * 2, native.F32)
     big = native.pullback_workspace(kb, [(65536, 4096)] * 4 + [(1, 4096)] * 3 + [(65536,)] * 2, native.F32)
     assert 0 < small < big < 64 << 20  # fp64 tile partials stay < 0.3% of the step's bytes
-    # odd widths take the generic path (no tile workspace)
-    assert native.pullback_workspace(kb, [(7, 1023)] * 4 + [(1, 1023)] * 3 + [(7,)] * 2, native.F32) == 256
+    # odd widths run the one-cell-per-thread tiled kernel: its (small) tile workspace
+    odd = native.pullback_workspace(kb, [(7, 1023)] * 4 + [(1, 1023)] * 3 + [(7,)] * 2, native.F32)
+    assert 256 <= odd < 1 << 20
+    # three irreducible axis groups: the generic kernel, no tile workspace
+    assert native.pullback_workspace(kb, [(4, 3, 8)] * 4 + [(1, 3, 8)] * 3 + [(4, 1, 8)] * 2, native.F32) == 256
 
 
 def test_status_codes_match_reference_errors():

@@ -187,7 +187,9 @@ def test_edge_shapes(gpu, oracle_lib, dtype, shape):
         assert_grads(got_g, want_g, want_a64, [a.shape for a in ins], (B, H), dtype, f"{shape}")
 
 
-def test_misaligned_views_take_generic_path(gpu, oracle_lib):
+def test_misaligned_views_take_scalar_tiled_path(gpu, oracle_lib):
+    """4-byte-aligned views of a 2-D problem: the tiled kernels at one cell
+    per thread (no 128-bit vectors) — forward and pullback, both policies."""
     import torch
     from paper_1810_08297_b200 import native
     rng = np.random.default_rng(9)
@@ -206,6 +208,21 @@ def test_misaligned_views_take_generic_path(gpu, oracle_lib):
     native.forward(k, dins, prim, None)
     want, _ = oracle_lib.forward("hmlstm_update", ins, real_body=True)
     assert_close(prim[0].cpu().numpy(), want[0], 1e-5, 1e-6, "misaligned primal")
+    # the full step on misaligned buffers: partials, seeds and adjoints offset too
+    def off_view(shape):
+        n = int(np.prod(shape))
+        return torch.empty(n + 1, dtype=torch.float32, device="cuda")[1:].view(shape)
+    parts = [off_view((B, H)) for _ in range(6)]
+    native.forward(k, dins, prim, parts)
+    seed = off_view((B, H))
+    seed.copy_(torch.from_numpy(rng.uniform(-1, 1, (B, H)).astype(np.float32)).cuda())
+    shapes = [a.shape for a in ins]
+    _, want_g, want_a64 = oracle_lib.mixed_step("hmlstm_update", ins, O.CACHE_FORWARD, [seed.cpu().numpy()])
+    for policy_parts in (parts, None):
+        adj = [off_view(s) for s in shapes]
+        native.pullback(k, shapes, [seed], policy_parts, dins, adj, workspace=native.new_workspace(k, shapes, torch.float32))
+        torch.cuda.synchronize()
+        assert_grads([a.cpu().numpy() for a in adj], want_g, want_a64, shapes, (B, H), np.float32, "misaligned grads")
 
 
 ERROR_CASES = [
