@@ -731,15 +731,21 @@ __global__ void __launch_bounds__(kThreads) fwd_generic_kernel(const __grid_cons
     }
 }
 
-// One thread per element e of each input j: walks the output cells that map
-// onto e (the broadcast axes of j, row-major) and sums the terms.
-template <class Body, class T, bool kRecompute>
+// Generic pullback. kWarp = false: one thread per element e of each input j
+// walks the output cells that map onto e (the broadcast axes of j,
+// row-major) and sums the terms. kWarp = true (arguments reduced over >= 32
+// cells): one warp per element, lanes take every 32nd cell, fixed-order
+// butterfly — the same fp64 sum of the same rounded terms, in parallel.
+template <class Body, class T, bool kRecompute, bool kWarp>
 __global__ void __launch_bounds__(kThreads) pull_generic_kernel(const __grid_constant__ GenParams<Body::kIn, Body::kOut, T> p) {
     constexpr int N = Body::kIn, M = Body::kOut;
     if constexpr (Body::kMayRaise && kRecompute) s_err_flag[threadIdx.x] = 0;
     const int64_t total = p.adj_offset[N];
-    for (int64_t g = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; g < total;
-         g += int64_t(gridDim.x) * blockDim.x) {
+    const int lane = threadIdx.x & 31;
+    const int64_t first = kWarp ? (blockIdx.x * int64_t(blockDim.x) + threadIdx.x) / 32
+                                : blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+    const int64_t step = kWarp ? int64_t(gridDim.x) * blockDim.x / 32 : int64_t(gridDim.x) * blockDim.x;
+    for (int64_t g = first; g < total; g += step) {
         int j = 0;
         while (j + 1 < N && g >= p.adj_offset[j + 1]) ++j;
         const int64_t e = g - p.adj_offset[j];
@@ -764,23 +770,15 @@ __global__ void __launch_bounds__(kThreads) pull_generic_kernel(const __grid_con
                     cnt *= p.out_dims[k];
                 }
         }
-        const bool acc = (p.acc_mask >> j) & 1u;
-        T exact = acc ? p.adj[j][e] : T(0);
-        double sum = 0.0;
-        int64_t coord[kMaxRank];
-        for (int k = 0; k < p.out_rank; ++k) coord[k] = base[k];
-        for (int64_t q = 0; q < cnt; ++q) {
-            int64_t flat = 0;
-            for (int k = 0; k < p.out_rank; ++k) flat = flat * p.out_dims[k] + coord[k];
+        // sum over outputs of the rounded terms w_i * D_ij at output cell `flat`
+        auto cell_terms = [&](int64_t flat, T* exact_out) -> double {
             T dj[M];
             if constexpr (kRecompute) {
                 int64_t off[N];
                 decode_offsets<N, M, T>(p, flat, off);
                 Dual<T, N> xi[N], yo[M];
 #pragma unroll
-                for (int jj = 0; jj < N; ++jj) {
-                    xi[jj] = Dual<T, N>::seeded(p.in[jj][off[jj]], jj);
-                }
+                for (int jj = 0; jj < N; ++jj) xi[jj] = Dual<T, N>::seeded(p.in[jj][off[jj]], jj);
                 Body::template body<Dual<T, N>>(xi, yo);
                 if constexpr (Body::kMayRaise) report_error(p.err, flat);
 #pragma unroll
@@ -795,22 +793,52 @@ __global__ void __launch_bounds__(kThreads) pull_generic_kernel(const __grid_con
 #pragma unroll
                 for (int i = 0; i < M; ++i) dj[i] = p.w[i] ? p.D[i * N + j][flat] : T(0);
             }
+            double sum = 0.0;
 #pragma unroll
             for (int i = 0; i < M; ++i) {
                 if (!p.w[i]) continue;
                 const T term = p.w[i][flat] * dj[i];
-                if (cnt == 1) exact = exact + term;
+                if (exact_out) *exact_out = *exact_out + term;
                 else sum += double(term);
             }
-            // odometer over the broadcast axes, last axis fastest
-            for (int b = nb - 1; b >= 0; --b) {
-                const int k = bax[b];
-                if (++coord[k] < p.out_dims[k]) break;
-                coord[k] = 0;
+            return sum;
+        };
+        const bool acc = (p.acc_mask >> j) & 1u;
+        int64_t coord[kMaxRank];
+        for (int k = 0; k < p.out_rank; ++k) coord[k] = base[k];
+        if constexpr (kWarp) {
+            double sum = 0.0;
+            for (int64_t q = lane; q < cnt; q += 32) {
+                int64_t rem = q;  // q -> coordinates on the broadcast axes, last fastest
+                for (int b2 = nb - 1; b2 >= 0; --b2) {
+                    const int k = bax[b2];
+                    coord[k] = rem % p.out_dims[k];
+                    rem /= p.out_dims[k];
+                }
+                int64_t flat = 0;
+                for (int k = 0; k < p.out_rank; ++k) flat = flat * p.out_dims[k] + coord[k];
+                sum += cell_terms(flat, nullptr);
             }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+            if (lane == 0) p.adj[j][e] = acc ? T(double(p.adj[j][e]) + sum) : T(sum);
+        } else {
+            T exact = acc ? p.adj[j][e] : T(0);
+            double sum = 0.0;
+            for (int64_t q = 0; q < cnt; ++q) {
+                int64_t flat = 0;
+                for (int k = 0; k < p.out_rank; ++k) flat = flat * p.out_dims[k] + coord[k];
+                sum += cell_terms(flat, cnt == 1 ? &exact : nullptr);
+                // odometer over the broadcast axes, last axis fastest
+                for (int b2 = nb - 1; b2 >= 0; --b2) {
+                    const int k = bax[b2];
+                    if (++coord[k] < p.out_dims[k]) break;
+                    coord[k] = 0;
+                }
+            }
+            if (cnt == 1) p.adj[j][e] = exact;
+            else p.adj[j][e] = acc ? T(double(p.adj[j][e]) + sum) : T(sum);
         }
-        if (cnt == 1) p.adj[j][e] = exact;
-        else p.adj[j][e] = acc ? T(double(p.adj[j][e]) + sum) : T(sum);
     }
 }
 

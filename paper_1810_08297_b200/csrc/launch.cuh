@@ -261,27 +261,44 @@ int launch_pull_t(const PullArgs& a, std::string* err) {
     if (pull_scalar2d_ok<T>(plan) &&
         a.ws_bytes >= pull_layout(plan, choose_tiling(plan, 1, class_mix(plan))).total)
         return launch_pull2d<Body, T, 1>(a, err);
+    // generic rank-N pullback: thread per element, or warp per element for
+    // arguments reduced over >= 32 output cells
     bcad_dev::GenParams<N, M, T> g{};
     fill_generic(g, plan);
-    int64_t off = 0;
-    for (int j = 0; j < N; ++j) {
-        g.in[j] = a.in ? static_cast<const T*>(a.in[j]) : nullptr;
-        g.adj[j] = static_cast<T*>(a.in_adj[j]);
+    for (int j = 0; j < N; ++j) g.in[j] = a.in ? static_cast<const T*>(a.in[j]) : nullptr;
+    for (int j = 0; j < N; ++j)
         if (a.accumulate && a.accumulate[j]) g.acc_mask |= 1u << j;
-        g.adj_offset[j] = off;
-        if (g.adj[j]) off += plan.arg_vol[j];
-    }
-    g.adj_offset[N] = off;
     for (int i = 0; i < M; ++i) {
         g.w[i] = static_cast<const T*>(a.out_adj[i]);
         for (int j = 0; j < N; ++j) g.D[i * N + j] = recompute ? nullptr : static_cast<const T*>(a.partials[i * N + j]);
     }
     g.err = a.err;
-    if (off == 0) return BCAD_CU_OK;
-    const int grid = generic_grid(off);
-    if (recompute) bcad_dev::pull_generic_kernel<Body, T, true><<<grid, kThreads, 0, a.stream>>>(g);
-    else bcad_dev::pull_generic_kernel<Body, T, false><<<grid, kThreads, 0, a.stream>>>(g);
-    return cuda_status(cudaGetLastError(), err);
+    bcad_dev::GenParams<N, M, T> gw = g;
+    int64_t off = 0, offw = 0;
+    for (int j = 0; j < N; ++j) {
+        const bool wide = a.in_adj[j] && plan.vol / (plan.arg_vol[j] > 0 ? plan.arg_vol[j] : 1) >= 32;
+        g.adj[j] = wide ? nullptr : static_cast<T*>(a.in_adj[j]);
+        gw.adj[j] = wide ? static_cast<T*>(a.in_adj[j]) : nullptr;
+        g.adj_offset[j] = off;
+        gw.adj_offset[j] = offw;
+        if (g.adj[j]) off += plan.arg_vol[j];
+        if (gw.adj[j]) offw += plan.arg_vol[j];
+    }
+    g.adj_offset[N] = off;
+    gw.adj_offset[N] = offw;
+    if (off > 0) {
+        const int grid = generic_grid(off);
+        if (recompute) bcad_dev::pull_generic_kernel<Body, T, true, false><<<grid, kThreads, 0, a.stream>>>(g);
+        else bcad_dev::pull_generic_kernel<Body, T, false, false><<<grid, kThreads, 0, a.stream>>>(g);
+        if (const int rc = cuda_status(cudaGetLastError(), err)) return rc;
+    }
+    if (offw > 0) {
+        const int grid = generic_grid(offw * 32);
+        if (recompute) bcad_dev::pull_generic_kernel<Body, T, true, true><<<grid, kThreads, 0, a.stream>>>(gw);
+        else bcad_dev::pull_generic_kernel<Body, T, false, true><<<grid, kThreads, 0, a.stream>>>(gw);
+        if (const int rc = cuda_status(cudaGetLastError(), err)) return rc;
+    }
+    return BCAD_CU_OK;
 }
 
 template <class Body, class... Sigs>

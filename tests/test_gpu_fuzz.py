@@ -71,3 +71,35 @@ def test_fuzz_tiled_kernels(gpu, oracle_lib, dtype):
         want_g = [w if e is None else (e.astype(np.float64) + w).astype(dtype) for w, e in zip(want_g, existing)]
         want_a64 = [w if e is None else e.astype(np.float64) + w for w, e in zip(want_a64, existing)]
         assert_grads(got_g, want_g, want_a64, shapes, out_shape, dtype, tag)
+
+
+@pytest.mark.parametrize("dtype", [np.float32, np.float64])
+def test_fuzz_generic_rank3(gpu, oracle_lib, dtype):
+    """Shapes with three irreducible axis groups run the generic rank-N
+    kernels; arguments reduced over >= 32 output cells take the
+    warp-per-element pullback. Both policies, accumulate flags."""
+    rng = np.random.default_rng(77 if dtype == np.float32 else 78)
+    rtol, atol = tol_for(dtype)
+    kinds3 = [lambda B, T, C: (B, T, C), lambda B, T, C: (1, T, C), lambda B, T, C: (B, 1, C),
+              lambda B, T, C: (B, T), lambda B, T, C: ()]
+    for case in range(24):
+        name = ["mul", "gate", "blend", "prod_diff", "two", "fiveway", "curl", "fanout"][case % 8]
+        n, m = oracle_lib.arity(name)
+        B, T, C = int(rng.integers(33, 200)), int(rng.integers(2, 40)), int(rng.integers(1, 9))
+        picks = [0] + [int(rng.integers(0, len(kinds3))) for _ in range(n - 1)]
+        rng.shuffle(picks)
+        shapes = [kinds3[k](B, T, C) for k in picks]
+        ins = [rng.uniform(-1, 1, s).astype(dtype) for s in shapes]
+        out_shape = O.broadcast_shape_py(shapes)
+        seeds = [rng.uniform(-1, 1, out_shape).astype(dtype) for _ in range(m)]
+        existing = [rng.uniform(-1, 1, s).astype(dtype) if rng.integers(0, 4) == 0 else None for s in shapes]
+        policy = int(rng.integers(0, 2))
+        tag = f"rank3 case {case} {name} {shapes} p{policy}"
+        got_p, got_d, got_g = gpu.step(name, ins, seeds=seeds, policy=policy, existing=existing)
+        want_p, want_d = oracle_lib.forward(name, ins)
+        _, want_g, want_a64 = oracle_lib.mixed_step(name, ins, O.CACHE_FORWARD, seeds)
+        for i in range(m):
+            assert_close(got_p[i], want_p[i], rtol, atol, tag + f" primal{i}")
+        want_g = [w if e is None else (e.astype(np.float64) + w).astype(dtype) for w, e in zip(want_g, existing)]
+        want_a64 = [w if e is None else e.astype(np.float64) + w for w, e in zip(want_a64, existing)]
+        assert_grads(got_g, want_g, want_a64, shapes, out_shape, dtype, tag)
