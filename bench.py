@@ -246,10 +246,9 @@ class Case:
             else:
                 self.adj.append(torch.empty(s, device=device, dtype=dt))
         self.ws = native.new_workspace(self.k, shapes, dt, device)
-        # K1 + K2, plus the finisher K2f when a reduction spans CTAs (its
-        # tile partials are what the workspace holds)
+        # K1 + K2, plus the finisher K2f when a reduction spans CTAs
         code = native.F32 if dt == torch.float32 else native.F64
-        self.launches = 3 if native.pullback_workspace(self.k, shapes, code) > 0 else 2
+        self.launches = 1 + native.pullback_launches(self.k, shapes, code)
         self.step = native.PreparedStep(self.k, ins, self.primal, self.partials, [self.seed], self.adj, self.ws,
                                         policy=policy)
 

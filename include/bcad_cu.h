@@ -120,6 +120,11 @@ int bcad_cu_forward(bcad_cu_kernel k, int dtype, int n_in, const void* const* in
 int bcad_cu_pullback_workspace(bcad_cu_kernel k, int dtype, int n_in, const bcad_cu_shape* in_shapes,
                                int m_out, size_t* bytes);
 
+/* Device kernel launches one bcad_cu_pullback of this problem issues with
+ * aligned pointers (1: K2; 2: K2 and its finisher K2f; 0: generic path). */
+int bcad_cu_pullback_launches(bcad_cu_kernel k, int dtype, int n_in, const bcad_cu_shape* in_shapes, int m_out,
+                              int* launches);
+
 /* Pullback of one mixed node: for every input j with in_adj[j] != NULL,
  *   in_adj[j] (=|+=) sum over outputs i with out_adj[i] != NULL of
  *                    (out_adj[i] (.) D_ij) sum-reduced over the axes input j

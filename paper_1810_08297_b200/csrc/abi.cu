@@ -346,6 +346,18 @@ int bcad_cu_pullback_workspace(bcad_cu_kernel k, int dtype, int n_in, const bcad
     return BCAD_CU_OK;
 }
 
+int bcad_cu_pullback_launches(bcad_cu_kernel k, int dtype, int n_in, const bcad_cu_shape* in_shapes, int m_out,
+                              int* launches) {
+    int rc = arity_check(k, n_in, m_out);
+    if (rc) return rc;
+    if ((rc = dtype_check(dtype))) return rc;
+    Plan plan;
+    std::string err;
+    if ((rc = make_plan(n_in, in_shapes, &plan, &err))) return fail(rc, err);
+    *launches = dtype == BCAD_CU_F32 ? pull_launches_t<float>(plan) : pull_launches_t<double>(plan);
+    return BCAD_CU_OK;
+}
+
 int bcad_cu_pullback(bcad_cu_kernel k, int dtype, int n_in, const bcad_cu_shape* in_shapes, int m_out,
                      const void* const* out_adj, const void* const* partials, const void* const* in,
                      void* const* in_adj, const unsigned char* accumulate, void* workspace, size_t workspace_bytes,

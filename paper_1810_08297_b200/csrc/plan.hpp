@@ -291,4 +291,25 @@ size_t pull_ws_t(const Plan& plan) {
     return ws;
 }
 
+// Kernel launches of one pullback on the tiled path with aligned pointers:
+// K2, plus the finisher K2f when a reduction spans CTAs (mirrors
+// bcad_dev::pull_finish_blocks). 0 when the problem takes the generic path.
+template <class T>
+int pull_launches_t(const Plan& plan) {
+    int V = vec_width<T>();
+    if (!pull_vec_shape_ok<T>(plan)) {
+        if (!pull_scalar2d_ok<T>(plan)) return 0;
+        V = 1;
+    }
+    const Tiling t = choose_tiling(plan, V, class_mix(plan));
+    int nr = 0, nc = 0, ns = 0;
+    for (int j = 0; j < plan.n; ++j) {
+        nr += plan.cls[j] == kRow;
+        nc += plan.cls[j] == kCol;
+        ns += plan.cls[j] == kScalar;
+    }
+    const bool fin = (t.n_col_tiles > 1 && nr > 0) || (t.n_row_tiles > 1 && nc > 0) || (t.n_ctas > 1 && ns > 0);
+    return fin ? 2 : 1;
+}
+
 }  // namespace bcad_cu_impl

@@ -122,6 +122,7 @@ PROTOS = {
     "bcad_cu_broadcast_shape": (I, [I, VP, VP]),
     "bcad_cu_forward": (I, [VP, I, I, VP, VP, I, VP, VP, VP]),
     "bcad_cu_pullback_workspace": (I, [VP, I, I, VP, I, C.POINTER(SZ)]),
+    "bcad_cu_pullback_launches": (I, [VP, I, I, VP, I, C.POINTER(I)]),
     "bcad_cu_pullback": (I, [VP, I, I, VP, I, VP, VP, VP, VP, VP, VP, SZ, VP]),
     "bcad_cu_scatter_add": (I, [I, VP, VP, VP, VP, I, VP]),
     "bcad_cu_fill": (I, [I, VP, I64, C.c_double, VP]),
@@ -292,6 +293,14 @@ def scatter_add(acc, contrib, zero_first=False, stream=None):
 
 def fill(t, value: float, stream=None):
     check(LIB.bcad_cu_fill(_dtype_code(t), _dptr(t), t.numel(), float(value), _stream_ptr(stream)))
+
+
+def pullback_launches(kernel: Kernel, shapes, dtype_code: int) -> int:
+    """Kernel launches of one pullback (1: K2, 2: K2 + finisher K2f)."""
+    n = C.c_int()
+    check(LIB.bcad_cu_pullback_launches(kernel.handle, dtype_code, len(shapes), _shape_array(shapes), kernel.m_out,
+                                        C.byref(n)))
+    return int(n.value)
 
 
 def new_workspace(kernel: Kernel, shapes, dtype, device="cuda"):

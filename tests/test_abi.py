@@ -110,3 +110,13 @@ def test_no_cpu_fallback_without_device():
     rc = native.LIB.bcad_cu_forward(k.handle, native.F64, 2, ptrs, shapes, 1, outs, None, None)
     assert rc == native.CudaError.code
     del np
+
+
+def test_pullback_launch_count():
+    from paper_1810_08297_b200 import native
+    k = native.Kernel("hmlstm_update")
+    kb = native.Kernel("hmlstm_update_bias")
+    # config 2: (B)-reductions finish inside a CTA (one K2 launch)
+    assert native.pullback_launches(k, [(1024, 1024)] * 4 + [(1024,)] * 2, native.F32) == 1
+    # (1,H) reductions over 1024 rows span CTAs: K2 + the finisher K2f
+    assert native.pullback_launches(kb, [(1024, 1024)] * 4 + [(1, 1024)] * 3 + [(1024,)] * 2, native.F32) == 2
