@@ -1,5 +1,6 @@
-"""Full-size parity through size-independent properties (BASELINE configs 4
-and 5 on one GPU), plus oracle checks on sampled rows. Rows are independent
+"""Full-size parity through size-independent properties (every BASELINE
+config at its full size on one GPU: 2, 3, 4, 4-divergence, 5), plus oracle
+checks on sampled rows. Rows are independent
 for every full-shape and per-row quantity, so a row sample of the big
 problem is checked exactly like a small problem; the (1,H) reductions over
 all 65536 rows are checked against an fp64 sum of the device's own rounded
@@ -24,7 +25,7 @@ def device_inputs(torch, B, H, dt, variant, seed):
     return ins
 
 
-@pytest.mark.parametrize("cfg", ["cfg5", "cfg4div"])
+@pytest.mark.parametrize("cfg", ["cfg2", "cfg3", "cfg4", "cfg4div", "cfg5"])
 def test_full_size_properties(oracle_lib, cfg):
     import torch
     from paper_1810_08297_b200 import native
