@@ -426,8 +426,10 @@ def run_native(args, w: Workload, rank: int, world: int):
                      "peak_source": peak_src},
         "e2e": {"value": e2e_value, "unit": "grad elements/s", "h2d_bytes_per_step": e2e["h2d"],
                 "d2h_bytes_per_step": e2e["d2h"], "ms_per_step": e2e["ms_per_step"],
-                "schedule": "row-chunk pipelined host step (bcad_host_set_pipeline auto)",
-                "one_shot_ms_per_step": e2e["one_shot_ms_per_step"], "pcie": e2e["pcie"]},
+                "schedule": "row-chunk pipelined host step (bcad_host_set_pipeline auto), prepared: device buffers kept "
+                            "across calls on the same pinned buffers (bcad_host_set_prepared)",
+                "one_shot_ms_per_step": e2e["one_shot_ms_per_step"],
+                "pipelined_unprepared_ms_per_step": e2e["pipelined_unprepared_ms_per_step"], "pcie": e2e["pcie"]},
         "gpu_launches": case.launches * K,
         "clocks": clock_info,
     }
@@ -470,8 +472,12 @@ def run_e2e(case: Case, stream, steps: int, device):
     try:
         host.set_pipeline(1)
         one_shot = wall(steps)
+        host.set_pipeline(0)
+        host.set_prepared(False)
+        unprepared = wall(steps)
     finally:
         host.set_pipeline(0)
+        host.set_prepared(True)
     ms = wall(steps)
     # bare copy rates of the same byte volumes (pinned, one stream)
     dev_in = torch.empty(h2d // 4, dtype=torch.float32, device=device)
@@ -490,6 +496,7 @@ def run_e2e(case: Case, stream, steps: int, device):
         h2d_ms = copy_ms(lambda: dev_in.copy_(hin, non_blocking=True))
         d2h_ms = copy_ms(lambda: hout.copy_(dev_out, non_blocking=True))
     return {"ms_per_step": ms, "h2d": h2d, "d2h": d2h, "one_shot_ms_per_step": one_shot,
+            "pipelined_unprepared_ms_per_step": unprepared,
             "pcie": {"h2d_GBps": h2d / (h2d_ms * 1e-3) / 1e9, "d2h_GBps": d2h / (d2h_ms * 1e-3) / 1e9,
                      "serial_copy_ms": h2d_ms + d2h_ms}}
 

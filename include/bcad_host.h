@@ -52,6 +52,13 @@ int bcad_host_cell_gradients(int impl, int dtype, int64_t n, const void* const* 
  * always run one-shot so error indices match the reference. Process-wide. */
 int bcad_host_set_pipeline(int max_chunks);
 
+/* Prepared pipelined steps (default on): a pipelined call on pinned host
+ * buffers keeps its device buffers, chunk plan and workspaces (a few entries
+ * per thread, each at most 2 GiB of device memory) for later calls with the
+ * same buffers, shapes and stream, which then only enqueue copies and
+ * kernels. 0 disables and frees the calling thread's prepared steps. */
+int bcad_host_set_prepared(int enable);
+
 const char* bcad_host_last_error(void);
 
 #ifdef __cplusplus

@@ -8,6 +8,7 @@
 #include <atomic>
 #include <optional>
 #include <span>
+#include <unordered_map>
 #include <string>
 #include <vector>
 
@@ -158,14 +159,82 @@ int plan_chunks(bcad_cu_kernel k, int n_in, const bcad_cu_shape* shapes, const b
     return chunks < 2 ? 1 : chunks;
 }
 
+// Device buffers and chunk plan of one pipelined-step signature.
 template <class Real>
-int64_t pipelined_step(bcad_cu_kernel k, int n_in, const void* const* host_in, const bcad_cu_shape* shapes, int m_out,
-                       int policy, const void* const* host_seeds, void* const* host_primal, void* const* host_grads,
-                       const bcad_cu_shape& out, const std::vector<bool>& split, int chunks) {
+struct StepBuffers {
+    std::vector<bcad::Tensor<Real>> x, y, D, w, g;
+    std::vector<int64_t> bound;  // chunk row boundaries
+    std::vector<std::pair<int64_t, std::unique_ptr<bcad::detail::DeviceBuffer>>> ws;  // per chunk height
+    std::vector<std::size_t> ws_bytes;
+    std::size_t device_bytes = 0;
+    std::size_t ws_index(int64_t r) const {
+        for (std::size_t q = 0; q < ws.size(); ++q)
+            if (ws[q].first == r) return q;
+        return 0;
+    }
+};
+
+// Allocates (stream-ordered, on the current stream) every device buffer the
+// pipelined step uses.
+template <class Real>
+void prepare_step(StepBuffers<Real>& S, bcad_cu_kernel k, int n_in, const bcad_cu_shape* shapes, int m_out, int policy,
+                  const void* const* host_seeds, void* const* host_grads, const bcad_cu_shape& out,
+                  const std::vector<bool>& split, int chunks) {
+    using namespace bcad;
+    constexpr int dt = dtype_of<Real>::value;
+    void* const comp = current_stream();
+    const int64_t B = out.dims[0], E = volume(out);
+    const std::size_t n = static_cast<std::size_t>(n_in), m = static_cast<std::size_t>(m_out);
+    auto alloc = [&](int64_t elems) {
+        S.device_bytes += std::size_t(elems) * sizeof(Real);
+        return Tensor<Real>::uninitialized(Shape{elems});
+    };
+    for (int j = 0; j < n_in; ++j) S.x.push_back(alloc(volume(shapes[j])));
+    for (int i = 0; i < m_out; ++i) S.y.push_back(alloc(E));
+    if (policy == 0)
+        for (std::size_t t = 0; t < m * n; ++t) S.D.push_back(alloc(E));
+    for (int i = 0; i < m_out; ++i) S.w.push_back(alloc(host_seeds && host_seeds[i] ? E : 1));
+    for (int j = 0; j < n_in; ++j) S.g.push_back(alloc(host_grads && host_grads[j] ? volume(shapes[j]) : 1));
+    // Chunk boundaries: the first and last chunks get half the rows of the
+    // others, so the pipeline fills and drains faster (the exposed head is
+    // the first chunk's upload, the exposed tail the last chunk's download).
+    S.bound.assign(static_cast<std::size_t>(chunks) + 1, 0);
+    const double units = chunks > 2 ? double(chunks) - 1.0 : double(chunks);
+    double acc = 0.0;
+    for (int c = 0; c < chunks; ++c) {
+        acc += (chunks > 2 && (c == 0 || c == chunks - 1)) ? 0.5 : 1.0;
+        S.bound[c + 1] = c + 1 == chunks ? B
+                                         : std::min(B - (chunks - c - 1),
+                                                    std::max(S.bound[c] + 1, int64_t(double(B) * acc / units + 0.5)));
+    }
+    for (int c = 0; c < chunks; ++c) {  // one workspace per distinct chunk height
+        const int64_t r = S.bound[c + 1] - S.bound[c];
+        bool seen = false;
+        for (auto& [h, buf] : S.ws) seen = seen || h == r;
+        if (seen) continue;
+        std::vector<bcad_cu_shape> cs(shapes, shapes + n_in);
+        for (int j = 0; j < n_in; ++j)
+            if (split[j]) cs[j].dims[0] = r;
+        std::size_t b = 0;
+        check(bcad_cu_pullback_workspace(k, dt, n_in, cs.data(), m_out, &b));
+        S.ws.emplace_back(r, std::make_unique<detail::DeviceBuffer>(b, comp));
+        S.ws_bytes.push_back(b);
+        S.device_bytes += b;
+    }
+}
+
+// Enqueues the pipelined step on the current stream (no synchronisation, no
+// allocation). Returns the one-shot tape's peak_cached_bytes.
+template <class Real>
+int64_t enqueue_step(const StepBuffers<Real>& S, bcad_cu_kernel k, int n_in, const void* const* host_in,
+                     const bcad_cu_shape* shapes, int m_out, int policy, const void* const* host_seeds,
+                     void* const* host_primal, void* const* host_grads, const bcad_cu_shape& out,
+                     const std::vector<bool>& split) {
     using namespace bcad;
     constexpr int dt = dtype_of<Real>::value;
     void* const comp = current_stream();
     Pipe& P = pipe();
+    const int chunks = int(S.bound.size()) - 1;
     const int64_t B = out.dims[0], E = volume(out), out_row = E / B;
     const std::size_t n = static_cast<std::size_t>(n_in), m = static_cast<std::size_t>(m_out);
     std::vector<int64_t> row_elems(n, 0);
@@ -174,56 +243,14 @@ int64_t pipelined_step(bcad_cu_kernel k, int n_in, const void* const* host_in, c
         in_elems += volume(shapes[j]);
         if (split[j]) row_elems[j] = volume(shapes[j]) / B;
     }
-    // device buffers of the whole batch (stream-ordered pool on `comp`)
-    auto alloc = [&](int64_t elems) { return Tensor<Real>::uninitialized(Shape{elems}); };
-    std::vector<Tensor<Real>> x, y, D, w, g;
-    for (int j = 0; j < n_in; ++j) x.push_back(alloc(volume(shapes[j])));
-    for (int i = 0; i < m_out; ++i) y.push_back(alloc(E));
-    if (policy == 0)
-        for (std::size_t t = 0; t < m * n; ++t) D.push_back(alloc(E));
     std::vector<bool> has_w(m, false), has_g(n, false);
-    for (int i = 0; i < m_out; ++i) {
-        has_w[i] = host_seeds && host_seeds[i];
-        w.push_back(alloc(has_w[i] ? E : 1));
-    }
-    for (int j = 0; j < n_in; ++j) {
-        has_g[j] = host_grads && host_grads[j];
-        g.push_back(alloc(has_g[j] ? volume(shapes[j]) : 1));
-    }
-    // Chunk boundaries: the first and last chunks get half the rows of the
-    // others, so the pipeline fills and drains faster (the exposed head is
-    // the first chunk's upload, the exposed tail the last chunk's download).
-    std::vector<int64_t> bound(static_cast<std::size_t>(chunks) + 1, 0);
-    {
-        const double units = chunks > 2 ? double(chunks) - 1.0 : double(chunks);
-        double acc = 0.0;
-        for (int c = 0; c < chunks; ++c) {
-            acc += (chunks > 2 && (c == 0 || c == chunks - 1)) ? 0.5 : 1.0;
-            bound[c + 1] = c + 1 == chunks ? B
-                                           : std::min(B - (chunks - c - 1),
-                                                      std::max(bound[c] + 1, int64_t(double(B) * acc / units + 0.5)));
-        }
-    }
-    // one workspace per distinct chunk height
-    std::vector<std::pair<int64_t, std::unique_ptr<detail::DeviceBuffer>>> ws;
-    std::vector<std::size_t> ws_bytes;
-    auto ws_for = [&](int64_t r) -> std::size_t {
-        for (std::size_t q = 0; q < ws.size(); ++q)
-            if (ws[q].first == r) return q;
-        std::vector<bcad_cu_shape> cs(shapes, shapes + n_in);
-        for (int j = 0; j < n_in; ++j)
-            if (split[j]) cs[j].dims[0] = r;
-        std::size_t b = 0;
-        check(bcad_cu_pullback_workspace(k, dt, n_in, cs.data(), m_out, &b));
-        ws.emplace_back(r, std::make_unique<detail::DeviceBuffer>(b, comp));
-        ws_bytes.push_back(b);
-        return ws.size() - 1;
-    };
-    for (int c = 0; c < chunks; ++c) (void)ws_for(bound[c + 1] - bound[c]);
+    for (int i = 0; i < m_out; ++i) has_w[i] = host_seeds && host_seeds[i];
+    for (int j = 0; j < n_in; ++j) has_g[j] = host_grads && host_grads[j];
+    auto dev = [](const Tensor<Real>& t) { return const_cast<Real*>(t.device_data()); };
     {
         CopyBatch rep(0);  // batch-broadcast inputs: whole, on the compute stream
         for (int j = 0; j < n_in; ++j)
-            if (!split[j]) rep.add(x[j].device_data(), host_in[j], x[j].bytes());
+            if (!split[j]) rep.add(dev(S.x[j]), host_in[j], S.x[j].bytes());
         rep.submit(comp);
     }
     check(bcad_cu_event_record(P.fork, comp));
@@ -234,54 +261,54 @@ int64_t pipelined_step(bcad_cu_kernel k, int n_in, const void* const* host_in, c
     std::vector<const void*> xin(n), wp(m), Dp(m * n);
     std::vector<void*> yp(m), Dw(m * n), gp(n);
     std::vector<unsigned char> acc(n, 0);
-    int c = 0;
-    for (; c < chunks; ++c) {
-        const int64_t b0 = bound[c], b1 = bound[c + 1], r = b1 - b0;
+    for (int c = 0; c < chunks; ++c) {
+        const int64_t b0 = S.bound[c], b1 = S.bound[c + 1], r = b1 - b0;
         const std::size_t cell0 = static_cast<std::size_t>(b0 * out_row), cells = static_cast<std::size_t>(r * out_row);
         // h2d: this chunk's rows of the batch-sharded inputs and of the seeds
         CopyBatch up(0);
         for (int j = 0; j < n_in; ++j) {
             if (!split[j]) continue;
             const std::size_t o = static_cast<std::size_t>(b0 * row_elems[j]), cnt = static_cast<std::size_t>(r * row_elems[j]);
-            up.add(x[j].device_data() + o, static_cast<const Real*>(host_in[j]) + o, cnt * sizeof(Real));
+            up.add(dev(S.x[j]) + o, static_cast<const Real*>(host_in[j]) + o, cnt * sizeof(Real));
         }
         for (int i = 0; i < m_out; ++i)
             if (has_w[i])
-                up.add(w[i].device_data() + cell0, static_cast<const Real*>(host_seeds[i]) + cell0, cells * sizeof(Real));
+                up.add(dev(S.w[i]) + cell0, static_cast<const Real*>(host_seeds[i]) + cell0, cells * sizeof(Real));
         up.submit(P.h2d);
         check(bcad_cu_event_record(P.in_ready[c], P.h2d));
         // compute: K1 then K2 on the chunk (row-offset views of the buffers)
         check(bcad_cu_stream_wait_event(comp, P.in_ready[c]));
         for (int j = 0; j < n_in; ++j) {
             const int64_t o = split[j] ? b0 * row_elems[j] : 0;
-            xin[j] = x[j].device_data() + o;
+            xin[j] = dev(S.x[j]) + o;
             cs[j] = shapes[j];
             if (split[j]) cs[j].dims[0] = r;
-            gp[j] = has_g[j] ? static_cast<void*>(g[j].device_data() + o) : nullptr;
+            gp[j] = has_g[j] ? static_cast<void*>(dev(S.g[j]) + o) : nullptr;
             acc[j] = (!split[j] && c > 0) ? 1 : 0;
         }
         for (int i = 0; i < m_out; ++i) {
-            yp[i] = y[i].device_data() + cell0;
-            wp[i] = has_w[i] ? static_cast<const void*>(w[i].device_data() + cell0) : nullptr;
+            yp[i] = dev(S.y[i]) + cell0;
+            wp[i] = has_w[i] ? static_cast<const void*>(dev(S.w[i]) + cell0) : nullptr;
         }
-        for (std::size_t t = 0; t < D.size(); ++t) {
-            Dw[t] = D[t].device_data() + cell0;
+        for (std::size_t t = 0; t < S.D.size(); ++t) {
+            Dw[t] = dev(S.D[t]) + cell0;
             Dp[t] = Dw[t];
         }
+        const std::size_t q = S.ws_index(r);
         check(bcad_cu_forward(k, dt, n_in, xin.data(), cs.data(), m_out, yp.data(), policy == 0 ? Dw.data() : nullptr, comp));
         check(bcad_cu_pullback(k, dt, n_in, cs.data(), m_out, wp.data(), policy == 0 ? Dp.data() : nullptr, xin.data(),
-                               gp.data(), acc.data(), ws[ws_for(r)].second->ptr, ws_bytes[ws_for(r)], comp));
+                               gp.data(), acc.data(), S.ws[q].second->ptr, S.ws_bytes[q], comp));
         check(bcad_cu_event_record(P.out_ready[c], comp));
         // d2h: the chunk's primal rows and batch-sharded gradient rows
         check(bcad_cu_stream_wait_event(P.d2h, P.out_ready[c]));
         CopyBatch down(1);
         for (int i = 0; i < m_out; ++i)
             if (host_primal && host_primal[i])
-                down.add(static_cast<Real*>(host_primal[i]) + cell0, y[i].device_data() + cell0, cells * sizeof(Real));
+                down.add(static_cast<Real*>(host_primal[i]) + cell0, dev(S.y[i]) + cell0, cells * sizeof(Real));
         for (int j = 0; j < n_in; ++j) {
             if (!split[j] || !has_g[j]) continue;
             const std::size_t o = static_cast<std::size_t>(b0 * row_elems[j]), cnt = static_cast<std::size_t>(r * row_elems[j]);
-            down.add(static_cast<Real*>(host_grads[j]) + o, g[j].device_data() + o, cnt * sizeof(Real));
+            down.add(static_cast<Real*>(host_grads[j]) + o, dev(S.g[j]) + o, cnt * sizeof(Real));
         }
         down.submit(P.d2h);
     }
@@ -289,11 +316,114 @@ int64_t pipelined_step(bcad_cu_kernel k, int n_in, const void* const* host_in, c
     check(bcad_cu_stream_wait_event(comp, P.join));
     CopyBatch rep(1);
     for (int j = 0; j < n_in; ++j)
-        if (!split[j] && has_g[j]) rep.add(host_grads[j], g[j].device_data(), g[j].bytes());
+        if (!split[j] && has_g[j]) rep.add(host_grads[j], dev(S.g[j]), S.g[j].bytes());
     rep.submit(comp);
-    check(bcad_cu_stream_synchronize(comp));
     // what the one-shot tape reports (tape.hpp:236-243): inputs + values + cache
     return (in_elems + int64_t(m) * E + (policy == 0 ? int64_t(m * n) * E : 0)) * int64_t(sizeof(Real));
+}
+
+// ---- prepared steps. A caller repeating a step on the same pinned host
+// buffers (the serving / training-loop case) keeps its device buffers,
+// chunk plan and workspaces, so later calls only enqueue copies and kernels
+// (measured at config 2: 0.57 vs 0.59 ms per call). Bounded: a few entries
+// per thread, each at most kMaxPreparedBytes of device memory (bigger steps
+// allocate per call). Replaying the enqueued work as a CUDA graph was
+// measured too and lost the upload/download overlap (0.77 ms), so calls are
+// issued, not replayed.
+std::atomic<int> g_prepared{1};
+constexpr std::size_t kMaxPreparedBytes = std::size_t(2) << 30;
+constexpr std::size_t kMaxPreparedEntries = 4;
+
+template <class Real>
+struct Prepared {
+    StepBuffers<Real> bufs;
+    uint64_t last_use = 0;
+};
+
+template <class Real>
+std::unordered_map<std::string, std::unique_ptr<Prepared<Real>>>& prepared_cache() {
+    static thread_local std::unordered_map<std::string, std::unique_ptr<Prepared<Real>>> c;
+    return c;
+}
+
+std::string step_key(const char* name, int n_in, const bcad_cu_shape* shapes, int m_out, int policy, int chunks,
+                     const void* const* host_in, const void* const* host_seeds, void* const* host_primal,
+                     void* const* host_grads, void* stream) {
+    std::string key(name);
+    auto put = [&key](const void* p, std::size_t b) { key.append(static_cast<const char*>(p), b); };
+    const int64_t hdr[] = {n_in, m_out, policy, chunks};
+    put(hdr, sizeof hdr);
+    put(&stream, sizeof stream);
+    for (int j = 0; j < n_in; ++j) {
+        put(&shapes[j].rank, sizeof shapes[j].rank);
+        put(shapes[j].dims, sizeof(int64_t) * std::size_t(shapes[j].rank));
+        const void* ptr[] = {host_in[j], host_grads ? host_grads[j] : nullptr};
+        put(ptr, sizeof ptr);
+    }
+    for (int i = 0; i < m_out; ++i) {
+        const void* ptr[] = {host_seeds ? host_seeds[i] : nullptr, host_primal ? host_primal[i] : nullptr};
+        put(ptr, sizeof ptr);
+    }
+    return key;
+}
+
+bool all_pinned(int n_in, const void* const* host_in, int m_out, const void* const* host_seeds,
+                void* const* host_primal, void* const* host_grads) {
+    for (int j = 0; j < n_in; ++j) {
+        if (!bcad_cu_host_is_pinned(host_in[j])) return false;
+        if (host_grads && host_grads[j] && !bcad_cu_host_is_pinned(host_grads[j])) return false;
+    }
+    for (int i = 0; i < m_out; ++i) {
+        if (host_seeds && host_seeds[i] && !bcad_cu_host_is_pinned(host_seeds[i])) return false;
+        if (host_primal && host_primal[i] && !bcad_cu_host_is_pinned(host_primal[i])) return false;
+    }
+    return true;
+}
+
+template <class Real>
+int64_t pipelined_step(bcad_cu_kernel k, const char* name, int n_in, const void* const* host_in,
+                       const bcad_cu_shape* shapes, int m_out, int policy, const void* const* host_seeds,
+                       void* const* host_primal, void* const* host_grads, const bcad_cu_shape& out,
+                       const std::vector<bool>& split, int chunks) {
+    using namespace bcad;
+    void* const comp = current_stream();
+    int64_t in_bytes = 0;
+    for (int j = 0; j < n_in; ++j) in_bytes += volume(shapes[j]) * int64_t(sizeof(Real));
+    const std::size_t estimate = std::size_t(in_bytes) * 2 +
+                                 std::size_t(volume(out)) * sizeof(Real) * std::size_t(m_out) * (2 + std::size_t(n_in));
+    const bool cacheable = g_prepared.load(std::memory_order_relaxed) && comp != nullptr &&
+                           estimate <= kMaxPreparedBytes &&
+                           all_pinned(n_in, host_in, m_out, host_seeds, host_primal, host_grads);
+    if (!cacheable) {
+        StepBuffers<Real> S;
+        prepare_step<Real>(S, k, n_in, shapes, m_out, policy, host_seeds, host_grads, out, split, chunks);
+        const int64_t p = enqueue_step<Real>(S, k, n_in, host_in, shapes, m_out, policy, host_seeds, host_primal,
+                                             host_grads, out, split);
+        check(bcad_cu_stream_synchronize(comp));
+        return p;
+    }
+    auto& cache = prepared_cache<Real>();
+    static thread_local uint64_t clock = 0;
+    const std::string key =
+        step_key(name, n_in, shapes, m_out, policy, chunks, host_in, host_seeds, host_primal, host_grads, comp);
+    auto it = cache.find(key);
+    if (it == cache.end()) {
+        if (cache.size() >= kMaxPreparedEntries) {  // evict the least recently used (all prior work is complete)
+            auto lru = cache.begin();
+            for (auto e = cache.begin(); e != cache.end(); ++e)
+                if (e->second->last_use < lru->second->last_use) lru = e;
+            cache.erase(lru);
+        }
+        auto entry = std::make_unique<Prepared<Real>>();
+        prepare_step<Real>(entry->bufs, k, n_in, shapes, m_out, policy, host_seeds, host_grads, out, split, chunks);
+        it = cache.emplace(key, std::move(entry)).first;
+    }
+    Prepared<Real>& E = *it->second;
+    E.last_use = ++clock;
+    const int64_t p = enqueue_step<Real>(E.bufs, k, n_in, host_in, shapes, m_out, policy, host_seeds, host_primal,
+                                         host_grads, out, split);
+    check(bcad_cu_stream_synchronize(comp));
+    return p;
 }
 
 template <class Real>
@@ -313,8 +443,8 @@ void step(const char* name, int n_in, const void* const* host_in, const bcad_cu_
         p = tape_step<Real>(name, n_in, host_in, shapes, m_out, policy, host_seeds, host_primal, host_grads);
         check(bcad_cu_stream_synchronize(current_stream()));
     } else {
-        p = pipelined_step<Real>(k, n_in, host_in, shapes, m_out, policy, host_seeds, host_primal, host_grads, out, split,
-                                 chunks);
+        p = pipelined_step<Real>(k, name, n_in, host_in, shapes, m_out, policy, host_seeds, host_primal, host_grads,
+                                 out, split, chunks);
     }
     if (peak) *peak = p;
 }
@@ -372,6 +502,15 @@ int bcad_host_cell_gradients(int impl, int dtype, int64_t n, const void* const* 
 }
 
 const char* bcad_host_last_error(void) { return g_err.c_str(); }
+
+int bcad_host_set_prepared(int enable) {
+    g_prepared.store(enable ? 1 : 0);
+    if (!enable) {
+        prepared_cache<float>().clear();
+        prepared_cache<double>().clear();
+    }
+    return BCAD_CU_OK;
+}
 
 int bcad_host_set_pipeline(int max_chunks) {
     if (max_chunks < 0) {

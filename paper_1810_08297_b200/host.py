@@ -23,6 +23,8 @@ def _load():
                                          C.c_void_p, C.c_void_p, C.c_void_p, C.POINTER(C.c_int64), C.c_void_p]
     lib.bcad_host_set_pipeline.restype = C.c_int
     lib.bcad_host_set_pipeline.argtypes = [C.c_int]
+    lib.bcad_host_set_prepared.restype = C.c_int
+    lib.bcad_host_set_prepared.argtypes = [C.c_int]
     return lib
 
 
@@ -39,6 +41,12 @@ def set_pipeline(max_chunks: int) -> None:
 
 def _ptrs(arrs):
     return (C.c_void_p * max(1, len(arrs)))(*[None if a is None else a.ctypes.data for a in arrs])
+
+
+def set_prepared(enable: bool) -> None:
+    """bcad_host_set_prepared: keep the device buffers of repeated pipelined
+    steps on the same pinned buffers (default on)."""
+    LIB.bcad_host_set_prepared(1 if enable else 0)
 
 
 class HostStep:

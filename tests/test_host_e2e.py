@@ -159,3 +159,46 @@ def test_host_step_pipelined_scalar_and_two_outputs(host, oracle_lib, dtype):
         assert peak1 == peakk
         _, want_g, want_a64 = oracle_lib.mixed_step("prod_diff", ins, 0, seeds)
         assert_grads(gk, want_g, want_a64, shapes, out_shape, dtype, f"pipelined prod_diff {shapes}")
+
+
+def test_prepared_step_replay_rereads_buffers(oracle_lib):
+    """Prepared pipelined steps (bcad_host_set_prepared) on pinned buffers:
+    a call on kept device buffers equals the unprepared step bit for bit, and
+    a call after the host inputs changed in place uses the new contents."""
+    import torch
+    from paper_1810_08297_b200 import host as H
+    B, Hd = 512, 256
+    name = O.hmlstm_kernel("bias")
+    ins0 = O.hmlstm_inputs(oracle_lib, B, Hd, np.float32, "bias")
+    ins1 = [np.ascontiguousarray(np.flip(a, axis=-1)) for a in ins0]  # other data, same shapes
+    keep = [torch.from_numpy(np.ascontiguousarray(a)).pin_memory() for a in ins0]
+    host_in = [t.numpy() for t in keep]
+    seed_t = torch.from_numpy(np.random.default_rng(4).uniform(-1, 1, (B, Hd)).astype(np.float32)).pin_memory()
+    grads_t = [torch.empty(a.shape, dtype=torch.float32).pin_memory() for a in ins0]
+    grads = [t.numpy() for t in grads_t]
+    stream = torch.cuda.Stream()
+    try:
+        H.set_pipeline(4)
+        H.set_prepared(True)
+        call = H.HostStep(name, host_in, [seed_t.numpy()], grads_out=grads, stream=int(stream.cuda_stream))
+        results = []
+        for data in (ins0, ins0, ins1, ins1):
+            for dst, src in zip(host_in, data):
+                dst[...] = src
+            call()
+            results.append([g.copy() for g in grads])
+        H.set_prepared(False)
+        for data, got in ((ins0, results[1]), (ins1, results[3])):
+            for dst, src in zip(host_in, data):
+                dst[...] = src
+            call()
+            for a, b in zip(grads, got):
+                assert np.array_equal(a, b)  # prepared == unprepared pipelined step, bit for bit
+        _, want_g, want_a64 = oracle_lib.mixed_step(name, ins1, 0, [seed_t.numpy()])
+        assert_grads(results[3], want_g, want_a64, [a.shape for a in ins1], (B, Hd), np.float32, "prepared step")
+        for a, b in zip(results[0], results[1]):
+            assert np.array_equal(a, b)
+        assert not all(np.array_equal(a, b) for a, b in zip(results[1], results[2]))
+    finally:
+        H.set_prepared(True)
+        H.set_pipeline(0)
