@@ -351,6 +351,69 @@ void k2_det(const char* tag, bool bias, int64_t B, int64_t H, int cy_override, i
     std::fflush(stdout);
 }
 
+// Every reduced adjoint against a host fp64 sum of the rounded terms
+// T(w * D_j) (the device's own partials), under a tiling, with the workspace
+// poisoned (0xFF = NaN pattern) before the launch and once more re-run.
+template <class Body, class T, class Sig>
+void k2_check(const char* tag, bool bias, int64_t B, int64_t H, const std::vector<std::array<int, 2>>& tilings) {
+    Problem<T> P(bias, B, H);
+    constexpr int V = vec_width<T>();
+    fwd<Body, T, Sig>(P, nullptr);
+    const int64_t E = B * H;
+    std::vector<T*> dp(P.partials.begin(), P.partials.end());
+    dp.push_back(P.w);
+    const auto hp = snapshot(dp, std::vector<size_t>(dp.size(), size_t(E)));
+    const auto& hw = hp.back();
+    std::vector<std::vector<double>> want(P.n);
+    for (int j = 0; j < P.n; ++j) {
+        const int64_t v = Problem<T>::vol(P.shapes[j]);
+        want[j].assign(size_t(v), 0.0);
+        if (v == E) continue;
+        const bool col = v == H && P.shapes[j].rank == 2 && P.shapes[j].dims[0] == 1;
+        for (int64_t b = 0; b < B; ++b)
+            for (int64_t h = 0; h < H; ++h) {
+                const size_t e = size_t(b * H + h);
+                want[j][size_t(col ? h : b)] += double(T(hw[e] * hp[j][e]));
+            }
+    }
+    std::vector<std::array<int, 2>> all = {{0, 0}};
+    all.insert(all.end(), tilings.begin(), tilings.end());
+    std::vector<size_t> ns;
+    for (auto& s : P.shapes) ns.push_back(size_t(Problem<T>::vol(s)));
+    for (auto [txv, rpt] : all) {
+        Tiling t = txv == 0 ? choose_tiling(P.plan, V, class_mix(P.plan)) : make_tiling(P.plan, V, txv, rpt, 1);
+        if (t.n_row_tiles > 65535) continue;
+        CK(cudaMemset(P.ws, 0xff, P.ws_bytes));
+        pull<Body, T, Sig>(P, &t);
+        const auto got = snapshot(P.adj, ns);
+        CK(cudaMemset(P.ws, 0x00, P.ws_bytes));
+        pull<Body, T, Sig>(P, &t);
+        const bool rerun_same = snapshot(P.adj, ns) == got;
+        double worst = 0.0;
+        long long bad = 0;
+        int worst_j = -1;
+        long long worst_e = -1;
+        for (int j = 0; j < P.n; ++j) {
+            if (ns[j] == size_t(E)) continue;
+            for (size_t e = 0; e < ns[j]; ++e) {
+                const double x = got[j][e], y = want[j][e];
+                const double r = std::abs(x - y) / (std::abs(y) + 1e-6);
+                if (!(r <= 1e-6)) ++bad;
+                if (!(r <= worst)) {
+                    worst = r;
+                    worst_j = j;
+                    worst_e = (long long)e;
+                }
+            }
+        }
+        std::printf("{\"exp\": \"%s\", \"B\": %lld, \"H\": %lld, \"txv\": %d, \"rpt\": %d, \"grid\": [%lld, %lld], "
+                    "\"bad\": %lld, \"worst_rel\": %.3e, \"worst_arg\": %d, \"worst_elem\": %lld, \"rerun_same\": %s}\n",
+                    tag, (long long)B, (long long)H, t.txv, t.rpt, (long long)t.n_col_tiles, (long long)t.n_row_tiles,
+                    bad, worst, worst_j, worst_e, rerun_same ? "true" : "false");
+        std::fflush(stdout);
+    }
+}
+
 int main(int argc, char** argv) {
     std::string which = argc > 1 ? argv[1] : "all";
     if (which.size() > 2 && which.compare(which.size() - 2, 2, ":r") == 0) {
@@ -435,6 +498,16 @@ int main(int argc, char** argv) {
         fwd<KHmlstmBias, float, SigHmlstmBias>(P, &fdef);
         for (int k = 0; k < 3; ++k) pull<KHmlstmBias, float, SigHmlstmBias>(P, nullptr);
         CK(cudaDeviceSynchronize());
+    }
+    if (which == "k2check") {
+        std::vector<std::array<int, 2>> t;
+        for (int txv : {8, 16, 32, 64, 128, 256})
+            for (int rpt : {1, 2, 4, 16}) t.push_back({txv, rpt});
+        k2_check<KHmlstmBias, float, SigHmlstmBias>("k2check_4096", true, 4096, 1024, t);
+        k2_check<KHmlstmBias, float, SigHmlstmBias>("k2check_1024", true, 1024, 1024, t);
+        k2_check<KHmlstmBias, float, SigHmlstmBias>("k2check_8192x4096", true, 8192, 4096, {{32, 1}, {32, 4}});
+        k2_check<KHmlstm, float, SigHmlstmCanonical>("k2check_canon_1024", false, 1024, 1024, t);
+        k2_check<KHmlstmBias, double, SigHmlstmBias>("k2check_f64_4096", true, 4096, 1024, {{32, 1}, {16, 4}});
     }
     if (which == "all" || which == "det") {
         k2_det<KHmlstmBias, float, SigHmlstmBias>("det_cfg5", true, 65536, 4096, 0, 4);
