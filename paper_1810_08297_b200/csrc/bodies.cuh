@@ -153,6 +153,9 @@ struct KTanhProduct {  // arity_workload.hpp:19-28
     // cells per K1 thread: the product's dual keeps all A partials live, so
     // wide arities evaluate fewer cells at once (register study, paper Fig. 3)
     static constexpr int kMaxVec = A >= 16 ? 1 : A >= 8 ? 2 : 4;
+    // K1 rows per thread on large problems (lab k1rpt, 4096^2 fp32: A=4
+    // 2 rows 0.83 -> 8 rows 0.87 of the copy peak, A=16 0.66 -> 0.71; A=1 flat)
+    static constexpr int kFwdRows = 8;
     template <class S>
     BCAD_HD static void body_select(const S* in, S* out) { body(in, out); }
     template <class S>

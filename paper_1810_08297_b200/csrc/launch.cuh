@@ -89,6 +89,21 @@ constexpr int fwd_vec_width() {
     else return v;
 }
 
+// K1's rows per thread on large problems (more than two waves of CTAs):
+// short CTAs, unless the body asks for more (Body::kFwdRows). The
+// primal-only K1p moves 5 tensors per cell instead of 1 + N + M*N and wants
+// longer CTAs. Measured (scripts/lab k1rpt / k5, fraction of the copy peak):
+// HM-LSTM bias 65536 x 4096 fp32 K1 2 rows 1.02, 4 rows 1.00, 55 rows 0.94;
+// fp64 8192 x 2048 K1 2 rows 1.00, 8 rows 0.96; K1p 65536 x 4096 2 rows 0.88,
+// 16 rows 1.00; tanh_product_4 4096^2 2 rows 0.83, 8 rows 0.87;
+// tanh_product_16 2 rows 0.66, 16 rows 0.71.
+constexpr int kFwdRows = 2, kFwdRowsPrimalOnly = 16;
+template <class Body>
+constexpr int fwd_rows() {
+    if constexpr (requires { Body::kFwdRows; }) return Body::kFwdRows;
+    else return kFwdRows;
+}
+
 // The tiled 2-D forward at VV cells per thread (the body's vector width, or
 // 1 for widths / pointers that do not allow vectors).
 template <class Body, class T, int VV, class... Sigs>
@@ -96,7 +111,9 @@ int launch_fwd2d(const FwdArgs& a, std::string* err) {
     constexpr int N = Body::kIn, M = Body::kOut;
     const Plan& plan = *a.plan;
     const bool real = a.partials == nullptr;
-    const Tiling t = a.tiling ? *a.tiling : choose_tiling(plan, VV, ClassMix{}, /*fine=*/true);  // no reductions in K1: wide row tiles
+    // no reductions in K1: wide row tiles
+    const Tiling t = a.tiling ? *a.tiling
+                              : choose_tiling(plan, VV, ClassMix{}, /*fine=*/true, real ? kFwdRowsPrimalOnly : fwd_rows<Body>());
     bcad_dev::Fwd2DParams<N, M, T> p{};
     for (int j = 0; j < N; ++j) {
         p.in[j] = static_cast<const T*>(a.in[j]);

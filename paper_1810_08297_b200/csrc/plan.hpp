@@ -179,12 +179,13 @@ inline ClassMix class_mix(const Plan& p) {
 //    (cols x row tiles) against the per-row ones (rows x column tiles);
 //  * otherwise a CTA spans up to 256 vector-columns of one row, so (B)-arg
 //    reductions finish inside the CTA (shuffles + one shared-memory pass).
-// Rows per thread: one wave of CTAs for small problems (latency-bound), about
-// eight waves for large ones (tail-bound), never more than 65535 row tiles.
+// Rows per thread: one wave of CTAs for small problems (latency-bound); short
+// CTAs for large ones (K1 `fine_rows`, the pullback about eight waves and at
+// most 16 rows), never more than 65535 row tiles.
 // fine = true (forward): small problems keep one row per thread so the
 // hardware's dynamic CTA scheduling evens out rows of unequal cost (the
 // HM-LSTM UPDATE / FLUSH / COPY branch is per row).
-inline Tiling choose_tiling(const Plan& p, int V, const ClassMix& mix, bool fine = false) {
+inline Tiling choose_tiling(const Plan& p, int V, const ClassMix& mix, bool fine = false, int fine_rows = 2) {
     Tiling t;
     t.V = V;
     t.vcols = p.cols / V;
@@ -207,11 +208,16 @@ inline Tiling choose_tiling(const Plan& p, int V, const ClassMix& mix, bool fine
     t.n_col_tiles = ceil_div(t.vcols, txv);
     const int64_t tiles1 = ceil_div(p.rows, t.ty);  // row tiles at rpt = 1
     const int64_t work = tiles1 * t.n_col_tiles;     // CTAs at rpt = 1
-    int64_t rpt = work <= 2 * slots ? (fine ? 1 : ceil_div(work, slots)) : work / (8 * slots);
+    // Large problems: short CTAs, many waves. K1 (fine, no reductions) takes
+    // `fine_rows` rows per thread (launch.cuh fwd_rows); the pullback about
+    // eight waves, at most 16 rows per thread. Measured at config 5 (lab k5,
+    // bias 65536 x 4096 fp32): K1 55 -> 2 rows 0.94 -> 1.02 of the copy peak,
+    // K2 55 -> 16 rows 0.94 -> 0.97.
+    int64_t rpt = work <= 2 * slots ? (fine ? 1 : ceil_div(work, slots)) : (fine ? fine_rows : work / (8 * slots));
     if (col_small) rpt = ceil_div(work, 2 * kSmCount);
     else if (mix.col && !fine && rpt < 4) rpt = 4;
     if (rpt < 1) rpt = 1;
-    if (rpt > 512) rpt = 512;
+    if (!fine && rpt > 16) rpt = 16;
     // keep the per-tile row partials in shared memory small
     if (mix.row)
         while (rpt > 1 && rpt * t.ty * (txv > 32 ? txv / 32 : 1) > 4096) rpt >>= 1;

@@ -72,6 +72,7 @@ struct Flush {
 
 static Flush* g_flush;
 static bool g_recompute = false;  // pull(): RecomputeReverse (partials re-derived) instead of cached
+static bool g_primal_only = false;  // fwd(): primal only (K1p, broadcast_apply)
 static cudaStream_t g_s;
 
 double time_us(const std::function<void()>& fn, int reps = 25) {
@@ -129,19 +130,23 @@ struct Problem {
         for (int k = 0; k < s.rank; ++k) v *= s.dims[k];
         return v;
     }
-    Problem(bool bias, int64_t B_, int64_t H_) : B(B_), H(H_) {
-        for (int k = 0; k < 4; ++k) shapes.push_back(shp({B, H}));
-        if (bias)
+    // bias: the HM-LSTM bias variant; arity > 0: tanh_product_<arity> (all full, no binary args)
+    Problem(bool bias, int64_t B_, int64_t H_, int arity = 0) : B(B_), H(H_) {
+        for (int k = 0; k < (arity > 0 ? arity : 4); ++k) shapes.push_back(shp({B, H}));
+        if (bias && arity == 0)
             for (int k = 0; k < 3; ++k) shapes.push_back(shp({1, H}));
-        shapes.push_back(shp({B}));
-        shapes.push_back(shp({B}));
+        if (arity == 0) {
+            shapes.push_back(shp({B}));
+            shapes.push_back(shp({B}));
+        }
         n = int(shapes.size());
+        const int n_binary = arity > 0 ? 0 : 2;
         const int64_t E = B * H;
         size_t in_elems = 0;
         for (int j = 0; j < n; ++j) {
             T* p;
             CK(cudaMalloc(&p, vol(shapes[j]) * sizeof(T)));
-            init_kernel<<<1024, 256>>>(p, vol(shapes[j]), 77u + 13u * j, j >= n - 2);
+            init_kernel<<<1024, 256>>>(p, vol(shapes[j]), 77u + 13u * j, j >= n - n_binary);
             in.push_back(p);
             in_elems += vol(shapes[j]);
             T* d;
@@ -176,13 +181,15 @@ int fwd(Problem<T>& P, const Tiling* t) {
     a.dtype = sizeof(T) == 4 ? BCAD_CU_F32 : BCAD_CU_F64;
     a.in = in.data();
     a.primal = prim;
-    a.partials = parts.data();
+    a.partials = g_primal_only ? nullptr : parts.data();
     a.stream = g_s;
     a.err = P.err;
     a.plan = &P.plan;
     a.tiling = t;
     std::string e;
-    const int rc = launch_fwd_t<Body, T, Sig>(a, &e);
+    int rc;
+    if constexpr (std::is_same_v<Sig, DynSig>) rc = launch_fwd_t<Body, T>(a, &e);
+    else rc = launch_fwd_t<Body, T, Sig>(a, &e);
     if (rc) std::fprintf(stderr, "fwd rc %d %s\n", rc, e.c_str());
     return rc;
 }
@@ -248,9 +255,11 @@ void print_tiling(const char* tag, const char* variant, int64_t B, int64_t H, co
 }
 
 template <class Body, class T, class Sig>
-void k1_sweep(const char* tag, bool bias, int64_t B, int64_t H, const std::vector<std::array<int, 2>>& tilings) {
-    Problem<T> P(bias, B, H);
-    constexpr int V = vec_width<T>();
+void k1_sweep(const char* tag, bool bias, int64_t B, int64_t H, const std::vector<std::array<int, 2>>& tilings,
+              int arity = 0) {
+    Problem<T> P(bias, B, H, arity);
+    if (g_primal_only) P.k1_bytes -= size_t(P.n) * B * H * sizeof(T);
+    constexpr int V = fwd_vec_width<Body, T>();
     const Tiling def = choose_tiling(P.plan, V, ClassMix{}, true);
     fwd<Body, T, Sig>(P, &def);
     std::vector<T*> outs(P.partials.begin(), P.partials.end());
@@ -269,7 +278,7 @@ void k1_sweep(const char* tag, bool bias, int64_t B, int64_t H, const std::vecto
         print_tiling(tag, "tiled", B, H, t, us, double(P.k1_bytes), same);
     }
     if constexpr (sizeof(T) == 4) {
-        if (!bias) {  // memory-only floor of the same access pattern
+        if (!bias && arity == 0 && !g_primal_only) {  // memory-only floor of the same access pattern
             float4** d_outs;
             CK(cudaMalloc(&d_outs, 7 * sizeof(float4*)));
             std::vector<float4*> h(7);
@@ -498,6 +507,33 @@ int main(int argc, char** argv) {
         fwd<KHmlstmBias, float, SigHmlstmBias>(P, &fdef);
         for (int k = 0; k < 3; ++k) pull<KHmlstmBias, float, SigHmlstmBias>(P, nullptr);
         CK(cudaDeviceSynchronize());
+    }
+    if (which == "k1b") {  // bias forward tilings ((1,H) loads amortised over rows per thread)
+        const std::vector<std::array<int, 2>> t = {{256, 1}, {256, 2}, {256, 4}, {256, 8}, {64, 2}, {64, 4},
+                                                    {32, 2}, {32, 4}, {32, 8}};
+        for (int64_t B : {256, 1024, 2048, 4096, 16384})
+            k1_sweep<KHmlstmBias, float, SigHmlstmBias>(("k1b_" + std::to_string(B)).c_str(), true, B, 1024, t);
+        k1_sweep<KHmlstmBias, float, SigHmlstmBias>("k1b_8192x4096", true, 8192, 4096, t);
+        k1_sweep<KHmlstm, float, SigHmlstmCanonical>("k1c_4096", false, 4096, 1024, t);
+    }
+    if (which == "k1rpt") {  // rows per thread of K1 / K1p across body widths
+        const std::vector<std::array<int, 2>> t = {{256, 1}, {256, 2}, {256, 4}, {256, 8}, {256, 16}, {256, 32}};
+        k1_sweep<KTanhProduct<1>, float, DynSig>("k1_tp1_4096", false, 4096, 4096, t, 1);
+        k1_sweep<KTanhProduct<4>, float, DynSig>("k1_tp4_4096", false, 4096, 4096, t, 4);
+        k1_sweep<KTanhProduct<16>, float, DynSig>("k1_tp16_4096", false, 4096, 4096, t, 16);
+        k1_sweep<KHmlstm, double, SigHmlstmCanonical>("k1_cfg4", false, 8192, 2048, t);
+        g_primal_only = true;
+        k1_sweep<KHmlstmBias, float, SigHmlstmBias>("k1p_cfg5", true, 65536, 4096, t);
+        k1_sweep<KHmlstm, float, SigHmlstmCanonical>("k1p_cfg2", false, 1024, 1024, t);
+        g_primal_only = false;
+    }
+    if (which == "k5") {  // config-5 size: wave quantisation of the default rpt
+        k1_sweep<KHmlstmBias, float, SigHmlstmBias>("k1_cfg5", true, 65536, 4096,
+                                                    {{256, 2}, {256, 4}, {256, 8}, {256, 28}, {256, 55}, {256, 56},
+                                                     {64, 2}, {64, 4}});
+        k2_sweep<KHmlstmBias, float, SigHmlstmBias>("k2_cfg5", true, 65536, 4096,
+                                                    {{32, 8, 1}, {32, 16, 1}, {32, 28, 1}, {32, 55, 1}, {32, 56, 1},
+                                                     {32, 64, 1}, {16, 16, 1}, {16, 28, 1}, {16, 56, 1}});
     }
     if (which == "k2check") {
         std::vector<std::array<int, 2>> t;
