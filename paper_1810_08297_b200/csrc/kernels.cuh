@@ -60,6 +60,10 @@ __device__ __forceinline__ Pack<T, V> ld_stream(const T* p) {
     return r;
 }
 
+// L2 prefetch of a line a later loop iteration reads (no register, no
+// scoreboard: the thread does not wait for it)
+__device__ __forceinline__ void prefetch_l2(const void* p) { asm volatile("prefetch.global.L2 [%0];" ::"l"(p)); }
+
 template <class T, int V>
 __device__ __forceinline__ Pack<T, V> ld_ro(const T* p) {  // read-only, may be re-read (COL args)
     Pack<T, V> r;
@@ -358,6 +362,7 @@ struct Pull2DParams {
     int64_t rows, cols;
     int vcols;
     int txv_shift, ty, rpt;
+    int prefetch;         // rows ahead whose streams are prefetched into L2 (0 = none)
     int64_t tile_rows;
     int n_row_tiles, n_col_tiles;
     int n_row_args, n_col_args, n_scalar_args;
@@ -463,16 +468,43 @@ __global__ void __launch_bounds__(kThreads, kRecompute ? kRecomputeCtasPerSm : k
         }
     };
 
+    // L2 prefetch of a later row's streams (register-free lookahead; a
+    // register double buffer would push the kernel below its resident CTAs)
+    auto prefetch_row = [&](int64_t r) {
+        const int64_t off = r * p.cols + c0;
+#pragma unroll
+        for (int i = 0; i < M; ++i)
+            if (kDense || p.w[i]) prefetch_l2(p.w[i] + off);
+        if constexpr (kRecompute) {
+#pragma unroll
+            for (int j = 0; j < N; ++j)
+                if (arg_class<S>(p.cls, j) == kFull) prefetch_l2(p.in[j] + off);
+        } else {
+#pragma unroll
+            for (int i = 0; i < M; ++i)
+#pragma unroll
+                for (int j = 0; j < N; ++j)
+                    if (kDense || (p.w[i] && p.adj[j])) prefetch_l2(p.D[i * N + j] + off);
+        }
+    };
+
+    // Compiled into the RecomputeReverse pullback of the registered signatures
+    // only: in the cached pullback it gains at most 1% and its addresses spill
+    // the all-FULL (divergence) signatures at 64 registers; the select-form
+    // (per-cell branch) recompute has no registers to spare for them either.
+    constexpr bool kPrefetch = kRecompute && S::kStatic && !(Body::kSelectForm && !vec_eval_ok<Body, S>());
     const int64_t r0 = int64_t(rt) * p.tile_rows + ty;
     // Every lane runs the same rpt iterations (rows past the end are masked),
-    // so the ROW shuffles always see complete lane groups. (No next-row
-    // prefetch here: it would push the kernel past 64 registers, i.e. below
-    // four resident CTAs per SM, which the tiling assumes.)
+    // so the ROW shuffles always see complete lane groups.
     for (int k = 0; k < p.rpt; ++k) {
         const int64_t r = r0 + int64_t(k) * p.ty;
         const bool live = active && r < p.rows;
+
         Pack<T, V> w[M], q[kStreams];
         if (live) load_row(r, w, q);
+        if (kPrefetch && k == 0 && active)  // behind the first row's loads
+            for (int kk = 1; kk <= p.prefetch && kk < p.rpt; ++kk)
+                if (r0 + int64_t(kk) * p.ty < p.rows) prefetch_row(r0 + int64_t(kk) * p.ty);
         const int64_t off = r * p.cols + c0;
         Pack<T, V> D[M * N];
         if constexpr (kRecompute) {
@@ -537,6 +569,11 @@ __global__ void __launch_bounds__(kThreads, kRecompute ? kRecomputeCtasPerSm : k
                 if ((tid & (lanes - 1)) == 0)
                     row_acc[(arg_slot<S, kDense>(p.slot, j) * trows + k * p.ty) * wpr + row_base] = t;
             }
+        }
+        // issued after this row's registers are retired (fewest live values)
+        if (kPrefetch && p.prefetch > 0 && active && k + 1 + p.prefetch < p.rpt) {
+            const int64_t rp = r + int64_t(1 + p.prefetch) * p.ty;
+            if (rp < p.rows) prefetch_row(rp);
         }
     }
     if constexpr (!kAnyRow && !kAnyCol && !kAnyScal) return;

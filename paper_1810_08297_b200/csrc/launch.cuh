@@ -182,6 +182,18 @@ int launch_fwd_t(const FwdArgs& a, std::string* err) {
 }
 
 // --------------------------------------------------------------- pullback
+// Pullback L2 lookahead (RecomputeReverse kernels only, kernels.cuh): the
+// streams of a thread's next row are prefetched into L2 while it evaluates
+// the current one. Measured (scripts/lab k2pf, fraction of the copy peak,
+// lookahead 0 -> 1): config 5 0.80 -> 0.92, fp64 config 4 0.82 -> 0.92,
+// canonical 65536 x 4096 0.95 -> 1.00, bias 16384 x 1024 0.61 -> 0.66;
+// neutral at config 3, off at two rows per thread (config 2: nothing to
+// overlap). Two rows ahead is slower everywhere.
+inline int pull_prefetch_rows(bool recompute, const Tiling& t) {
+    if (t.prefetch >= 0) return t.prefetch;
+    return recompute && t.rpt >= 3 ? 1 : 0;
+}
+
 // The tiled 2-D pullback at VV cells per thread (VV = the 128-bit width, or
 // 1 for widths / pointers that do not allow vectors) with signature
 // dispatch over Sigs (none: runtime classes only).
@@ -219,6 +231,7 @@ int launch_pull2d(const PullArgs& a, std::string* err) {
     p.txv_shift = __builtin_ctz(unsigned(t.txv));
     p.ty = t.ty;
     p.rpt = t.rpt;
+    p.prefetch = pull_prefetch_rows(recompute, t);
     p.tile_rows = t.tile_rows;
     p.n_col_tiles = int(t.n_col_tiles);
     p.n_row_tiles = int(t.n_row_tiles);

@@ -146,6 +146,7 @@ struct Tiling {
     int txv = 32, ty = 8, rpt = 1;
     int64_t tile_rows = 8;
     int64_t n_row_tiles = 1, n_col_tiles = 1, n_ctas = 1;
+    int prefetch = -1;  // pullback: rows ahead prefetched into L2 (-1 = the launcher's default)
 };
 
 constexpr int kSmCount = 148;

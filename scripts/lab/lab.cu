@@ -423,6 +423,29 @@ void k2_check(const char* tag, bool bias, int64_t B, int64_t H, const std::vecto
     }
 }
 
+// Pullback time under L2 lookahead distances 0..2, CacheForward and RecomputeReverse.
+template <class Body, class T, class Sig>
+void k2_prefetch(const char* tag, bool bias, int64_t B, int64_t H) {
+    Problem<T> P(bias, B, H);
+    fwd<Body, T, Sig>(P, nullptr);
+    constexpr int V = vec_width<T>();
+    const int64_t E = B * H;
+    for (int rec : {0, 1}) {
+        g_recompute = rec;
+        for (int pf : {0, 1, 2}) {
+            Tiling t = choose_tiling(P.plan, V, class_mix(P.plan));
+            t.prefetch = pf;
+            const double us = time_us([&] { pull<Body, T, Sig>(P, &t); }, 21);
+            // recompute streams the 4 full inputs instead of the n partials
+            const double bytes = rec ? double(P.k2_bytes) - double(P.n - 4) * E * sizeof(T) : double(P.k2_bytes);
+            std::printf("{\"exp\": \"%s\", \"recompute\": %d, \"prefetch\": %d, \"rpt\": %d, \"us\": %.3f, "
+                        "\"frac\": %.3f}\n", tag, rec, pf, t.rpt, us, bytes / (us * 1e-6) / 1e9 / 6544.0);
+            std::fflush(stdout);
+        }
+    }
+    g_recompute = false;
+}
+
 int main(int argc, char** argv) {
     std::string which = argc > 1 ? argv[1] : "all";
     if (which.size() > 2 && which.compare(which.size() - 2, 2, ":r") == 0) {
@@ -526,6 +549,14 @@ int main(int argc, char** argv) {
         k1_sweep<KHmlstmBias, float, SigHmlstmBias>("k1p_cfg5", true, 65536, 4096, t);
         k1_sweep<KHmlstm, float, SigHmlstmCanonical>("k1p_cfg2", false, 1024, 1024, t);
         g_primal_only = false;
+    }
+    if (which == "k2pf") {  // pullback L2 lookahead, both policies, several sizes
+        k2_prefetch<KHmlstmBias, float, SigHmlstmBias>("k2pf_cfg5", true, 65536, 4096);
+        k2_prefetch<KHmlstm, float, SigHmlstmCanonical>("k2pf_cfg2", false, 1024, 1024);
+        k2_prefetch<KHmlstmBias, float, SigHmlstmBias>("k2pf_cfg3", true, 1024, 1024);
+        k2_prefetch<KHmlstmBias, float, SigHmlstmBias>("k2pf_bias16384", true, 16384, 1024);
+        k2_prefetch<KHmlstm, double, SigHmlstmCanonical>("k2pf_cfg4", false, 8192, 2048);
+        k2_prefetch<KHmlstm, float, SigHmlstmCanonical>("k2pf_canon65536x4096", false, 65536, 4096);
     }
     if (which == "k5") {  // config-5 size: wave quantisation of the default rpt
         k1_sweep<KHmlstmBias, float, SigHmlstmBias>("k1_cfg5", true, 65536, 4096,
