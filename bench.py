@@ -417,7 +417,7 @@ def run_native(args, w: Workload, rank: int, world: int):
                    "parallelism": f"batch-sharded dp{world}" if world > 1 else "single GPU",
                    "l2": L2Flush.DESCRIPTION,
                    "launch": "CUDA graph replay of K1->K2 (PDL edges)" if args.graph else "stream launches (PDL)"},
-        "breakdown_ms": {"K1_forward": k1_avg, "K2_pullback": k2_avg, "allreduce": statistics.mean(ar_ms),
+        "breakdown_ms": {"K1_forward": k1_avg, "K2_pullback": k2_avg, "allreduce": statistics.mean(ar_ms) if comm is not None else None,
                          "step_min": min(step_ms), "step_median": statistics.median(step_ms)},
         "step_roofline": {"bytes": step_bytes, "achieved_GBps": step_bytes / (statistics.mean(step_ms) * 1e-3) / 1e9,
                           "frac": step_bytes / (statistics.mean(step_ms) * 1e-3) / 1e9 / peak},

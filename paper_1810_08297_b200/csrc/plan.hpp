@@ -183,9 +183,9 @@ inline ClassMix class_mix(const Plan& p) {
 // Rows per thread: one wave of CTAs for small problems (latency-bound); short
 // CTAs for large ones (K1 `fine_rows`, the pullback about eight waves and at
 // most 16 rows), never more than 65535 row tiles.
-// fine = true (forward): small problems keep one row per thread so the
-// hardware's dynamic CTA scheduling evens out rows of unequal cost (the
-// HM-LSTM UPDATE / FLUSH / COPY branch is per row).
+// Small problems (at most two waves at one row per thread) run as one wave:
+// config-2 K1 at two rows per thread 12.3 us against 14.3 us at one
+// (interleaved A/B, scripts/lab k1ab; config 3 unchanged).
 inline Tiling choose_tiling(const Plan& p, int V, const ClassMix& mix, bool fine = false, int fine_rows = 2) {
     Tiling t;
     t.V = V;
@@ -214,7 +214,7 @@ inline Tiling choose_tiling(const Plan& p, int V, const ClassMix& mix, bool fine
     // eight waves, at most 16 rows per thread. Measured at config 5 (lab k5,
     // bias 65536 x 4096 fp32): K1 55 -> 2 rows 0.94 -> 1.02 of the copy peak,
     // K2 55 -> 16 rows 0.94 -> 0.97.
-    int64_t rpt = work <= 2 * slots ? (fine ? 1 : ceil_div(work, slots)) : (fine ? fine_rows : work / (8 * slots));
+    int64_t rpt = work <= 2 * slots ? ceil_div(work, slots) : (fine ? fine_rows : work / (8 * slots));
     if (col_small) rpt = ceil_div(work, 2 * kSmCount);
     else if (mix.col && !fine && rpt < 4) rpt = 4;
     if (rpt < 1) rpt = 1;

@@ -56,6 +56,42 @@ __global__ void copy_floor_kernel(const float4* c, const float4* f, const float4
     }
 }
 
+
+// the same floor with 256-bit loads (ld.global.v8.f32, LDG.E.256 on sm_100a) and 2 x 128-bit stores
+struct F8 { float v[8]; };
+__device__ __forceinline__ F8 ld8(const float* p) {
+    F8 r;
+    asm volatile("ld.global.L1::no_allocate.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=f"(r.v[0]), "=f"(r.v[1]), "=f"(r.v[2]), "=f"(r.v[3]), "=f"(r.v[4]), "=f"(r.v[5]), "=f"(r.v[6]), "=f"(r.v[7])
+                 : "l"(p));
+    return r;
+}
+__device__ __forceinline__ void st8(float* p, const F8& a) {
+    asm volatile("st.global.v8.f32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p), "f"(a.v[0]), "f"(a.v[1]), "f"(a.v[2]),
+                 "f"(a.v[3]), "f"(a.v[4]), "f"(a.v[5]), "f"(a.v[6]), "f"(a.v[7]) : "memory");
+}
+__global__ void copy_floor8_kernel(const float* c, const float* f, const float* i, const float* g, const float* z1,
+                                   const float* z2, float* const* outs, int vcols8, size_t nvec8, int st256) {
+    for (size_t k = blockIdx.x * size_t(blockDim.x) + threadIdx.x; k < nvec8; k += size_t(gridDim.x) * blockDim.x) {
+        const size_t r = k / vcols8;
+        const float a = __ldg(z1 + r) + __ldg(z2 + r);
+        F8 x = ld8(c + 8 * k), y = ld8(f + 8 * k), u = ld8(i + 8 * k), w = ld8(g + 8 * k);
+        F8 o[7];
+        for (int e = 0; e < 8; ++e) {
+            o[0].v[e] = x.v[e] + a; o[1].v[e] = y.v[e] * a; o[2].v[e] = u.v[e] - a; o[3].v[e] = w.v[e] + a;
+            o[4].v[e] = a; o[5].v[e] = x.v[e]; o[6].v[e] = y.v[e];
+        }
+        for (int t = 0; t < 7; ++t) {
+            if (st256) st8(outs[t] + 8 * k, o[t]);
+            else {
+                float4* d = reinterpret_cast<float4*>(outs[t] + 8 * k);
+                d[0] = make_float4(o[t].v[0], o[t].v[1], o[t].v[2], o[t].v[3]);
+                d[1] = make_float4(o[t].v[4], o[t].v[5], o[t].v[6], o[t].v[7]);
+            }
+        }
+    }
+}
+
 struct Flush {
     float* buf = nullptr;
     float* sink = nullptr;
@@ -297,6 +333,18 @@ void k1_sweep(const char* tag, bool bias, int64_t B, int64_t H, const std::vecto
                 std::printf("{\"exp\": \"%s\", \"variant\": \"copy_floor\", \"blocks\": %d, \"us\": %.3f, \"GBps\": %.1f}\n",
                             tag, blocks, us, double(P.k1_bytes) / (us * 1e-6) / 1e9);
             }
+            const size_t nvec8 = size_t(B * H / 8);
+            for (int st256 : {0, 1})
+                for (int blocks : {148 * 2, 148 * 4, int((nvec8 + 255) / 256)}) {
+                    us = time_us([&] {
+                        copy_floor8_kernel<<<blocks, 256, 0, g_s>>>(P.in[0], P.in[1], P.in[2], P.in[3], P.in[4], P.in[5],
+                                                                    reinterpret_cast<float* const*>(d_outs), int(H / 8),
+                                                                    nvec8, st256);
+                    });
+                    std::printf("{\"exp\": \"%s\", \"variant\": \"copy_floor_v8%s\", \"blocks\": %d, \"us\": %.3f, "
+                                "\"GBps\": %.1f}\n", tag, st256 ? "_st256" : "", blocks, us,
+                                double(P.k1_bytes) / (us * 1e-6) / 1e9);
+                }
             CK(cudaFree(d_outs));
         }
     }
@@ -456,6 +504,22 @@ int main(int argc, char** argv) {
     CK(cudaStreamCreateWithFlags(&g_s, cudaStreamNonBlocking));
     g_flush = new Flush();
     using namespace bcad_dev;
+    if (which == "k1ab") {  // interleaved A/B of K1 rows per thread on small problems
+        Problem<float> Pc(false, 1024, 1024), Pb(true, 1024, 1024);
+        for (int rep = 0; rep < 6; ++rep)
+            for (int rpt : {1, 2, 4}) {
+                const Tiling tc = make_tiling(Pc.plan, 4, 256, rpt, 1), tb = make_tiling(Pb.plan, 4, 256, rpt, 1);
+                const double uc = time_us([&] { fwd<KHmlstm, float, SigHmlstmCanonical>(Pc, &tc); }, 41);
+                const double ub = time_us([&] { fwd<KHmlstmBias, float, SigHmlstmBias>(Pb, &tb); }, 41);
+                std::printf("{\"exp\": \"k1ab\", \"rep\": %d, \"rpt\": %d, \"cfg2_us\": %.3f, \"cfg3_us\": %.3f}\n", rep,
+                            rpt, uc, ub);
+                std::fflush(stdout);
+            }
+    }
+    if (which == "floor") {
+        k1_sweep<KHmlstm, float, SigHmlstmCanonical>("k1_cfg2", false, 1024, 1024, {{256, 1}, {256, 2}});
+        k1_sweep<KHmlstm, float, SigHmlstmCanonical>("k1_4096", false, 4096, 1024, {{256, 2}});
+    }
     if (which == "all" || which == "k1") {
         const std::vector<std::array<int, 2>> t1 = {{256, 1}, {256, 2}, {128, 1}, {128, 2}, {64, 1}, {64, 2},
                                                      {32, 1}, {32, 2}, {32, 4}};
