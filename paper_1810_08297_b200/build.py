@@ -117,7 +117,7 @@ def build_oracle(verbose: bool = False):
     oracle/_ref/libbcad_ref.so only where /root/reference exists."""
     mk = os.path.join(ROOT, "oracle", "Makefile")
     targets = ["all"] if os.path.isdir("/root/reference/proj") else [os.path.join(ROOT, "oracle", "liboracle.so")]
-    _run(["make", "-s", "-f", mk, *targets], verbose)
+    _run(["make", "-s", "-j8", "-f", mk, *targets], verbose)
 
 
 def build_all(verbose: bool = False):
