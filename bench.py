@@ -399,9 +399,9 @@ def run_native(args, w: Workload, rank: int, world: int):
             elif key == "arity":
                 extra[key] = measure_arity(device, stream, max(5, K // 2))
             elif key.endswith(":r"):  # RecomputeReverse: K1p primal + fused K2r
-                extra[key] = measure_secondary(WORKLOADS[key[:-2]], device, stream, max(5, K // 2), 1)
+                extra[key] = measure_secondary(WORKLOADS[key[:-2]], device, stream, max(5, K // 2), 1, bool(args.graph))
             else:
-                extra[key] = measure_secondary(WORKLOADS[key], device, stream, max(5, K // 2), args.policy)
+                extra[key] = measure_secondary(WORKLOADS[key], device, stream, max(5, K // 2), args.policy, bool(args.graph))
 
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
@@ -501,7 +501,7 @@ def run_e2e(case: Case, stream, steps: int, device):
                      "serial_copy_ms": h2d_ms + d2h_ms}}
 
 
-def measure_secondary(w: Workload, device, stream, steps: int, policy: int):
+def measure_secondary(w: Workload, device, stream, steps: int, policy: int, graph_step: bool = True):
     import torch
     case = Case(w, w.B, device, seed=99, policy=policy)
     l2 = L2Flush(device)
@@ -509,24 +509,48 @@ def measure_secondary(w: Workload, device, stream, steps: int, policy: int):
     ev = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(steps)]
     ev2 = [[torch.cuda.Event(enable_timing=True) for _ in range(2)] for _ in range(steps)]
     with torch.cuda.stream(stream):
-        for k in range(3 + 2 * steps):
+        # per-kernel split: stream launches with events between K1 and K2
+        for k in range(3 + steps):
             l2()
-            e = ev[k - 3] if 3 <= k < 3 + steps else (ev2[k - 3 - steps] if k >= 3 + steps else None)
+            e = ev[k - 3] if k >= 3 else None
             if e:
                 e[0].record(stream)
             case.step.forward(sp)
-            if e and len(e) == 3:
+            if e:
                 e[1].record(stream)
             case.step.pullback(sp)
             if e:
-                e[-1].record(stream)
+                e[2].record(stream)
+    graph = None
+    if graph_step:  # the step as the headline runs it: one CUDA-graph replay (PDL edges kept)
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.stream(stream):
+            with torch.cuda.graph(graph, stream=stream):
+                case.step.forward(sp)
+                case.step.pullback(sp)
+        torch.cuda.synchronize(device)
+    with torch.cuda.stream(stream):
+        for k in range(3 + steps):
+            l2()
+            e = ev2[k - 3] if k >= 3 else None
+            if e:
+                e[0].record(stream)
+            if graph is not None:
+                graph.replay()
+            else:
+                case.step.forward(sp)
+                case.step.pullback(sp)
+            if e:
+                e[1].record(stream)
     torch.cuda.synchronize(device)
+    del graph
     peak, _ = hbm_peak()
     step = statistics.mean(e[0].elapsed_time(e[1]) for e in ev2)
     k1 = statistics.mean(e[0].elapsed_time(e[1]) for e in ev)
     k2 = statistics.mean(e[1].elapsed_time(e[2]) for e in ev)
     b1, b2 = w.k1_bytes(policy=policy), w.k2_bytes(policy=policy)
     out = {"workload": w.describe, "ms_per_step": step, "value": w.E / (step * 1e-3), "unit": "grad elements/s",
+           "launch": "step: CUDA graph replay; K1/K2 split: stream launches" if graph_step else "stream launches",
            "K1_ms": k1, "K2_ms": k2, "K1_frac_hbm": b1 / (k1 * 1e-3) / 1e9 / peak,
            "K2_frac_hbm": b2 / (k2 * 1e-3) / 1e9 / peak,
            "step_frac_hbm": (b1 + b2) / (step * 1e-3) / 1e9 / peak}
