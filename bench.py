@@ -105,6 +105,25 @@ class ClockSampler:
 
 
 # -------------------------------------------------------------- reference
+def cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def reference_split(ref, w: Workload, ins, rows: int, reps: int, threads: int = 0) -> dict:
+    """the reference step's forward (tape inputs + mixed_broadcast)
+    and backward (Tape::backward + gradient copies) medians, scaled to the
+    full batch like ms_per_step."""
+    f, b = ref.time_mixed_split(w.kernel, ins, threads=threads, reps=reps)
+    scale = w.B / rows
+    return {"forward_ms": statistics.median(f) / 1e6 * scale, "backward_ms": statistics.median(b) / 1e6 * scale}
+
+
 def cpu_reference_rate(w: Workload, budget_s: float, min_reps: int = 1, threads: int = 0):
     """Time the unmodified reference (oracle/_ref) on host cores: Tape +
     mixed_broadcast(CacheForward) + backward(ones), bench.cpp:112-128.
@@ -138,10 +157,13 @@ def cpu_reference_rate(w: Workload, budget_s: float, min_reps: int = 1, threads:
         cores = 1
     med = statistics.median(ns)
     cells = rows * w.H
-    return {"value": cells / (med * 1e-9), "unit": "grad elements/s", "cores": cores, "kind": kind,
-            "sample": f"{rows}x{w.H} rows of {w.B}x{w.H} {w.dtype} {w.variant}, {len(ns)} reps, median "
-                      f"{med / 1e6:.2f} ms/rep",
-            "ms_per_rep": med / 1e6, "reps": len(ns)}
+    out = {"value": cells / (med * 1e-9), "unit": "grad elements/s", "cores": cores, "kind": kind,
+           "sample": f"{rows}x{w.H} rows of {w.B}x{w.H} {w.dtype} {w.variant}, {len(ns)} reps, median "
+                     f"{med / 1e6:.2f} ms/rep",
+           "ms_per_rep": med / 1e6, "reps": len(ns), "cpu_model": cpu_model(), "omp_threads": cores}
+    if ref:
+        out["split"] = reference_split(ref, w, ins, rows, 3, threads)
+    return out
 
 
 def run_reference_arm(args, w: Workload, rank: int, world: int):
@@ -181,8 +203,12 @@ def run_reference_arm(args, w: Workload, rank: int, world: int):
             "scaling": "weak", "vs_baseline": None, "dtype": w.dtype, "data": "synthetic (bcad Rng, mix_seed)",
             "config": {"workload": w.describe, "B": w.B, "H": w.H, "variant": w.variant},
             "cpu_baseline": {"value": val, "unit": "grad elements/s", "cores": cores, "kind": kind,
-                             "sample": f"{rows}x{w.H} of {w.B}x{w.H} per step (rows are independent)"},
+                             "sample": f"{rows}x{w.H} of {w.B}x{w.H} per step (rows are independent)",
+                             "cpu_model": cpu_model(), "omp_threads": cores,
+                             "nproc": os.cpu_count()},
             "e2e": {"value": val, "unit": "grad elements/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    if ref:
+        line["breakdown_ms"] = reference_split(ref, w, ins, rows, max(1, args.steps))
     print(json.dumps(line), flush=True)
 
 

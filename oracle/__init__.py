@@ -256,6 +256,19 @@ class Reference(_Base):
         return [int(v) for v in out]
 
 
+    def time_mixed_split(self, name, inputs, policy=CACHE_FORWARD, threads=0, reps=3):
+        """Per-rep (forward ns, backward ns) of the reference mixed step, split
+        after mixed_broadcast."""
+        fwd, bwd = (C.c_uint64 * reps)(), (C.c_uint64 * reps)()
+        f = self.lib.ref_time_mixed_split
+        f.argtypes = [C.c_char_p, C.c_int, C.c_int, C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.c_int,
+                      C.c_void_p, C.c_void_p]
+        ins = [np.ascontiguousarray(a) for a in inputs]
+        self._check(f(name.encode(), _dt(inputs[0].dtype), len(inputs), _ptrs(ins),
+                      _shapes([a.shape for a in inputs]), policy, threads, reps, fwd, bwd))
+        return [int(v) for v in fwd], [int(v) for v in bwd]
+
+
 def reference_available() -> bool:
     return os.path.exists(REF_SO)
 

@@ -177,17 +177,21 @@ void forward_t(const char* name, int n, const void* const* in, const OShape* sha
     }
 }
 
+std::uint64_t now_ns();
+
 // One mixed step through the reference's tape (bench.cpp:112-128):
 // inputs -> mixed_broadcast(policy) -> backward(seeds) -> leaf gradients.
+// t_mid (optional) receives the clock after mixed_broadcast (forward / backward split).
 template <class Real>
 std::int64_t mixed_step_t(const BroadcastKernel<Real>& k, const std::vector<Tensor<Real>>& args,
                           int policy, const void* const* seeds, void* const* primal_out,
-                          void* const* grads_out) {
+                          void* const* grads_out, std::uint64_t* t_mid = nullptr) {
     Tape<Real> tape;
     std::vector<Var<Real>> vars;
     for (const auto& a : args) vars.push_back(tape.input(a));
     const auto outs = mixed_broadcast<Real>(
         tape, k, vars, policy == 0 ? MixedPolicy::CacheForward : MixedPolicy::RecomputeReverse);
+    if (t_mid) *t_mid = now_ns();
     std::vector<std::pair<Var<Real>, Tensor<Real>>> sv;
     for (size_t i = 0; i < outs.size(); ++i) {
         const Tensor<Real>& val = tape.value(outs[i]);
@@ -317,6 +321,37 @@ int ref_time_mixed(const char* name, int dtype, int n_in, const void* const* in,
                 const std::uint64_t t0 = now_ns();
                 mixed_step_t<Real>(k, args, policy, seeds.data(), nullptr, nullptr);
                 out_ns[r] = now_ns() - t0;
+            }
+        };
+        if (dtype == 0) run(float{});
+        else run(double{});
+        set_broadcast_threads(0);
+    });
+}
+
+// The same steps split at the end of mixed_broadcast: forward (tape inputs +
+// the mixed node's forward) and backward (seed + Tape::backward + gradient
+// copies) ns per rep (SURVEY §8(d) asks for both).
+int ref_time_mixed_split(const char* name, int dtype, int n_in, const void* const* in, const OShape* shapes,
+                         int policy, int threads, int reps, uint64_t* fwd_ns, uint64_t* bwd_ns) {
+    return guarded([&] {
+        set_broadcast_threads(threads);
+        auto run = [&](auto tag) {
+            using Real = decltype(tag);
+            const auto k = make_kernel<Real>(name);
+            const auto args = wrap_inputs<Real>(n_in, in, shapes);
+            std::vector<Shape> s;
+            for (const auto& a : args) s.push_back(a.shape());
+            const Shape out = broadcast_shape(std::span<const Shape>(s));
+            std::vector<Real> ones(size_t(out.volume()), Real(1));
+            std::vector<const void*> seeds(size_t(k.arity_out()), ones.data());
+            for (int r = 0; r < reps; ++r) {
+                std::uint64_t mid = 0;
+                const std::uint64_t t0 = now_ns();
+                mixed_step_t<Real>(k, args, policy, seeds.data(), nullptr, nullptr, &mid);
+                const std::uint64_t t1 = now_ns();
+                fwd_ns[r] = mid - t0;
+                bwd_ns[r] = t1 - mid;
             }
         };
         if (dtype == 0) run(float{});
