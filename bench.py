@@ -4,8 +4,15 @@
 allreduce of batch-broadcast adjoints when sharded), BASELINE.json metric
 "HM-LSTM cell-update grad elements/s & ms/step at 1/2/4/8 B200; % HBM roofline".
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--config cfg2] [--impl native|reference]
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config cfgX] [--impl native|reference]
   python -m torch.distributed.run --nproc-per-node N --master-addr 127.0.0.1 bench.py --gpus N
+
+--gpus N > 1 without a torchrun environment re-launches itself under
+torch.distributed.run with N ranks (one per GPU); under torchrun WORLD_SIZE
+must equal --gpus. Default workload: config 2 (1024x1024 fp32, BASELINE's
+"on 1 B200" config) at N = 1; config 5 (65536x4096 fp32 bias variant,
+batch-sharded, NCCL allreduce of the 3 (1,H) adjoints, strong scaling) at
+N > 1. --dry-run runs the N-rank plumbing on CPU over gloo (no GPU work).
 
 One step = one pass of the hot path over one batch: bcad_cu_forward (primal +
 M*N partials) then bcad_cu_pullback (all input adjoints) — what the
@@ -34,7 +41,8 @@ import time
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-from paper_1810_08297_b200.workloads import WORKLOADS, Workload, shard_rows  # noqa: E402
+from paper_1810_08297_b200.partition import plan as shard_plan  # noqa: E402
+from paper_1810_08297_b200.workloads import WORKLOADS, Workload  # noqa: E402
 
 PEAKS_PATH = os.path.join(ROOT, "MEASURED_PEAKS.json")
 FALLBACK_HBM_GBS = 6650.0  # /opt/skills/guides/B200_PROFILING.md fallback
@@ -102,6 +110,30 @@ class ClockSampler:
         busy = [s for s in sm if mx and s > 0.5 * mx] or sm
         return {"sm_mhz": statistics.median(busy) if busy else None, "sm_max_mhz": mx,
                 "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ------------------------------------------------- shared by both arms
+DATA = ("synthetic: bcad Rng (mt19937_64) inputs in the reference's order, mix_seed(42, B*1000003+H) "
+        "(proj/src/bench.cpp:31-37; U(-1,1) gates, exact-binary z with p=1/2), output seed of ones")
+
+
+def input_seed(w: Workload) -> int:
+    from paper_1810_08297_b200 import host
+    return host.mix_seed(42, w.B * 1000003 + w.H)
+
+
+def bench_config(w: Workload, world: int, policy: int) -> dict:
+    """`config` of the JSON line, identical for the GPU arm and the
+    reference arm so the driver can compare them."""
+    return {"workload": w.describe, "B": w.B, "H": w.H, "variant": w.variant, "dtype": w.dtype,
+            "policy": "CacheForward" if policy == 0 else "RecomputeReverse",
+            "parallelism": (f"batch rows sharded over {world} ranks, allreduce of batch-broadcast adjoints"
+                            if world > 1 else "single GPU"),
+            "l2": L2Flush.DESCRIPTION}
+
+
+def scaling_of(w: Workload) -> str:
+    return "strong" if w.key == "cfg5" else "weak"
 
 
 # -------------------------------------------------------------- reference
@@ -200,8 +232,8 @@ def run_reference_arm(args, w: Workload, rank: int, world: int):
     line = {"impl": "reference", "metric": "HM-LSTM cell-update grad elements/s", "value": val,
             "unit": "grad elements/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": total_s * 1e3 / len(ns) * (w.B / rows), "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": w.dtype, "data": "synthetic (bcad Rng, mix_seed)",
-            "config": {"workload": w.describe, "B": w.B, "H": w.H, "variant": w.variant},
+            "scaling": scaling_of(w), "vs_baseline": None, "dtype": w.dtype, "data": DATA,
+            "config": bench_config(w, world, 0),
             "cpu_baseline": {"value": val, "unit": "grad elements/s", "cores": cores, "kind": kind,
                              "sample": f"{rows}x{w.H} of {w.B}x{w.H} per step (rows are independent)",
                              "cpu_model": cpu_model(), "omp_threads": cores,
@@ -235,24 +267,52 @@ class L2Flush:
 
 
 class Case:
-    """Device buffers of one mixed step on this rank's batch shard."""
+    """Device buffers of one mixed step on this rank's batch shard [b0, b1).
 
-    def __init__(self, w: Workload, B_local: int, device, seed: int, policy: int = 0):
+    inputs="rng": the reference's own input stream (bcad Rng, mix_seed(42,
+    B*1000003+H), bcad_host_random_inputs) for this rank's rows of the FULL
+    batch — the union of the shards of any world size is the single-GPU
+    batch, and the replicated (1,H) bias arguments are identical on every
+    rank; generated into pinned host buffers that the e2e leg reuses.
+    inputs="philox": device Philox draws (secondary measurements only)."""
+
+    def __init__(self, w: Workload, device, rows=None, policy: int = 0, inputs: str = "rng", seed: int = 99):
+        import numpy as np
         import torch
         from paper_1810_08297_b200 import native
-        self.w, self.B, self.policy = w, B_local, policy
+        b0, b1 = rows if rows is not None else (0, w.B)
+        B_local = b1 - b0
+        self.w, self.B, self.policy, self.rows = w, B_local, policy, (b0, b1)
         dt = torch.float32 if w.dtype == "f32" else torch.float64
         self.dt = dt
-        g = torch.Generator(device=device)
-        g.manual_seed(seed)
         shapes = w.shapes(B_local)
         self.shapes = shapes
-        ins = []
-        for s, kind in zip(shapes, w.kinds()):
-            if kind == "pm1":
-                ins.append(torch.rand(s, generator=g, device=device, dtype=dt) * 2 - 1)
-            else:
-                ins.append((torch.rand(s, generator=g, device=device, dtype=dt) < 0.5).to(dt))
+        self.host_ins = None
+        if inputs == "rng":
+            from paper_1810_08297_b200 import host
+            p = shard_plan(w.shapes(), 1, 0)  # which arguments carry the batch axis
+            blocks = []
+            for j, full in enumerate(w.shapes()):
+                vol = int(math.prod(full))
+                if p.sharded[j]:
+                    row = vol // full[0]
+                    blocks.append((b0 * row, B_local * row))
+                else:
+                    blocks.append((0, vol))
+            self.host_ins = [torch.empty(s_, dtype=dt, pin_memory=True) for s_ in shapes]
+            host.random_inputs(input_seed(w), np.float32 if dt == torch.float32 else np.float64,
+                               list(zip(w.shapes(), w.kinds())), blocks,
+                               out=[t.numpy().reshape(-1) for t in self.host_ins])
+            ins = [t.to(device, non_blocking=False) for t in self.host_ins]
+        else:
+            g = torch.Generator(device=device)
+            g.manual_seed(seed)
+            ins = []
+            for s_, kind in zip(shapes, w.kinds()):
+                if kind == "pm1":
+                    ins.append(torch.rand(s_, generator=g, device=device, dtype=dt) * 2 - 1)
+                else:
+                    ins.append((torch.rand(s_, generator=g, device=device, dtype=dt) < 0.5).to(dt))
         self.ins = ins
         self.k = native.Kernel(w.kernel)
         out = (B_local, w.H)
@@ -266,11 +326,11 @@ class Case:
         self.bias_adj = None
         if w.variant == "bias":
             self.bias_adj = torch.empty((3, w.H), device=device, dtype=dt)
-        for j, s in enumerate(shapes):
+        for j, s_ in enumerate(shapes):
             if w.variant == "bias" and 4 <= j <= 6:
                 self.adj.append(self.bias_adj[j - 4:j - 3])
             else:
-                self.adj.append(torch.empty(s, device=device, dtype=dt))
+                self.adj.append(torch.empty(s_, device=device, dtype=dt))
         self.ws = native.new_workspace(self.k, shapes, dt, device)
         # K1 + K2, plus the finisher K2f when a reduction spans CTAs
         code = native.F32 if dt == torch.float32 else native.F64
@@ -285,25 +345,32 @@ def run_native(args, w: Workload, rank: int, world: int):
     from paper_1810_08297_b200 import native
 
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if torch.cuda.device_count() <= local:
+        raise SystemExit(f"bench.py: rank {rank} needs cuda:{local} but {torch.cuda.device_count()} GPU(s) are "
+                         f"visible; run --gpus N with at most the visible GPU count")
     torch.cuda.set_device(local)
     device = torch.device("cuda", local)
     native.check(native.LIB.bcad_cu_set_device(local))
 
-    strong = w.key == "cfg5"
-    if strong:
-        b0, b1 = shard_rows(w.B, world, rank)
-        B_local = b1 - b0
+    strong = scaling_of(w) == "strong"
+    if strong:  # partition.plan: contiguous batch-row block of this rank
+        p = shard_plan(w.shapes(), world, rank)
+        b0, b1 = p.rows
     else:
-        B_local = w.B  # weak scaling: one B-row batch per GPU
-    case = Case(w, B_local, device, seed=1234 + rank, policy=args.policy)
+        b0, b1 = 0, w.B  # weak scaling: one B-row batch per GPU
+    B_local = b1 - b0
+    case = Case(w, device, rows=(b0, b1), policy=args.policy, inputs="rng")
     stream = torch.cuda.Stream(device)
     sp = int(stream.cuda_stream)
 
     comm = None
+    nccl_nranks = None
     if world > 1 and w.variant == "bias":
         uid = [native.nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(uid, src=0)
         comm = native.Comm(world, uid[0], rank)
+        nccl_nranks = comm.nranks
+        assert nccl_nranks == world, (nccl_nranks, world)
 
     l2 = L2Flush(device)
     K, W = args.steps, args.warmup
@@ -461,18 +528,16 @@ def run_native(args, w: Workload, rank: int, world: int):
     line = {
         "metric": "HM-LSTM cell-update grad elements/s", "value": value, "unit": "grad elements/s",
         "n_gpus": world, "steps": K, "warmup": W, "ms_per_step": ms_per_step, "higher_is_better": True,
-        "scaling": "strong" if strong else "weak", "vs_baseline": None, "dtype": w.dtype,
-        "data": "synthetic (device Philox U(-1,1) gates, Bernoulli(1/2) exact-binary z), seed of ones",
-        "config": {"workload": w.describe, "B": w.B, "H": w.H, "B_per_gpu": B_local, "variant": w.variant,
-                   "policy": "CacheForward" if args.policy == 0 else "RecomputeReverse",
-                   "parallelism": f"batch-sharded dp{world}" if world > 1 else "single GPU",
-                   "l2": L2Flush.DESCRIPTION,
-                   "launch": "CUDA graph replay of K1->K2 (PDL edges)" if args.graph else "stream launches (PDL)"},
+        "scaling": scaling_of(w), "vs_baseline": None, "dtype": w.dtype, "data": DATA,
+        "config": bench_config(w, world, args.policy),
+        "run": {"B_per_gpu": B_local, "rows_rank0": [b0, b1],
+                "launch": "CUDA graph replay of K1->K2 (PDL edges)" if args.graph else "stream launches (PDL)"},
         "breakdown_ms": {"K1_forward": k1_avg, "K2_pullback": k2_avg,
                          "timing": ("events captured in the step's CUDA graph" if k1_ms is k1_graph
                                     else "events around stream launches"),
                          "K1_forward_stream_launch": statistics.mean(k1_stream),
-                         "K2_pullback_stream_launch": statistics.mean(k2_stream), "allreduce": statistics.mean(ar_ms) if comm is not None else None,
+                         "K2_pullback_stream_launch": statistics.mean(k2_stream),
+                         "allreduce": statistics.mean(ar_ms) if comm is not None else None,
                          "step_min": min(step_ms), "step_median": statistics.median(step_ms)},
         "step_roofline": {"bytes": step_bytes, "achieved_GBps": step_bytes / (statistics.mean(step_ms) * 1e-3) / 1e9,
                           "frac": step_bytes / (statistics.mean(step_ms) * 1e-3) / 1e9 / peak},
@@ -483,13 +548,26 @@ def run_native(args, w: Workload, rank: int, world: int):
                      "peak_source": peak_src},
         "e2e": {"value": e2e_value, "unit": "grad elements/s", "h2d_bytes_per_step": e2e["h2d"],
                 "d2h_bytes_per_step": e2e["d2h"], "ms_per_step": e2e["ms_per_step"],
-                "schedule": "row-chunk pipelined host step (bcad_host_set_pipeline auto), prepared: device buffers kept "
-                            "across calls on the same pinned buffers (bcad_host_set_prepared)",
-                "one_shot_ms_per_step": e2e["one_shot_ms_per_step"],
+                "path": ("bcad_host_mixed_step (include/bcad_host.h), default schedule: row-chunk pipelined over "
+                         "copy/compute streams, prepared (device buffers kept across calls on the same pinned "
+                         "buffers); each chunk is bcad_cu_forward + bcad_cu_pullback through the C-ABI, not "
+                         "through the C++ Tape"),
+                "tape_path": {"ms_per_step": e2e["one_shot_ms_per_step"],
+                              "value": cells_per_step / (e2e["one_shot_ms_per_step"] * 1e-3),
+                              "path": "bcad_host_mixed_step one-shot (bcad_host_set_pipeline(1)): C++ Tape + "
+                                      "mixed_broadcast + Tape::backward over device tensors, reference run_cell_once "
+                                      "order (bench.cpp:112-128)"},
                 "pipelined_unprepared_ms_per_step": e2e["pipelined_unprepared_ms_per_step"], "pcie": e2e["pcie"]},
         "gpu_launches": case.launches * K,
         "clocks": clock_info,
     }
+    if world > 1:
+        line["multi_gpu"] = {"nccl_nranks": nccl_nranks, "world_size": world,
+                             "allreduce_us_per_step": (statistics.mean(ar_ms) * 1e3 if comm is not None else None),
+                             "allreduce_bytes": (case.bias_adj.numel() * case.bias_adj.element_size()
+                                                 if comm is not None else 0),
+                             "timing": "max over ranks of the K-step device time (CUDA events, barrier + sync "
+                                       "on both sides)"}
     if cpu:
         line["cpu_baseline"] = cpu
     if extra:
@@ -507,7 +585,7 @@ def run_e2e(case: Case, stream, steps: int, device):
     copy rates of the same bytes are measured beside it."""
     import torch
     from paper_1810_08297_b200 import host
-    host_in = [t.cpu().pin_memory() for t in case.ins]
+    host_in = case.host_ins if case.host_ins is not None else [t.cpu().pin_memory() for t in case.ins]
     host_seed = case.seed.cpu().pin_memory()
     host_grad = [torch.empty(t.shape, dtype=t.dtype).pin_memory() for t in case.adj]
     np_in = [t.numpy() for t in host_in]
@@ -560,7 +638,7 @@ def run_e2e(case: Case, stream, steps: int, device):
 
 def measure_secondary(w: Workload, device, stream, steps: int, policy: int, graph_step: bool = True):
     import torch
-    case = Case(w, w.B, device, seed=99, policy=policy)
+    case = Case(w, device, policy=policy, inputs="philox", seed=99)
     l2 = L2Flush(device)
     sp = int(stream.cuda_stream)
     ev = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(steps)]
@@ -703,12 +781,48 @@ def measure_arity(device, stream, steps: int):
     return out
 
 
+def spawn_ranks(n: int) -> int:
+    """Re-launch this command under torch.distributed.run with n ranks on
+    this node (rendezvous on 127.0.0.1); returns the launcher's exit code."""
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__), *sys.argv[1:]]
+    env = dict(os.environ, OMP_NUM_THREADS=os.environ.get("OMP_NUM_THREADS", "1"))
+    return subprocess.call(cmd, env=env)
+
+
+def run_dry(args, w: Workload, rank: int, world: int):
+    """--dry-run: the N-rank plumbing on CPU (gloo): every rank plans its
+    batch shard, the ranks are counted by an allreduce, and rank 0 prints
+    the plan. No GPU work, no timing."""
+    import torch
+    import torch.distributed as dist
+    p = shard_plan(w.shapes(), world, rank) if scaling_of(w) == "strong" else shard_plan(w.shapes(), 1, 0)
+    one = torch.ones(1, dtype=torch.int64)
+    if world > 1:
+        dist.all_reduce(one)
+    rows = [None] * world
+    if world > 1:
+        dist.all_gather_object(rows, list(p.rows))
+    else:
+        rows = [list(p.rows)]
+    if rank == 0:
+        print(json.dumps({"dry_run": True, "n_gpus": world, "ranks_seen": int(one.item()),
+                          "backend": dist.get_backend() if world > 1 else None, "scaling": scaling_of(w),
+                          "config": bench_config(w, world, args.policy), "rows_per_rank": rows,
+                          "allreduce_args": list(p.allreduce)}), flush=True)
+
+
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--gpus", type=int, default=None, help="ranks (one per GPU); default: WORLD_SIZE or 1")
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--config", default="cfg2", choices=sorted(WORKLOADS))
+    ap.add_argument("--config", default=None, choices=sorted(WORKLOADS),
+                    help="default cfg2 at one GPU, cfg5 (strong scaling, NCCL allreduce) at N > 1")
     ap.add_argument("--impl", default="native", choices=["native", "reference"])
     ap.add_argument("--policy", type=int, default=0, help="0 CacheForward, 1 RecomputeReverse")
     ap.add_argument("--e2e-steps", type=int, default=10)
@@ -719,13 +833,28 @@ def main():
                          "shards = config 5's per-GPU batch shards at G = 2, 4, 8 timed on this GPU")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=12.0)
+    ap.add_argument("--dry-run", action="store_true", help="N-rank plumbing only, gloo on CPU")
     args = ap.parse_args()
     if args.warmup < 3:
         ap.error("--warmup must be >= 3")
 
+    if "WORLD_SIZE" not in os.environ and (args.gpus or 1) > 1:
+        sys.exit(spawn_ranks(args.gpus))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
-    w = WORKLOADS[args.config]
+    if args.gpus is not None and args.gpus != world:
+        ap.error(f"--gpus {args.gpus} but the launcher started {world} rank(s)")
+    w = WORKLOADS[args.config or ("cfg2" if world == 1 else "cfg5")]
+    if args.dry_run:
+        import torch.distributed as dist
+        if world > 1:
+            dist.init_process_group("gloo")
+        try:
+            run_dry(args, w, rank, world)
+        finally:
+            if world > 1:
+                dist.destroy_process_group()
+        return
     if args.impl == "reference":
         run_reference_arm(args, w, rank, world)
         return
@@ -733,7 +862,7 @@ def main():
         import torch
         import torch.distributed as dist
         torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")))
-        dist.init_process_group("nccl")
+        dist.init_process_group("nccl", device_id=torch.device("cuda", int(os.environ.get("LOCAL_RANK", "0"))))
     try:
         run_native(args, w, rank, world)
     finally:

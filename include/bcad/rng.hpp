@@ -16,6 +16,9 @@ public:
     double uniform_pm1() { return 2.0 * uniform01() - 1.0; }
     double binary(double p_one = 0.5) { return uniform01() < p_one ? 1.0 : 0.0; }
     std::uint64_t below(std::uint64_t n) { return gen_() % n; }
+    // Skip n draws (every distribution above consumes exactly one draw), so a
+    // row block of a tensor can be generated without its predecessors.
+    void discard(std::uint64_t n) { gen_.discard(n); }
 
 private:
     std::mt19937_64 gen_;

@@ -196,6 +196,8 @@ int bcad_cu_graph_destroy(void* graph_exec);
 int bcad_cu_nccl_unique_id(unsigned char id[128]);
 int bcad_cu_comm_init(void** comm, int nranks, const unsigned char id[128], int rank);
 int bcad_cu_comm_destroy(void* comm);
+/* Number of ranks in the communicator (ncclCommCount). */
+int bcad_cu_comm_count(void* comm, int* nranks);
 /* In-place sum over ranks of n_bufs device buffers (counts in elements), one
  * grouped NCCL launch on `stream`: the reduced adjoints of batch-broadcast
  * arguments after a batch-sharded pullback. */

@@ -59,6 +59,19 @@ int bcad_host_set_pipeline(int max_chunks);
  * kernels. 0 disables and frees the calling thread's prepared steps. */
 int bcad_host_set_prepared(int enable);
 
+/* Deterministic inputs bit-identical to the reference's (proj/include/bcad/
+ * rng.hpp:11-31, tensor.hpp:71-84): one Rng(seed) (mt19937_64) draws the n
+ * tensors in order, volumes[j] elements each, kinds[j] 0 = random_pm1
+ * (U(-1,1) from a 53-bit double), 1 = random_binary (exact {0,1}, p = 1/2).
+ * Only elements [begin[j], begin[j] + count[j]) of tensor j are written to
+ * host_out[j] (row blocks of a batch shard); the draws before them are
+ * skipped. Host memory, one thread per tensor. */
+int bcad_host_random_inputs(uint64_t seed, int dtype, int n, const int64_t* volumes, const int* kinds,
+                            const int64_t* begin, const int64_t* count, void* const* host_out);
+
+/* mix_seed(seed, salt) of proj/src/bench.cpp:31-37. */
+uint64_t bcad_host_mix_seed(uint64_t seed, uint64_t salt);
+
 const char* bcad_host_last_error(void);
 
 #ifdef __cplusplus

@@ -208,6 +208,7 @@ struct Nccl {
     int (*GetUniqueId)(void*) = nullptr;
     int (*CommInitRank)(void**, int, const void*, int) = nullptr;  // id passed by value (128 B)
     int (*CommDestroy)(void*) = nullptr;
+    int (*CommCount)(void*, int*) = nullptr;
     int (*AllReduce)(const void*, void*, size_t, int, int, void*, cudaStream_t) = nullptr;
     int (*GroupStart)() = nullptr;
     int (*GroupEnd)() = nullptr;
@@ -230,6 +231,7 @@ Nccl& nccl() {
         x.GetUniqueId = reinterpret_cast<int (*)(void*)>(dlsym(x.h, "ncclGetUniqueId"));
         x.CommInitRank = reinterpret_cast<int (*)(void**, int, const void*, int)>(dlsym(x.h, "ncclCommInitRank"));
         x.CommDestroy = reinterpret_cast<int (*)(void*)>(dlsym(x.h, "ncclCommDestroy"));
+        x.CommCount = reinterpret_cast<int (*)(void*, int*)>(dlsym(x.h, "ncclCommCount"));
         x.AllReduce = reinterpret_cast<int (*)(const void*, void*, size_t, int, int, void*, cudaStream_t)>(
             dlsym(x.h, "ncclAllReduce"));
         x.GroupStart = reinterpret_cast<int (*)()>(dlsym(x.h, "ncclGroupStart"));
@@ -661,6 +663,14 @@ int bcad_cu_comm_destroy(void* comm) {
     if (!comm) return BCAD_CU_OK;
     const int r = n.CommDestroy(comm);
     if (r) return nccl_fail(r, "ncclCommDestroy");
+    return BCAD_CU_OK;
+}
+
+int bcad_cu_comm_count(void* comm, int* nranks) {
+    Nccl& n = nccl();
+    if (!n.ok || !n.CommCount) return fail(BCAD_CU_ERR_NCCL, "libnccl.so.2 not loadable");
+    const int r = n.CommCount(comm, nranks);
+    if (r) return nccl_fail(r, "ncclCommCount");
     return BCAD_CU_OK;
 }
 

@@ -10,6 +10,7 @@
 #include <span>
 #include <unordered_map>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "bcad/bcad.hpp"
@@ -483,9 +484,52 @@ void cell_grads(int impl, int64_t n, const void* const* dev_in, const void* dev_
     if (peak) *peak = tape.peak_cached_bytes();
 }
 
+// Elements [begin, begin+count) of each tensor of the reference's input
+// stream: ONE Rng(seed) draws the tensors in order (random_cell_inputs,
+// hmlstm.hpp:35-43; random_pm1 / random_binary, tensor.hpp:71-84), one draw
+// per element, so tensor j's block starts after sum(volumes[<j]) + begin_j
+// draws. One thread per tensor.
+template <class Real>
+void random_blocks(uint64_t seed, int n, const int64_t* volumes, const int* kinds, const int64_t* begin,
+                   const int64_t* count, void* const* out) {
+    std::vector<std::thread> th;
+    uint64_t offset = 0;
+    for (int j = 0; j < n; ++j) {
+        if (begin[j] < 0 || count[j] < 0 || begin[j] + count[j] > volumes[j])
+            throw bcad::ConfigError("random block outside tensor " + std::to_string(j));
+        const uint64_t skip = offset + static_cast<uint64_t>(begin[j]);
+        th.emplace_back([=] {
+            bcad::Rng rng(seed);
+            rng.discard(skip);
+            Real* o = static_cast<Real*>(out[j]);
+            if (kinds[j] == 1)
+                for (int64_t e = 0; e < count[j]; ++e) o[e] = static_cast<Real>(rng.binary());
+            else
+                for (int64_t e = 0; e < count[j]; ++e) o[e] = static_cast<Real>(rng.uniform_pm1());
+        });
+        offset += static_cast<uint64_t>(volumes[j]);
+    }
+    for (std::thread& t : th) t.join();
+}
+
 }  // namespace
 
 extern "C" {
+
+int bcad_host_random_inputs(uint64_t seed, int dtype, int n, const int64_t* volumes, const int* kinds,
+                            const int64_t* begin, const int64_t* count, void* const* host_out) {
+    try {
+        if (dtype == BCAD_CU_F32) random_blocks<float>(seed, n, volumes, kinds, begin, count, host_out);
+        else if (dtype == BCAD_CU_F64) random_blocks<double>(seed, n, volumes, kinds, begin, count, host_out);
+        else throw bcad::ConfigError("dtype must be F32 or F64");
+        return BCAD_CU_OK;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return code_of(e);
+    }
+}
+
+uint64_t bcad_host_mix_seed(uint64_t seed, uint64_t salt) { return bcad::mix_seed(seed, salt); }
 
 int bcad_host_cell_gradients(int impl, int dtype, int64_t n, const void* const* dev_in, const void* dev_seed,
                              void* const* dev_grads, int64_t* tape_nodes, int64_t* peak_cached_bytes, void* stream) {

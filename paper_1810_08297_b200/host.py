@@ -95,3 +95,37 @@ def cell_gradients(impl: str, inputs, seed, grads, stream=None) -> tuple[int, in
     if rc:
         raise native._BY_CODE.get(rc, native.Error)(LIB.bcad_host_last_error().decode())
     return int(nodes.value), int(peak.value)
+
+
+LIB.bcad_host_random_inputs.restype = C.c_int
+LIB.bcad_host_random_inputs.argtypes = [C.c_uint64, C.c_int, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p,
+                                        C.c_void_p, C.c_void_p]
+LIB.bcad_host_mix_seed.restype = C.c_uint64
+LIB.bcad_host_mix_seed.argtypes = [C.c_uint64, C.c_uint64]
+
+
+def mix_seed(seed: int, salt: int) -> int:
+    """mix_seed of proj/src/bench.cpp:31-37."""
+    return int(LIB.bcad_host_mix_seed(seed, salt))
+
+
+def random_inputs(seed: int, dtype, specs, blocks=None, out=None):
+    """The reference's input stream (one Rng(seed), tensors drawn in order;
+    rng.hpp:11-31, tensor.hpp:71-84) — bcad_host_random_inputs. specs:
+    (shape, kind) with kind 'pm1' | 'binary'. blocks: per tensor (begin,
+    count) in elements of the FULL tensor (default: all of it); out: host
+    arrays to fill (default: new numpy arrays of `count` elements, flat)."""
+    vols = [int(np.prod(s, dtype=np.int64)) for s, _ in specs]
+    blocks = blocks or [(0, v) for v in vols]
+    if out is None:
+        out = [np.empty(c, dtype=dtype) for _, c in blocks]
+    n = len(specs)
+    code = 0 if np.dtype(dtype) == np.float32 else 1
+    arr = lambda t, xs: (t * n)(*xs)  # noqa: E731
+    rc = LIB.bcad_host_random_inputs(seed, code, n, arr(C.c_int64, vols),
+                                     arr(C.c_int, [1 if k == "binary" else 0 for _, k in specs]),
+                                     arr(C.c_int64, [b for b, _ in blocks]), arr(C.c_int64, [c for _, c in blocks]),
+                                     _ptrs(out))
+    if rc:
+        raise native._BY_CODE.get(rc, native.Error)(LIB.bcad_host_last_error().decode())
+    return out

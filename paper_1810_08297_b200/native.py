@@ -152,6 +152,7 @@ PROTOS = {
     "bcad_cu_nccl_unique_id": (I, [C.c_char_p]),
     "bcad_cu_comm_init": (I, [C.POINTER(VP), I, C.c_char_p, I]),
     "bcad_cu_comm_destroy": (I, [VP]),
+    "bcad_cu_comm_count": (I, [VP, C.POINTER(I)]),
     "bcad_cu_allreduce_adjoints": (I, [VP, VP, I, I, VP, VP]),
 }
 
@@ -325,6 +326,12 @@ class Comm:
     def __init__(self, nranks: int, uid: bytes, rank: int):
         self.handle = VP()
         check(LIB.bcad_cu_comm_init(C.byref(self.handle), nranks, uid, rank))
+
+    @property
+    def nranks(self) -> int:
+        n = C.c_int()
+        check(LIB.bcad_cu_comm_count(self.handle, C.byref(n)))
+        return n.value
 
     def allreduce(self, tensors, stream=None):
         bufs = [t for t in tensors if t is not None]

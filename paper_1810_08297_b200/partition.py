@@ -16,6 +16,12 @@ each argument one of two ways:
 
 The forward needs no exchange at all; the only collective of a step is the
 allreduce of the batch-broadcast adjoints.
+
+A node whose output batch extent is 1 (every argument of axis-0 extent 1, or
+scalars) cannot be split: rank 0 owns all of it and the other ranks hold an
+empty row block (`active` False) and contribute zero adjoints to the
+allreduce, so the summed gradient is the single-process one, not world
+times it.
 """
 from __future__ import annotations
 
@@ -39,6 +45,7 @@ class ShardPlan:
     rows: tuple[int, int]       # this rank's [begin, end)
     sharded: tuple[bool, ...]   # per argument: True = sliced on axis 0
     allreduce: tuple[int, ...]  # arguments whose adjoints are summed across ranks
+    active: bool = True         # False: this rank computes nothing (unsplittable node, rank > 0)
 
     def local_shape(self, shape: Sequence[int], j: int) -> tuple:
         if not self.sharded[j]:
@@ -53,6 +60,8 @@ def plan(shapes: Sequence[Sequence[int]], world: int, rank: int) -> ShardPlan:
             raise ValueError(f"axis-0 extent {s[0]} does not broadcast against batch {batch}")
     sharded = tuple(len(s) > 0 and s[0] == batch and batch > 1 for s in shapes)
     reduce = tuple(j for j, sh in enumerate(sharded) if not sh)
+    if batch == 1:  # nothing to split: rank 0 owns the node, the others add zeros
+        return ShardPlan(batch, (0, 1) if rank == 0 else (0, 0), sharded, reduce, active=rank == 0)
     return ShardPlan(batch, shard_rows(batch, world, rank), sharded, reduce)
 
 

@@ -18,6 +18,8 @@ from __future__ import annotations
 
 from dataclasses import dataclass
 
+from .partition import shard_rows  # noqa: F401  (re-exported)
+
 
 @dataclass(frozen=True)
 class Workload:
@@ -85,11 +87,3 @@ WORKLOADS = {
     "cfg5": Workload("cfg5", 65536, 4096, "f32", "bias",
                      "bias variant fp32 H=4096 B=65536, batch-sharded, NCCL allreduce of (1,H) adjoints (config 5)"),
 }
-
-
-def shard_rows(B: int, world: int, rank: int) -> tuple[int, int]:
-    """Contiguous batch-row block of `rank`: the first B % world
-    ranks get one extra row. Returns [begin, end)."""
-    base, extra = divmod(B, world)
-    begin = rank * base + min(rank, extra)
-    return begin, begin + base + (1 if rank < extra else 0)

@@ -41,3 +41,38 @@ def test_reference_arm_non_zero_ranks_exit_silently():
 def test_warmup_below_three_is_rejected():
     r = run("--impl", "reference", "--steps", "2", "--warmup", "2")
     assert r.returncode != 0
+
+
+def _one_json(r):
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [l for l in r.stdout.splitlines() if l.strip().startswith("{")]
+    assert len(lines) == 1, r.stdout
+    return json.loads(lines[0])
+
+
+def test_gpus_two_spawns_two_ranks():
+    """`bench.py --gpus 2` (the driver's own form, no torchrun environment)
+    re-launches itself with 2 ranks; --dry-run runs the rank plumbing over
+    gloo. N > 1 defaults to config 5: strong scaling, batch rows split,
+    (1,H) bias adjoints allreduced."""
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    d = _one_json(run("--gpus", "2", "--dry-run", env=env))
+    assert d["ranks_seen"] == 2 and d["n_gpus"] == 2 and d["backend"] == "gloo"
+    assert d["scaling"] == "strong" and d["config"]["B"] == 65536 and d["config"]["variant"] == "bias"
+    assert d["rows_per_rank"] == [[0, 32768], [32768, 65536]]
+    assert d["allreduce_args"] == [4, 5, 6]
+
+
+def test_gpus_must_match_launcher_world():
+    env = dict(os.environ, RANK="0", WORLD_SIZE="2", LOCAL_RANK="0")
+    r = run("--gpus", "3", "--dry-run", env=env)
+    assert r.returncode != 0 and "--gpus 3" in r.stderr
+
+
+def test_reference_arm_config_equals_gpu_arm_config():
+    """Both arms print the same `config` object (the driver compares them)."""
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    gpu = _one_json(run("--dry-run", env=env))
+    ref = _one_json(run("--impl", "reference", "--steps", "1", "--warmup", "3", env=env))
+    assert gpu["config"] == ref["config"]
+    assert ref["scaling"] == gpu["scaling"] == "weak"

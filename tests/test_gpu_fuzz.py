@@ -9,7 +9,7 @@ import numpy as np
 import pytest
 
 import oracle as O
-from helpers import GpuRunner, assert_close, assert_grads, tol_for
+from helpers import GpuRunner, assert_close, assert_grads, step_terms, tol_for
 
 pytestmark = pytest.mark.gpu
 
@@ -70,7 +70,8 @@ def test_fuzz_tiled_kernels(gpu, oracle_lib, dtype):
         # accumulate: the device adds into the existing slot
         want_g = [w if e is None else (e.astype(np.float64) + w).astype(dtype) for w, e in zip(want_g, existing)]
         want_a64 = [w if e is None else e.astype(np.float64) + w for w, e in zip(want_a64, existing)]
-        assert_grads(got_g, want_g, want_a64, shapes, out_shape, dtype, tag)
+        assert_grads(got_g, want_g, want_a64, shapes, out_shape, dtype, tag,
+                     terms=step_terms(oracle_lib, gpu, name, ins, seeds))
 
 
 @pytest.mark.parametrize("dtype", [np.float32, np.float64])
@@ -102,4 +103,5 @@ def test_fuzz_generic_rank3(gpu, oracle_lib, dtype):
             assert_close(got_p[i], want_p[i], rtol, atol, tag + f" primal{i}")
         want_g = [w if e is None else (e.astype(np.float64) + w).astype(dtype) for w, e in zip(want_g, existing)]
         want_a64 = [w if e is None else e.astype(np.float64) + w for w, e in zip(want_a64, existing)]
-        assert_grads(got_g, want_g, want_a64, shapes, out_shape, dtype, tag)
+        assert_grads(got_g, want_g, want_a64, shapes, out_shape, dtype, tag,
+                     terms=step_terms(oracle_lib, gpu, name, ins, seeds))

@@ -8,10 +8,13 @@ Tape::backward (tape.hpp:185-211). The device step through the C-ABI must
 reproduce them under SURVEY Appendix A:
   * primals, partials, full-shape gradients: |a-b| <= atol + rtol*max(|a|,|b|)
     (fp32 1e-5/1e-6, fp64 1e-12/1e-14);
-  * reduced gradients: against the fp64 sum of the reference's own rounded
-    terms T(w_i * D_ij) over the broadcast axes, rtol as above, atol scaled by
-    sqrt(terms) (the device accumulates in fp64; the reference's serial fp32
-    sum is itself off by up to ~1e-4 relative at large B);
+  * reduced gradients: against the fp64 sum S of the reference's own rounded
+    terms T(w_i * D_ij) over the broadcast axes: |got - S| <= rtol_red*|S| +
+    sum|t_dev - t_ref| (rtol_red 1e-6 fp32 / 1e-12 fp64; the second term is
+    what the per-cell ulp differences of the partials, already checked
+    elementwise, can move the sum; zero where they are bit-identical). The
+    device accumulates in fp64; the reference's serial fp32 sum is itself
+    off by up to ~1e-4 relative at large B (reported, loose bound);
   * HM-LSTM branch decisions bit-exact (D_c in {0, 1, (0,1)} against the z
     predicate of hmlstm.hpp:51-53).
 """
@@ -21,7 +24,7 @@ import os
 import numpy as np
 import pytest
 
-from helpers import GpuRunner, assert_close, tol_for
+from helpers import GpuRunner, _assert_reduced, abs_terms, assert_close, reduce_to, term_slack, tol_for
 
 pytestmark = pytest.mark.gpu
 
@@ -35,16 +38,6 @@ def load(path):
     ins = [d[f"in{j}"] for j in range(n)]
     seeds = [d[f"seed{i}"] if f"seed{i}" in d.files else None for i in range(m)]
     return str(d["kernel"]), ins, seeds, d, n, m
-
-
-def reduce_to(terms, arg_shape):
-    """Sum an output-shaped array over the axes a first-axis-aligned argument
-    of `arg_shape` is broadcast along (shape.hpp:13-16), keeping its shape."""
-    out_rank = terms.ndim
-    padded = tuple(arg_shape) + (1,) * (out_rank - len(arg_shape))
-    axes = tuple(k for k in range(out_rank) if padded[k] == 1 and terms.shape[k] != 1)
-    s = terms.sum(axis=axes, keepdims=True) if axes else terms
-    return s.reshape(arg_shape)
 
 
 @pytest.fixture(scope="module")
@@ -78,7 +71,10 @@ def test_device_matches_reference_outputs(gpu, path):
             if seeds[i] is not None:  # the reference's rounded terms w_i * D_ij
                 terms += (seeds[i] * d[f"partial{i * n + j}"]).astype(dtype).astype(np.float64)
         want64 = reduce_to(terms, ins[j].shape)
-        assert_close(grads[j], want64, rtol, atol * np.sqrt(cnt), f"{kernel} grad{j} (reduced x{cnt})")
+        ref_parts = [d[f"partial{k}"] for k in range(m * n)]
+        slack = term_slack(seeds, parts, ref_parts, j, n, tuple(ins[j].shape), dtype.type)
+        at = abs_terms(seeds, ref_parts, j, n, tuple(ins[j].shape), dtype.type, out_shape)
+        _assert_reduced(grads[j], want64, dtype.type, slack, f"{kernel} grad{j} (reduced x{cnt})", at)
         # informational bound vs the reference's serial-fp32 sum itself
         assert_close(grads[j], want_serial, 1e-4 if dtype == np.float32 else 1e-10,
                      atol * cnt, f"{kernel} grad{j} vs serial reference")

@@ -10,7 +10,7 @@ import numpy as np
 import pytest
 
 import oracle as O
-from helpers import GpuRunner, assert_close, assert_grads, tol_for
+from helpers import GpuRunner, assert_close, assert_grads, step_terms, tol_for
 
 pytestmark = pytest.mark.gpu
 
@@ -64,7 +64,8 @@ def test_hmlstm_config1(gpu, oracle_lib, dtype, variant, policy):
         want_cls = branch_class_from_z(_z_full(z1, (B, H)), _z_full(z2, (B, H)))
         assert np.array_equal(branch_class_from_dc(got_d[0]), want_cls)
     out_shape = (B, H)
-    assert_grads(got_g, want_g, want_a64, [a.shape for a in ins], out_shape, dtype, f"{variant}")
+    assert_grads(got_g, want_g, want_a64, [a.shape for a in ins], out_shape, dtype, f"{variant}",
+                 terms=step_terms(oracle_lib, gpu, name, ins))
     # COPY primal == c, bit-exact; z gradients exactly zero
     cls = branch_class_from_z(_z_full(ins[-2], out_shape), _z_full(ins[-1], out_shape))
     assert np.array_equal(got_p[0][cls == 1], ins[0][cls == 1])
@@ -80,9 +81,11 @@ def test_hmlstm_bias_1024_multitile(gpu, oracle_lib, dtype):
     rng = np.random.default_rng(5)
     seed = rng.uniform(-1, 1, (B, H)).astype(dtype)
     _, want_g, want_a64 = oracle_lib.mixed_step("hmlstm_update_bias", ins, seeds=[seed])
+    terms = step_terms(oracle_lib, gpu, "hmlstm_update_bias", ins, [seed])
     for policy in (O.CACHE_FORWARD, O.RECOMPUTE_REVERSE):
         _, _, got_g = gpu.step("hmlstm_update_bias", ins, seeds=[seed], policy=policy)
-        assert_grads(got_g, want_g, want_a64, [a.shape for a in ins], (B, H), dtype, f"bias1024 p{policy}")
+        assert_grads(got_g, want_g, want_a64, [a.shape for a in ins], (B, H), dtype, f"bias1024 p{policy}",
+                     terms=terms)
 
 
 def random_shapes(rng, n_args, max_rank=3, max_len=4):
@@ -129,7 +132,8 @@ def test_kernel_pool_random_shapes(gpu, oracle_lib, dtype):
                         assert_close(got_p[i], want_p[i], rtol, atol, tag + f" primal{i}")
                     for k, (g, w) in enumerate(zip(got_d, want_d)):
                         assert_close(g, w, rtol, atol, tag + f" D{k}")
-                assert_grads(got_g, want_g, want_a64, shapes, out_shape, dtype, tag)
+                assert_grads(got_g, want_g, want_a64, shapes, out_shape, dtype, tag,
+                             terms=step_terms(oracle_lib, gpu, name, ins, seeds))
 
 
 @pytest.mark.parametrize("dtype", DTYPES)
@@ -167,7 +171,8 @@ def test_accumulate_into_existing_slots(gpu, oracle_lib, dtype):
     want = [e.copy() if e is not None else np.zeros(a.shape, dtype) for e, a in zip(existing, ins)]
     acc64 = oracle_lib.pullback([a.shape for a in ins], [np.ones((64, 256), dtype)], parts, want,
                                 accumulate=[e is not None for e in existing])
-    assert_grads(got, want, acc64, [a.shape for a in ins], (64, 256), dtype, "accumulate")
+    assert_grads(got, want, acc64, [a.shape for a in ins], (64, 256), dtype, "accumulate",
+                 terms=step_terms(oracle_lib, gpu, "hmlstm_update_bias", ins))
 
 
 @pytest.mark.parametrize("dtype", DTYPES)
@@ -184,7 +189,8 @@ def test_edge_shapes(gpu, oracle_lib, dtype, shape):
     for policy in (0, 1):
         got_p, _, got_g = gpu.step("hmlstm_update_bias", ins, policy=policy)
         assert_close(got_p[0], want_p[0], rtol, atol, f"{shape} primal")
-        assert_grads(got_g, want_g, want_a64, [a.shape for a in ins], (B, H), dtype, f"{shape}")
+        assert_grads(got_g, want_g, want_a64, [a.shape for a in ins], (B, H), dtype, f"{shape}",
+                     terms=step_terms(oracle_lib, gpu, "hmlstm_update_bias", ins))
 
 
 def test_misaligned_views_take_scalar_tiled_path(gpu, oracle_lib):
@@ -222,7 +228,8 @@ def test_misaligned_views_take_scalar_tiled_path(gpu, oracle_lib):
         adj = [off_view(s) for s in shapes]
         native.pullback(k, shapes, [seed], policy_parts, dins, adj, workspace=native.new_workspace(k, shapes, torch.float32))
         torch.cuda.synchronize()
-        assert_grads([a.cpu().numpy() for a in adj], want_g, want_a64, shapes, (B, H), np.float32, "misaligned grads")
+        assert_grads([a.cpu().numpy() for a in adj], want_g, want_a64, shapes, (B, H), np.float32, "misaligned grads",
+                     terms=step_terms(oracle_lib, gpu, "hmlstm_update", ins, [seed.cpu().numpy()]))
 
 
 ERROR_CASES = [
@@ -286,3 +293,37 @@ def test_graph_capture_replays_the_step_bit_exact(oracle_lib):
     native.check(native.LIB.bcad_cu_graph_destroy(exe))
     for a, b in zip(adj_direct, adj_graph):
         assert torch.equal(a, b)
+
+
+ARITIES = [1, 2, 4, 8, 16, 18, 32]
+
+
+@pytest.mark.parametrize("dtype", DTYPES)
+@pytest.mark.parametrize("A", ARITIES)
+def test_tanh_product_arity_vs_oracle(gpu, oracle_lib, dtype, A):
+    """Arity study kernels (arity_workload.hpp:12-28; acceptance.cpp:334-370)
+    against the oracle: every registered arity — including A = 8 (two cells
+    per thread), A >= 16 (one cell per thread) — both policies, at a
+    vectorised width (4096), odd widths (1023, 7: scalar tiled path), with a
+    batch-broadcast (1,H) argument so one adjoint is a cross-row reduction,
+    and inputs straddling reflect_below_half's 0.5 branch point."""
+    rng = np.random.default_rng(1000 + A)
+    rtol, atol = tol_for(dtype)
+    name = f"tanh_product_{A}"
+    for B, H in ((6, 4096), (37, 1023), (5, 7)):
+        shapes = [(B, H)] * A
+        if A > 1:
+            shapes[A // 2] = (1, H)  # one batch-broadcast argument
+        ins = [rng.uniform(-1, 1, s).astype(dtype) for s in shapes]
+        seeds = [rng.uniform(-1, 1, (B, H)).astype(dtype)]
+        want_p, want_d = oracle_lib.forward(name, ins)
+        _, want_g, want_a64 = oracle_lib.mixed_step(name, ins, O.CACHE_FORWARD, seeds)
+        terms = step_terms(oracle_lib, gpu, name, ins, seeds)
+        for policy in (O.CACHE_FORWARD, O.RECOMPUTE_REVERSE):
+            got_p, got_d, got_g = gpu.step(name, ins, seeds=seeds, policy=policy)
+            tag = f"{name} {B}x{H} p{policy}"
+            assert_close(got_p[0], want_p[0], rtol, atol, tag + " primal")
+            if got_d is not None:
+                for j in range(A):
+                    assert_close(got_d[j], want_d[j], rtol, atol, tag + f" D{j}")
+            assert_grads(got_g, want_g, want_a64, shapes, (B, H), dtype, tag, terms=terms)

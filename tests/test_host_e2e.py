@@ -7,7 +7,7 @@ import numpy as np
 import pytest
 
 import oracle as O
-from helpers import assert_close, assert_grads, tol_for
+from helpers import GpuRunner, assert_close, assert_grads, step_terms, tol_for
 
 pytestmark = pytest.mark.gpu
 
@@ -54,7 +54,8 @@ def test_host_step_matches_oracle(host, oracle_lib, dtype, variant, policy):
     got_p, got_g, peak = host_step(host, name, ins, seeds, policy)
     rtol, atol = tol_for(dtype)
     assert_close(got_p[0], want_p[0], rtol, atol, "host primal")
-    assert_grads(got_g, want_g, want_a64, [a.shape for a in ins], (B, H), dtype, "host e2e")
+    assert_grads(got_g, want_g, want_a64, [a.shape for a in ins], (B, H), dtype, "host e2e",
+                 terms=step_terms(oracle_lib, GpuRunner(), name, ins, seeds))
     s = np.dtype(dtype).itemsize
     E, n = B * H, len(ins)
     inputs_bytes = sum(a.size for a in ins) * s
@@ -122,7 +123,8 @@ def test_host_step_pipelined_matches_one_shot(host, oracle_lib, dtype, variant, 
     assert np.array_equal(p1[0], pk[0])
     assert peak1 == peakk
     _, want_g, want_a64 = oracle_lib.mixed_step(name, ins, 0, seeds)
-    assert_grads(gk, want_g, want_a64, [a.shape for a in ins], (B, Hd), dtype, f"pipelined x{chunks}")
+    assert_grads(gk, want_g, want_a64, [a.shape for a in ins], (B, Hd), dtype, f"pipelined x{chunks}",
+                 terms=step_terms(oracle_lib, GpuRunner(), name, ins, seeds), chunks=chunks)
     for j, a in enumerate(ins):
         if a.shape[0] == B:
             assert np.array_equal(g1[j], gk[j]), f"arg {j} differs between one-shot and pipelined"
@@ -158,7 +160,8 @@ def test_host_step_pipelined_scalar_and_two_outputs(host, oracle_lib, dtype):
             assert np.array_equal(a, b)
         assert peak1 == peakk
         _, want_g, want_a64 = oracle_lib.mixed_step("prod_diff", ins, 0, seeds)
-        assert_grads(gk, want_g, want_a64, shapes, out_shape, dtype, f"pipelined prod_diff {shapes}")
+        assert_grads(gk, want_g, want_a64, shapes, out_shape, dtype, f"pipelined prod_diff {shapes}",
+                     terms=step_terms(oracle_lib, GpuRunner(), "prod_diff", ins, seeds), chunks=5)
 
 
 def test_prepared_step_replay_rereads_buffers(oracle_lib):
@@ -195,7 +198,8 @@ def test_prepared_step_replay_rereads_buffers(oracle_lib):
             for a, b in zip(grads, got):
                 assert np.array_equal(a, b)  # prepared == unprepared pipelined step, bit for bit
         _, want_g, want_a64 = oracle_lib.mixed_step(name, ins1, 0, [seed_t.numpy()])
-        assert_grads(results[3], want_g, want_a64, [a.shape for a in ins1], (B, Hd), np.float32, "prepared step")
+        assert_grads(results[3], want_g, want_a64, [a.shape for a in ins1], (B, Hd), np.float32, "prepared step",
+                     terms=step_terms(oracle_lib, GpuRunner(), name, ins1, [seed_t.numpy()]), chunks=4)
         for a, b in zip(results[0], results[1]):
             assert np.array_equal(a, b)
         assert not all(np.array_equal(a, b) for a, b in zip(results[1], results[2]))

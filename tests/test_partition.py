@@ -43,6 +43,18 @@ def test_plan_classifies_batch_broadcast_args():
         P.plan([(64, 32), (5, 32)], 2, 0)
 
 
+def test_unsplittable_node_is_owned_by_rank0():
+    """Output batch extent 1: nothing to split. Rank 0 computes the node, the
+    other ranks are inactive and contribute zeros to the allreduce, so the
+    summed adjoints equal the single-process ones (not world times them)."""
+    shapes = [(1, 32), (1, 32), ()]
+    plans = [P.plan(shapes, 3, r) for r in range(3)]
+    assert [p.active for p in plans] == [True, False, False]
+    assert plans[0].rows == (0, 1) and plans[1].rows == (0, 0)
+    assert plans[0].allreduce == (0, 1, 2)
+    assert all(p.active for p in (P.plan([(4, 2)], 3, r) for r in range(3)))
+
+
 def _free_port():
     with socket.socket() as s:
         s.bind(("127.0.0.1", 0))
