@@ -31,6 +31,41 @@ struct ForwardBroadcastResult {
     DiagJacobian<Real> jacobian;
 };
 
+// The pointwise Jacobian operator (forward.hpp:38-72): one evaluation of
+// the kernel on seeded duals at a single point gives the M primals and the
+// row-major M x N partial matrix. A scalar utility (BroadcastKernel::eval);
+// the broadcast path is broadcast_diag_jacobian below, on the device.
+template <class Real>
+class PointwiseJacobian {
+public:
+    explicit PointwiseJacobian(BroadcastKernel<Real> kernel) : kernel_(std::move(kernel)) {}
+    int arity_in() const { return kernel_.arity_in(); }
+    int arity_out() const { return kernel_.arity_out(); }
+    void operator()(std::span<const Real> x, std::span<Real> primals, std::span<Real> jacobian) const {
+        const int n = kernel_.arity_in(), m = kernel_.arity_out();
+        const Tag tag = fresh_tag();
+        std::array<Dual<Real>, kMaxKernelInputs> in;
+        seed_into<Real>(x, tag, std::span<Dual<Real>>(in.data(), static_cast<std::size_t>(n)));
+        std::array<Dual<Real>, kMaxKernelOutputs> out;
+        kernel_.eval(std::span<const Dual<Real>>(in.data(), static_cast<std::size_t>(n)),
+                     std::span<Dual<Real>>(out.data(), static_cast<std::size_t>(m)));
+        for (int i = 0; i < m; ++i) {
+            primals[static_cast<std::size_t>(i)] = out[static_cast<std::size_t>(i)].primal();
+            for (int j = 0; j < n; ++j)
+                jacobian[static_cast<std::size_t>(i * n + j)] = out[static_cast<std::size_t>(i)].partial_for(tag, j);
+        }
+    }
+    const BroadcastKernel<Real>& kernel() const { return kernel_; }
+
+private:
+    BroadcastKernel<Real> kernel_;
+};
+
+template <class Real>
+PointwiseJacobian<Real> jacobian_operator(const BroadcastKernel<Real>& kernel) {
+    return PointwiseJacobian<Real>(kernel);
+}
+
 namespace detail {
 
 template <class Real>
@@ -118,6 +153,62 @@ ForwardBroadcastResult<Real> broadcast_diag_jacobian(const BroadcastKernel<Real>
                                                      const Ts&... args) {
     const std::array<const Tensor<Real>*, sizeof...(Ts)> ptrs{&args...};
     return broadcast_diag_jacobian<Real>(kernel, std::span<const Tensor<Real>* const>(ptrs), want_primal);
+}
+
+// The reference's serial diagonal path (forward.hpp:162-210), kept because
+// its API has it: one host PointwiseJacobian evaluation per output cell on
+// host copies of the arguments. It is the test-side comparison for
+// broadcast_diag_jacobian, never called by it.
+template <class Real>
+ForwardBroadcastResult<Real> broadcast_diag_jacobian_reference(const BroadcastKernel<Real>& kernel,
+                                                               std::span<const Tensor<Real>* const> args,
+                                                               bool want_primal) {
+    detail::check_arity(kernel, args.size(), "broadcast_diag_jacobian_reference");
+    std::vector<Shape> shapes;
+    std::vector<std::vector<Real>> host;
+    for (const Tensor<Real>* t : args) {
+        shapes.push_back(t->shape());
+        host.push_back(t->to_host());
+    }
+    const Shape out = broadcast_shape(std::span<const Shape>(shapes));
+    const std::int64_t vol = out.volume();
+    const int n = kernel.arity_in(), m = kernel.arity_out();
+    const PointwiseJacobian<Real> op(kernel);
+    std::vector<std::vector<Real>> prim(static_cast<std::size_t>(m), std::vector<Real>(static_cast<std::size_t>(vol)));
+    std::vector<std::vector<Real>> part(static_cast<std::size_t>(m * n), std::vector<Real>(static_cast<std::size_t>(vol)));
+    std::vector<std::int64_t> idx(static_cast<std::size_t>(out.rank()));
+    std::array<Real, kMaxKernelInputs> x;
+    std::array<Real, kMaxKernelOutputs> p;
+    std::array<Real, kMaxKernelInputs * kMaxKernelOutputs> jac;
+    for (std::int64_t c = 0; c < vol; ++c) {
+        unflatten_index(out, c, idx);
+        for (int j = 0; j < n; ++j)
+            x[static_cast<std::size_t>(j)] = host[static_cast<std::size_t>(j)][static_cast<std::size_t>(
+                virtual_index(shapes[static_cast<std::size_t>(j)], idx, out))];
+        op(std::span<const Real>(x.data(), static_cast<std::size_t>(n)), std::span<Real>(p.data(), static_cast<std::size_t>(m)),
+           std::span<Real>(jac.data(), static_cast<std::size_t>(m * n)));
+        for (int i = 0; i < m; ++i) {
+            prim[static_cast<std::size_t>(i)][static_cast<std::size_t>(c)] = p[static_cast<std::size_t>(i)];
+            for (int j = 0; j < n; ++j)
+                part[static_cast<std::size_t>(i * n + j)][static_cast<std::size_t>(c)] = jac[static_cast<std::size_t>(i * n + j)];
+        }
+    }
+    ForwardBroadcastResult<Real> r;
+    r.jacobian.out_shape = out;
+    r.jacobian.outputs = m;
+    r.jacobian.inputs = n;
+    for (auto& v : part) r.jacobian.entries.push_back(Tensor<Real>::from(out, v));
+    if (want_primal)
+        for (auto& v : prim) r.primals.push_back(Tensor<Real>::from(out, v));
+    return r;
+}
+
+template <class Real, class... Ts>
+    requires(std::same_as<std::remove_cvref_t<Ts>, Tensor<Real>> && ...)
+ForwardBroadcastResult<Real> broadcast_diag_jacobian_reference(const BroadcastKernel<Real>& kernel, bool want_primal,
+                                                               const Ts&... args) {
+    const std::array<const Tensor<Real>*, sizeof...(Ts)> ptrs{&args...};
+    return broadcast_diag_jacobian_reference<Real>(kernel, std::span<const Tensor<Real>* const>(ptrs), want_primal);
 }
 
 // The central broadcast-adjoint rule: reduces `contribution` over axes `acc`

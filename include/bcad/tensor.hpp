@@ -158,20 +158,45 @@ public:
         return h;
     }
 
-    // Synchronous single-element read (test convenience, not a hot path).
-    T operator[](std::int64_t flat) const {
-        T v{};
-        check(bcad_cu_memcpy(&v, device_data() + flat, sizeof(T), 1, stream()));
-        check(bcad_cu_stream_synchronize(stream()));
-        return v;
+    // Synchronous single-element access (reference element semantics,
+    // tensor.hpp:40-51; a test / oracle convenience, not a hot path): a read
+    // is one device->host copy, a write one host->device copy, each
+    // synchronised on the tensor's stream.
+    // Writable access (operator[] / at on an lvalue) goes through an
+    // ElementRef; const and temporary tensors return the value, so no
+    // reference can outlive its tensor.
+    T operator[](std::int64_t flat) const& { return read(flat); }
+    T operator[](std::int64_t flat) && { return read(flat); }
+    T at(std::span<const std::int64_t> index) const& { return read(flat_index(index)); }
+    T at(std::span<const std::int64_t> index) && { return read(flat_index(index)); }
+    T at(std::initializer_list<std::int64_t> index) const& {
+        return read(flat_index(std::span<const std::int64_t>(index.begin(), index.size())));
     }
-    T at(std::span<const std::int64_t> index) const {
-        std::int64_t flat = 0;
-        for (int k = 0; k < shape_.rank(); ++k) flat = flat * shape_.dim(k) + index[static_cast<std::size_t>(k)];
-        return (*this)[flat];
+    T at(std::initializer_list<std::int64_t> index) && {
+        return read(flat_index(std::span<const std::int64_t>(index.begin(), index.size())));
     }
-    T at(std::initializer_list<std::int64_t> index) const {
-        return at(std::span<const std::int64_t>(index.begin(), index.size()));
+
+    class ElementRef {
+    public:
+        ElementRef(Tensor* t, std::int64_t flat) : t_(t), flat_(flat) {}
+        operator T() const { return t_->read(flat_); }  // NOLINT: reads like the reference's Real&
+        ElementRef& operator=(T v) {
+            t_->write(flat_, v);
+            return *this;
+        }
+        ElementRef& operator=(const ElementRef& o) { return *this = static_cast<T>(o); }
+        ElementRef& operator+=(T v) { return *this = static_cast<T>(*this) + v; }
+        ElementRef& operator-=(T v) { return *this = static_cast<T>(*this) - v; }
+        ElementRef& operator*=(T v) { return *this = static_cast<T>(*this) * v; }
+
+    private:
+        Tensor* t_;
+        std::int64_t flat_;
+    };
+    ElementRef operator[](std::int64_t flat) & { return ElementRef(this, flat); }
+    ElementRef at(std::span<const std::int64_t> index) & { return ElementRef(this, flat_index(index)); }
+    ElementRef at(std::initializer_list<std::int64_t> index) & {
+        return ElementRef(this, flat_index(std::span<const std::int64_t>(index.begin(), index.size())));
     }
 
     void write_csv(std::ostream& os) const {  // tensor.hpp:53-61
@@ -185,6 +210,22 @@ public:
     }
 
 private:
+    std::int64_t flat_index(std::span<const std::int64_t> index) const {
+        std::int64_t flat = 0;
+        for (int k = 0; k < shape_.rank(); ++k) flat = flat * shape_.dim(k) + index[static_cast<std::size_t>(k)];
+        return flat;
+    }
+    T read(std::int64_t flat) const {
+        T v{};
+        check(bcad_cu_memcpy(&v, device_data() + flat, sizeof(T), 1, stream()));
+        check(bcad_cu_stream_synchronize(stream()));
+        return v;
+    }
+    void write(std::int64_t flat, T v) {
+        check(bcad_cu_memcpy(device_data() + flat, &v, sizeof(T), 0, stream()));
+        check(bcad_cu_stream_synchronize(stream()));
+    }
+
     // device->device through the copy kernel (a launch is cheaper on the host
     // than a cudaMemcpyAsync)
     void copy_in_device(const void* src) {

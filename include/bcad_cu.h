@@ -31,8 +31,13 @@
  * Status codes map one-to-one onto proj/include/bcad/errors.hpp:8-66.
  * Ownership: the caller allocates every buffer (device memory may come from
  * bcad_cu_malloc); the library never retains a pointer after return. The
- * only library-owned device state is one 8-byte error word per device.
- * Thread safety: reentrant per stream.
+ * only library-owned device state is a per-device pool of 8-byte error
+ * words, one taken by each in-flight call of a may-raise kernel.
+ * Thread safety: reentrant; concurrent calls on different streams or host
+ * threads do not share state. A may-raise kernel (bcad_cu_kernel_may_raise)
+ * synchronises its stream after the launch to decode the domain check
+ * (forward.hpp:137-146) and refuses CUDA-graph capture with
+ * BCAD_CU_ERR_CONFIG; every other launch is asynchronous and capturable.
  */
 #ifndef BCAD_CU_H
 #define BCAD_CU_H
@@ -95,6 +100,13 @@ int bcad_cu_kernel_lookup(const char* name, int n_in, int m_out, bcad_cu_kernel*
 int bcad_cu_kernel_arity(bcad_cu_kernel k, int* n_in, int* m_out);
 /* 1 if the kernel's dual rules can raise (log/div/sqrt/abs/pow). */
 int bcad_cu_kernel_may_raise(bcad_cu_kernel k);
+/* Registers a user device body (the entry the BCAD_DEVICE_KERNEL macro of
+ * include/bcad/device_kernel.cuh builds in the user's nvcc translation unit:
+ * forward and pullback launchers instantiated on the user's functor). The
+ * entry must have static lifetime. A name that is already registered is
+ * refused (CONFIG): a second body can never shadow or replace a first one.
+ * Replaces the reference's type-erased body capture, kernel.hpp:26-43. */
+int bcad_cu_register_kernel(const struct bcad_cu_kernel_entry* entry);
 
 /* First-axis broadcast of n shapes (shape.hpp:70-90). */
 int bcad_cu_broadcast_shape(int n, const bcad_cu_shape* shapes, bcad_cu_shape* out);

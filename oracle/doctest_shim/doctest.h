@@ -81,9 +81,44 @@ inline void report(bool ok, const std::string& what, const char* file, int line)
     std::fprintf(stderr, "%s:%d: ERROR: %s\n", file, line, what.c_str());
 }
 
+// doctest's -tce / --test-case-exclude=<filters>: comma-separated names,
+// '*' matching any run of characters.
+inline bool glob_match(const char* p, const char* s) {
+    if (*p == 0) return *s == 0;
+    if (*p == '*') return glob_match(p + 1, s) || (*s && glob_match(p, s + 1));
+    return *s == *p && glob_match(p + 1, s + 1);
+}
+inline std::vector<std::string>& excluded() {
+    static std::vector<std::string> v;
+    return v;
+}
+inline void parse_args(int argc, char** argv) {
+    for (int a = 1; a < argc; ++a) {
+        std::string arg = argv[a];
+        for (const char* pre : {"-tce=", "--test-case-exclude="}) {
+            const std::string p = pre;
+            if (arg.rfind(p, 0) != 0) continue;
+            std::string rest = arg.substr(p.size());
+            size_t pos;
+            while ((pos = rest.find(',')) != std::string::npos) {
+                excluded().push_back(rest.substr(0, pos));
+                rest = rest.substr(pos + 1);
+            }
+            if (!rest.empty()) excluded().push_back(rest);
+        }
+    }
+}
+
 inline int run_all() {
-    int passed = 0, failed = 0;
+    int passed = 0, failed = 0, skipped = 0;
     for (const Case& tc : cases()) {
+        bool skip = false;
+        for (const std::string& f : excluded()) skip = skip || glob_match(f.c_str(), tc.name);
+        if (skip) {
+            ++skipped;
+            std::printf("[doctest-shim] excluded: %s\n", tc.name);
+            continue;
+        }
         counters().case_failed = false;
         try {
             tc.fn();
@@ -100,7 +135,8 @@ inline int run_all() {
             ++passed;
         }
     }
-    std::printf("[doctest-shim] test cases: %d | %d passed | %d failed\n", passed + failed, passed, failed);
+    std::printf("[doctest-shim] test cases: %d | %d passed | %d failed | %d skipped\n", passed + failed, passed, failed,
+                skipped);
     std::printf("[doctest-shim] assertions: %ld | %ld passed | %ld failed\n", counters().checks,
                 counters().checks - counters().failed_checks, counters().failed_checks);
     return failed == 0 ? 0 : 1;
@@ -162,5 +198,8 @@ inline int run_all() {
     } while (0)
 
 #ifdef DOCTEST_CONFIG_IMPLEMENT_WITH_MAIN
-int main() { return ::doctest::detail::run_all(); }
+int main(int argc, char** argv) {
+    ::doctest::detail::parse_args(argc, argv);
+    return ::doctest::detail::run_all();
+}
 #endif

@@ -13,6 +13,7 @@ from __future__ import annotations
 
 import concurrent.futures as cf
 import glob
+import hashlib
 import os
 import shutil
 import subprocess
@@ -43,11 +44,35 @@ def cxx() -> str:
     return "/usr/bin/g++" if os.path.exists("/usr/bin/g++") else "g++"
 
 
-def _newer(target: str, deps: list[str]) -> bool:
-    if not os.path.exists(target):
+def _digest(deps: list[str], cmd: list[str]) -> str:
+    h = hashlib.sha256(" ".join(cmd).encode())
+    for d in sorted(set(deps)):
+        h.update(d.encode())
+        with open(d, "rb") as f:
+            h.update(hashlib.sha256(f.read()).digest())
+    return h.hexdigest()
+
+
+def _stale(target: str, deps: list[str], cmd: list[str]) -> bool:
+    """Content-hash rebuild rule: the target is rebuilt unless its stamp
+    (build/stamps/<target>.stamp) records the SHA-256 of the command and of every
+    dependency's bytes — a stale artefact shipped with a snapshot or a
+    touched-but-unchanged file cannot fool it the way mtimes can."""
+    st = _stamp_path(target)
+    if not os.path.exists(target) or not os.path.exists(st):
         return True
-    t = os.path.getmtime(target)
-    return any(os.path.getmtime(d) > t for d in deps)
+    with open(st) as f:
+        return f.read().strip() != _digest(deps, cmd)
+
+
+def _stamp_path(target: str) -> str:
+    return os.path.join(BUILD, "stamps", os.path.relpath(target, ROOT).replace(os.sep, "__") + ".stamp")
+
+
+def _stamp(target: str, deps: list[str], cmd: list[str]):
+    os.makedirs(os.path.join(BUILD, "stamps"), exist_ok=True)
+    with open(_stamp_path(target), "w") as f:
+        f.write(_digest(deps, cmd) + "\n")
 
 
 def _run(cmd: list[str], verbose: bool):
@@ -69,14 +94,18 @@ def build_cuda(verbose: bool = False, jobs: int | None = None) -> str:
     for src in sources:
         obj = os.path.join(BUILD, os.path.basename(src) + ".o")
         objs.append(obj)
-        if _newer(obj, [src] + headers):
-            todo.append([nvcc(), *NVCC_FLAGS, "-c", src, "-o", obj])
+        cmd = [nvcc(), *NVCC_FLAGS, "-c", src, "-o", obj]
+        if _stale(obj, [src] + headers, cmd):
+            todo.append((obj, [src] + headers, cmd))
     jobs = jobs or max(1, min(len(todo), os.cpu_count() or 4))
     with cf.ThreadPoolExecutor(jobs) as ex:
-        for f in [ex.submit(_run, c, verbose) for c in todo]:
+        for (obj, deps, cmd), f in [(t, ex.submit(_run, t[2], verbose)) for t in todo]:
             f.result()
-    if todo or _newer(LIB, objs):
-        _run([nvcc(), "-shared", *ARCH, "-o", LIB, *objs, "-ldl", "-Xcompiler", "-fPIC"], verbose)
+            _stamp(obj, deps, cmd)
+    link = [nvcc(), "-shared", *ARCH, "-o", LIB, *objs, "-ldl", "-Xcompiler", "-fPIC"]
+    if todo or _stale(LIB, objs, link):
+        _run(link, verbose)
+        _stamp(LIB, objs, link)
     return LIB
 
 
@@ -86,14 +115,18 @@ def build_host(verbose: bool = False) -> str:
     srcs = [os.path.join(CSRC, "host_api.cpp"), os.path.join(CSRC, "bench.cpp")]
     deps = srcs + glob.glob(os.path.join(INCLUDE, "bcad", "*.hpp")) + [os.path.join(INCLUDE, "bcad_cu.h"),
                                                                         os.path.join(INCLUDE, "bcad_host.h"), LIB]
-    if _newer(HOST_LIB, deps):
-        _run([cxx(), "-std=c++20", "-O2", "-fPIC", "-shared", "-Wall", "-Wextra", "-I" + INCLUDE, *srcs,
-              "-o", HOST_LIB, "-L" + PKG, "-lbcad_cu", "-Wl,-rpath,$ORIGIN"], verbose)
+    cmd = [cxx(), "-std=c++20", "-O2", "-fPIC", "-shared", "-Wall", "-Wextra", "-I" + INCLUDE, *srcs,
+           "-o", HOST_LIB, "-L" + PKG, "-lbcad_cu", "-Wl,-rpath,$ORIGIN"]
+    if _stale(HOST_LIB, deps, cmd):
+        _run(cmd, verbose)
+        _stamp(HOST_LIB, deps, cmd)
     main = os.path.join(CSRC, "bench_main.cpp")
-    if _newer(BENCH_EXE, [main, HOST_LIB]):
+    cmd = [cxx(), "-std=c++20", "-O2", "-Wall", "-Wextra", "-I" + INCLUDE, main, "-o", BENCH_EXE, "-L" + PKG,
+           "-lbcad_host", "-lbcad_cu", "-Wl,-rpath,$ORIGIN/.."]
+    if _stale(BENCH_EXE, [main, HOST_LIB], cmd):
         os.makedirs(os.path.dirname(BENCH_EXE), exist_ok=True)
-        _run([cxx(), "-std=c++20", "-O2", "-Wall", "-Wextra", "-I" + INCLUDE, main, "-o", BENCH_EXE, "-L" + PKG,
-              "-lbcad_host", "-lbcad_cu", "-Wl,-rpath,$ORIGIN/.."], verbose)
+        _run(cmd, verbose)
+        _stamp(BENCH_EXE, [main, HOST_LIB], cmd)
     return HOST_LIB
 
 
@@ -105,11 +138,72 @@ def build_cpp_tests(verbose: bool = False) -> list[str]:
         exe = os.path.join(tdir, "bin", os.path.splitext(os.path.basename(src))[0])
         deps = [src] + glob.glob(os.path.join(tdir, "*.hpp")) + glob.glob(os.path.join(INCLUDE, "bcad", "*.hpp")) + \
             [LIB, HOST_LIB]
-        if _newer(exe, deps):
-            _run([cxx(), "-std=c++20", "-O2", "-Wall", "-Wextra", "-I" + INCLUDE, "-I" + tdir, src, "-o", exe,
-                  "-L" + PKG, "-lbcad_host", "-lbcad_cu", "-Wl,-rpath,$ORIGIN/../../../paper_1810_08297_b200"], verbose)
+        cmd = [cxx(), "-std=c++20", "-O2", "-Wall", "-Wextra", "-I" + INCLUDE, "-I" + tdir, src, "-o", exe,
+               "-L" + PKG, "-lbcad_host", "-lbcad_cu", "-Wl,-rpath,$ORIGIN/../../../paper_1810_08297_b200"]
+        if _stale(exe, deps, cmd):
+            _run(cmd, verbose)
+            _stamp(exe, deps, cmd)
         out.append(exe)
+    # nvcc test programs: user device bodies registered through bcad/device_kernel.cuh
+    for src in sorted(glob.glob(os.path.join(tdir, "test_*.cu"))):
+        os.makedirs(os.path.join(tdir, "bin"), exist_ok=True)
+        exe = os.path.join(tdir, "bin", os.path.splitext(os.path.basename(src))[0])
+        deps = [src] + glob.glob(os.path.join(tdir, "*.hpp")) + glob.glob(os.path.join(INCLUDE, "bcad", "*")) + \
+            glob.glob(os.path.join(CSRC, "*.cuh")) + glob.glob(os.path.join(CSRC, "*.hpp")) + [LIB]
+        cmd = [nvcc(), *NVCC_FLAGS, "-I" + tdir, src, "-o", exe, "-L" + PKG, "-lbcad_cu",
+               "-Xlinker", "-rpath,$ORIGIN/../../../paper_1810_08297_b200"]
+        if _stale(exe, deps, cmd):
+            _run(cmd, verbose)
+            _stamp(exe, deps, cmd)
+        out.append(exe)
+    out += build_ref_suites_b200(verbose)
     return out
+
+
+REF_TESTS = "/root/reference/proj/tests"
+REF_SUITES_B200 = os.path.join(ROOT, "tests", "cpp", "bin", "ref_suites_b200")
+# The reference's own doctest suites that exercise the drop-in surface,
+# compiled UNCHANGED against this repo's include/ (not the reference's) with
+# oracle/doctest_shim for the absent doctest.h, linked to libbcad_cu.so: every
+# Tensor lives in HBM and every broadcast runs on the B200. test_broadcast.cpp
+# is not among them: it drives the reference's host-side iteration API
+# (BroadcastPlan / plan_for_each, tensor_zip / tensor_map over arbitrary host
+# lambdas, broadcast_apply_reference), which has no device counterpart here.
+REF_SUITES = ["test_mixed", "test_hmlstm", "test_forward", "test_tape", "test_dual", "test_oracle"]
+
+
+def build_ref_suites_b200(verbose: bool = False) -> list[str]:
+    """Only where /root/reference exists (this container); the binary travels
+    to the GPU box with the snapshot (tests/cpp/bin is git-ignored, not
+    gpurun-ignored)."""
+    if not os.path.isdir(REF_TESTS):
+        return []
+    shim = os.path.join(ROOT, "oracle", "doctest_shim")
+    odir = os.path.join(BUILD, "ref_suites_b200")
+    os.makedirs(odir, exist_ok=True)
+    os.makedirs(os.path.dirname(REF_SUITES_B200), exist_ok=True)
+    hdrs = glob.glob(os.path.join(INCLUDE, "bcad", "*.hpp")) + [os.path.join(INCLUDE, "bcad_cu.h"),
+                                                                 os.path.join(shim, "doctest.h")] + \
+        glob.glob(os.path.join(REF_TESTS, "support", "*.hpp"))
+    flags = [cxx(), "-std=c++20", "-O1", "-w", "-I" + shim, "-I" + INCLUDE, "-I" + REF_TESTS]
+    objs, todo = [], []
+    for t in REF_SUITES + ["doctest_main"]:
+        src = os.path.join(REF_TESTS, t + ".cpp")
+        obj = os.path.join(odir, t + ".o")
+        objs.append(obj)
+        cmd = flags + ["-c", src, "-o", obj]
+        if _stale(obj, [src] + hdrs, cmd):
+            todo.append((obj, [src] + hdrs, cmd))
+    with cf.ThreadPoolExecutor(max(1, min(len(todo), os.cpu_count() or 4))) as ex:
+        for (obj, deps, cmd), f in [(t, ex.submit(_run, t[2], verbose)) for t in todo]:
+            f.result()
+            _stamp(obj, deps, cmd)
+    link = [cxx(), "-o", REF_SUITES_B200, *objs, "-L" + PKG, "-lbcad_cu",
+            "-Wl,-rpath,$ORIGIN/../../../paper_1810_08297_b200"]
+    if todo or _stale(REF_SUITES_B200, objs + [LIB], link):
+        _run(link, verbose)
+        _stamp(REF_SUITES_B200, objs + [LIB], link)
+    return [REF_SUITES_B200]
 
 
 def build_oracle(verbose: bool = False):

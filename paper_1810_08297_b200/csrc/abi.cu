@@ -35,7 +35,12 @@ int cuda_fail(cudaError_t e, const char* what) {
     } while (0)
 
 // ---------------------------------------------------------------- registry
+// The library's bodies (registration groups, one per translation unit) plus
+// bodies registered at load time from users' nvcc translation units
+// (bcad/device_kernel.cuh -> bcad_cu_register_kernel). Entries are never
+// removed, so a handle stays valid for the life of the process.
 struct Registry {
+    std::mutex mu;
     std::vector<const bcad_cu_kernel_entry*> all;
     Registry() {
         int (*groups[])(const bcad_cu_kernel_entry**) = {&bcad_reg_hmlstm, &bcad_reg_pool, &bcad_reg_probe, &bcad_reg_prims,
@@ -48,27 +53,67 @@ struct Registry {
     }
 };
 
-const Registry& registry() {
-    static const Registry r;
+Registry& registry() {
+    static Registry r;
     return r;
 }
 
 // ---------------------------------------------------------- error words
+// A may-raise launch needs a device error word of its own: calls on
+// different streams / threads run concurrently, so each call takes a word
+// from a per-device pool (slabs of 64, grown on demand, never freed) and
+// returns it after decoding. No two in-flight calls share a word.
 constexpr int kMaxDevices = 64;
-std::mutex g_err_mutex;
-unsigned long long* g_err_word[kMaxDevices] = {};
+constexpr int kSlab = 64;
+struct ErrorWordPool {
+    std::mutex mu;
+    std::vector<unsigned long long*> free_words[kMaxDevices];
+};
+ErrorWordPool& word_pool() {
+    static ErrorWordPool p;
+    return p;
+}
 
-int error_word(unsigned long long** out) {
-    int dev = 0;
-    CU_TRY(cudaGetDevice(&dev), "cudaGetDevice");
-    if (dev < 0 || dev >= kMaxDevices) return fail(BCAD_CU_ERR_CUDA, "device ordinal out of range");
-    std::lock_guard<std::mutex> lock(g_err_mutex);
-    if (!g_err_word[dev]) {
-        void* p = nullptr;
-        CU_TRY(cudaMalloc(&p, sizeof(unsigned long long)), "cudaMalloc(error word)");
-        g_err_word[dev] = static_cast<unsigned long long*>(p);
+class ErrorWord {
+public:
+    ErrorWord() = default;
+    ErrorWord(const ErrorWord&) = delete;
+    ErrorWord& operator=(const ErrorWord&) = delete;
+    ~ErrorWord() {
+        if (!word_) return;
+        std::lock_guard<std::mutex> lock(word_pool().mu);
+        word_pool().free_words[dev_].push_back(word_);
     }
-    *out = g_err_word[dev];
+    int acquire() {
+        CU_TRY(cudaGetDevice(&dev_), "cudaGetDevice");
+        if (dev_ < 0 || dev_ >= kMaxDevices) return fail(BCAD_CU_ERR_CUDA, "device ordinal out of range");
+        std::lock_guard<std::mutex> lock(word_pool().mu);
+        auto& fl = word_pool().free_words[dev_];
+        if (fl.empty()) {
+            void* p = nullptr;
+            CU_TRY(cudaMalloc(&p, kSlab * sizeof(unsigned long long)), "cudaMalloc(error words)");
+            for (int i = kSlab - 1; i >= 0; --i) fl.push_back(static_cast<unsigned long long*>(p) + i);
+        }
+        word_ = fl.back();
+        fl.pop_back();
+        return BCAD_CU_OK;
+    }
+    unsigned long long* get() const { return word_; }
+
+private:
+    int dev_ = 0;
+    unsigned long long* word_ = nullptr;
+};
+
+// A may-raise launch decodes its error word synchronously, which a stream
+// under CUDA-graph capture cannot do: refuse explicitly instead.
+int refuse_if_capturing(cudaStream_t s, const char* kernel) {
+    cudaStreamCaptureStatus st = cudaStreamCaptureStatusNone;
+    CU_TRY(cudaStreamIsCapturing(s, &st), "cudaStreamIsCapturing");
+    if (st != cudaStreamCaptureStatusNone)
+        return fail(BCAD_CU_ERR_CONFIG, std::string("kernel ") + kernel +
+                                            " may raise a domain error, which is checked synchronously after the "
+                                            "launch; it cannot be captured into a CUDA graph");
     return BCAD_CU_OK;
 }
 
@@ -261,11 +306,30 @@ int bcad_cu_version(void) { return BCAD_CU_VERSION; }
 
 const char* bcad_cu_last_error(void) { return g_err.c_str(); }
 
-int bcad_cu_kernel_count(void) { return int(registry().all.size()); }
+int bcad_cu_kernel_count(void) {
+    std::lock_guard<std::mutex> lock(registry().mu);
+    return int(registry().all.size());
+}
 
 const char* bcad_cu_kernel_name(int index) {
+    std::lock_guard<std::mutex> lock(registry().mu);
     const auto& all = registry().all;
     return index >= 0 && index < int(all.size()) ? all[size_t(index)]->name : nullptr;
+}
+
+int bcad_cu_register_kernel(const bcad_cu_kernel_entry* entry) {
+    if (!entry || !entry->name || !entry->fwd || !entry->pull) return fail(BCAD_CU_ERR_CONFIG, "incomplete kernel entry");
+    if (entry->n_in < 1 || entry->n_in > BCAD_CU_MAX_INPUTS || entry->m_out < 1 || entry->m_out > BCAD_CU_MAX_OUTPUTS)
+        return fail(BCAD_CU_ERR_ARITY_MISMATCH, std::string("kernel ") + entry->name + ": arity (" +
+                                                    std::to_string(entry->n_in) + " -> " + std::to_string(entry->m_out) +
+                                                    ") outside [1, 32] -> [1, 8]");
+    std::lock_guard<std::mutex> lock(registry().mu);
+    for (const bcad_cu_kernel_entry* e : registry().all)
+        if (std::strcmp(e->name, entry->name) == 0)
+            return fail(BCAD_CU_ERR_CONFIG, std::string("a device body is already registered under the name '") +
+                                                entry->name + "'; registering a second body under it is refused");
+    registry().all.push_back(entry);
+    return BCAD_CU_OK;
 }
 
 int bcad_cu_kernel_lookup(const char* name, int n_in, int m_out, bcad_cu_kernel* out) {
@@ -277,6 +341,7 @@ int bcad_cu_kernel_lookup(const char* name, int n_in, int m_out, bcad_cu_kernel*
     if (m_out < 1 || m_out > BCAD_CU_MAX_OUTPUTS)
         return fail(BCAD_CU_ERR_ARITY_MISMATCH, "kernel output arity " + std::to_string(m_out) + " outside [1, " +
                                                     std::to_string(BCAD_CU_MAX_OUTPUTS) + "]");
+    std::lock_guard<std::mutex> lock(registry().mu);
     for (const bcad_cu_kernel_entry* e : registry().all) {
         if (std::strcmp(e->name, name) != 0) continue;
         if (e->n_in != n_in || e->m_out != m_out)
@@ -324,12 +389,13 @@ int bcad_cu_forward(bcad_cu_kernel k, int dtype, int n_in, const void* const* in
     std::string err;
     if ((rc = make_plan(n_in, in_shapes, &plan, &err))) return fail(rc, err);
     cudaStream_t s = static_cast<cudaStream_t>(stream);
-    unsigned long long* word = nullptr;
+    ErrorWord ew;
     const bool check = k->may_raise && partials_out != nullptr;
     if (check) {
-        if ((rc = error_word(&word))) return rc;
-        CU_TRY(cudaMemsetAsync(word, 0xff, sizeof(*word), s), "cudaMemsetAsync(error word)");
+        if ((rc = refuse_if_capturing(s, k->name)) || (rc = ew.acquire())) return rc;
+        CU_TRY(cudaMemsetAsync(ew.get(), 0xff, sizeof(unsigned long long), s), "cudaMemsetAsync(error word)");
     }
+    unsigned long long* word = ew.get();
     FwdArgs a{dtype, in, primal_out, partials_out, s, word, &plan};
     if ((rc = k->fwd(a, &err))) return fail(rc, err);
     if (check) return check_error_word(word, s, plan);
@@ -391,12 +457,13 @@ int bcad_cu_pullback(bcad_cu_kernel k, int dtype, int n_in, const bcad_cu_shape*
     std::string err;
     if ((rc = make_plan(n_in, in_shapes, &plan, &err))) return fail(rc, err);
     cudaStream_t s = static_cast<cudaStream_t>(stream);
-    unsigned long long* word = nullptr;
+    ErrorWord ew;
     const bool check = k->may_raise && recompute;
     if (check) {
-        if ((rc = error_word(&word))) return rc;
-        CU_TRY(cudaMemsetAsync(word, 0xff, sizeof(*word), s), "cudaMemsetAsync(error word)");
+        if ((rc = refuse_if_capturing(s, k->name)) || (rc = ew.acquire())) return rc;
+        CU_TRY(cudaMemsetAsync(ew.get(), 0xff, sizeof(unsigned long long), s), "cudaMemsetAsync(error word)");
     }
+    unsigned long long* word = ew.get();
     PullArgs a{dtype, out_adj, partials, in, in_adj, accumulate, workspace, workspace_bytes, s, word, &plan};
     if ((rc = k->pull(a, &err))) return fail(rc, err);
     if (check) return check_error_word(word, s, plan);

@@ -244,7 +244,7 @@ std::vector<BenchRecord> run_arity_for(const BenchConfig& cfg) {
         // point, away from the reflect_below_half boundary (x = 0.5)
         std::vector<std::vector<Real>> host_in;
         for (const Tensor<Real>& t : inputs) host_in.push_back(t.to_host());
-        auto body_at = [&](const std::vector<Real>& point) {
+        auto body_at = [&](const std::vector<Real>& point) -> Real {
             std::vector<Tensor<Real>> cell;
             for (Real v : point) cell.push_back(Tensor<Real>::from(Shape{1}, std::vector<Real>{v}));
             std::vector<const Tensor<Real>*> cp;

@@ -26,7 +26,7 @@ inline int cuda_status(cudaError_t e, std::string* err) {
 
 inline int generic_grid(int64_t work) {
     const int64_t blocks = ceil_div(work, kThreads);
-    const int64_t cap = int64_t(kSmCount) * 16;
+    const int64_t cap = int64_t(sm_count()) * 16;
     return int(blocks < 1 ? 1 : (blocks > cap ? cap : blocks));
 }
 

@@ -12,9 +12,12 @@
 #pragma once
 
 #include <algorithm>
+#include <atomic>
 #include <cstdint>
 #include <cstring>
 #include <string>
+
+#include <cuda_runtime.h>
 
 #include "bcad_cu.h"
 
@@ -149,7 +152,27 @@ struct Tiling {
     int prefetch = -1;  // pullback: rows ahead prefetched into L2 (-1 = the launcher's default)
 };
 
-constexpr int kSmCount = 148;
+// SM count of the current device (cached per ordinal; 148 on B200, and the
+// fallback when no device is visible, so host-only workspace queries still
+// answer). Workspace sizes follow the tiling, so a workspace must be queried
+// with the device it will run on current.
+constexpr int kDefaultSmCount = 148;
+inline int sm_count() {
+    static std::atomic<int> cache[64] = {};
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) {
+        (void)cudaGetLastError();
+        return kDefaultSmCount;
+    }
+    int n = cache[dev].load(std::memory_order_relaxed);
+    if (n > 0) return n;
+    if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n < 1) {
+        (void)cudaGetLastError();
+        n = kDefaultSmCount;
+    }
+    cache[dev].store(n, std::memory_order_relaxed);
+    return n;
+}
 constexpr int kCtasPerSm = 4;  // 256-thread CTAs at <= 64 registers per thread
 // RecomputeReverse pullback (duals re-derived in registers): three CTAs per
 // SM (<= 80 registers; the registered HM-LSTM signatures fit without spills).
@@ -193,7 +216,8 @@ inline Tiling choose_tiling(const Plan& p, int V, const ClassMix& mix, bool fine
     const int cap = mix.col ? 32 : 256;
     int txv = 1;
     while (txv < cap && txv < t.vcols) txv <<= 1;
-    const int64_t slots = int64_t(kSmCount) * kCtasPerSm;
+    const int sms = sm_count();
+    const int64_t slots = int64_t(sms) * kCtasPerSm;
     // Column reductions ((1,H) arguments): at least 4 rows per thread, which
     // amortises each CTA's shared-memory setup and combine; small problems
     // also take 16-lane column tiles (64 fp32 columns) and about two CTAs per
@@ -215,7 +239,7 @@ inline Tiling choose_tiling(const Plan& p, int V, const ClassMix& mix, bool fine
     // bias 65536 x 4096 fp32): K1 55 -> 2 rows 0.94 -> 1.02 of the copy peak,
     // K2 55 -> 16 rows 0.94 -> 0.97.
     int64_t rpt = work <= 2 * slots ? ceil_div(work, slots) : (fine ? fine_rows : work / (8 * slots));
-    if (col_small) rpt = ceil_div(work, 2 * kSmCount);
+    if (col_small) rpt = ceil_div(work, 2 * sms);
     else if (mix.col && !fine && rpt < 4) rpt = 4;
     if (rpt < 1) rpt = 1;
     if (!fine && rpt > 16) rpt = 16;

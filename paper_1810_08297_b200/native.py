@@ -119,6 +119,7 @@ PROTOS = {
     "bcad_cu_kernel_lookup": (I, [C.c_char_p, I, I, C.POINTER(VP)]),
     "bcad_cu_kernel_arity": (I, [VP, C.POINTER(I), C.POINTER(I)]),
     "bcad_cu_kernel_may_raise": (I, [VP]),
+    "bcad_cu_register_kernel": (I, [VP]),
     "bcad_cu_broadcast_shape": (I, [I, VP, VP]),
     "bcad_cu_forward": (I, [VP, I, I, VP, VP, I, VP, VP, VP]),
     "bcad_cu_pullback_workspace": (I, [VP, I, I, VP, I, C.POINTER(SZ)]),

@@ -1,0 +1,138 @@
+// User device bodies (include/bcad/device_kernel.cuh) and the body check of
+// the reference-signature BroadcastKernel constructor (include/bcad/kernel.hpp),
+// on the B200. Reference behaviour replaced: proj/include/bcad/kernel.hpp:26-43
+// (any generic lambda becomes a kernel body).
+#include <cmath>
+#include <vector>
+
+#include "bcad/bcad.hpp"
+#include "bcad/device_kernel.cuh"
+#include "mini_test.hpp"
+
+// Two bodies registered from this translation unit at load time.
+BCAD_DEVICE_KERNEL_NOTHROW(UserSoftGate, "user_soft_gate", 2, 1,
+                           out[0] = sigmoid(in[0]) * tanh(in[1]) + in[0] * in[0])
+BCAD_DEVICE_KERNEL(UserLogRatio, "user_log_ratio", 2, 2, out[0] = log(in[0]) / in[1]; out[1] = in[0] * in[1])
+
+namespace {
+// A body under a name the library already has, registered by hand below.
+struct ShadowMul {
+    static constexpr const char* kName = "mul";
+    static constexpr int kIn = 2, kOut = 1;
+    static constexpr bool kMayRaise = false;
+    static constexpr uint32_t kPredicateArgs = ~0u;
+    static constexpr bool kSelectForm = false;
+    template <class S>
+    BCAD_HD static void body(const S* in, S* out) { out[0] = in[0] + in[1]; }
+    template <class S>
+    BCAD_HD static void body_select(const S* in, S* out) { out[0] = in[0] + in[1]; }
+};
+}  // namespace
+
+using namespace bcad;
+
+namespace {
+const auto soft_gate_body = [](auto in, auto out) { out[0] = sigmoid(in[0]) * tanh(in[1]) + in[0] * in[0]; };
+}
+
+TEST_CASE("a user body registered from an nvcc TU runs the mixed step; gradients match host duals") {
+    for (MixedPolicy policy : {MixedPolicy::CacheForward, MixedPolicy::RecomputeReverse}) {
+        const BroadcastKernel<double> k(2, 1, "user_soft_gate", soft_gate_body);
+        Rng rng(5);
+        const std::int64_t B = 37, H = 24;
+        const Tensor<double> x = random_pm1<double>(Shape{B, H}, rng);
+        const Tensor<double> b = random_pm1<double>(Shape{1, H}, rng);
+        const Tensor<double> w = random_pm1<double>(Shape{B, H}, rng);
+        Tape<double> tape;
+        const Var<double> vx = tape.input(x), vb = tape.input(b);
+        const Var<double> vy = mixed_broadcast(tape, k, {vx, vb}, policy)[0];
+        const auto grads = tape.backward(vy, w);
+        const auto hx = x.to_host(), hb = b.to_host(), hw = w.to_host(), hy = tape.value(vy).to_host();
+        const auto gx = grads.at(vx).to_host(), gb = grads.at(vb).to_host();
+        std::vector<double> want_gb(static_cast<std::size_t>(H), 0.0);
+        for (std::int64_t r = 0; r < B; ++r)
+            for (std::int64_t c = 0; c < H; ++c) {
+                const std::size_t e = static_cast<std::size_t>(r * H + c);
+                const Tag tag = fresh_tag();
+                const double pt[2] = {hx[e], hb[static_cast<std::size_t>(c)]};
+                Dual<double> in[2], out[1];
+                seed_into<double>(std::span<const double>(pt, 2), tag, std::span<Dual<double>>(in, 2));
+                k.eval(std::span<const Dual<double>>(in, 2), std::span<Dual<double>>(out, 1));
+                CHECK(mini::close(hy[e], out[0].primal(), 1e-12, 1e-14));
+                CHECK(mini::close(gx[e], hw[e] * out[0].partial_for(tag, 0), 1e-12, 1e-14));
+                want_gb[static_cast<std::size_t>(c)] += hw[e] * out[0].partial_for(tag, 1);
+            }
+        for (std::int64_t c = 0; c < H; ++c)
+            CHECK(mini::close(gb[static_cast<std::size_t>(c)], want_gb[static_cast<std::size_t>(c)], 1e-12, 1e-13));
+    }
+}
+
+TEST_CASE("a lambda under a registered name that computes something else is refused") {
+    CHECK_THROWS_AS((BroadcastKernel<double>(2, 1, "mul", [](auto in, auto out) { out[0] = in[0] + in[1]; })),
+                    ConfigError);
+    CHECK_THROWS_AS((BroadcastKernel<float>(2, 1, "user_soft_gate",
+                                            [](auto in, auto out) { out[0] = sigmoid(in[0]) * tanh(in[1]); })),
+                    ConfigError);
+    // ... a body that differs only on one branch is caught by the exact 0 / 1 probe values
+    CHECK_THROWS_AS((BroadcastKernel<double>(6, 1, "hmlstm_update",
+                                             [](auto in, auto out) {
+                                                 if (in[4] == 0.0 && in[5] == 1.0)
+                                                     out[0] = sigmoid(in[1]) * in[0] + sigmoid(in[2]) * tanh(in[3]);
+                                                 else if (in[4] == 0.0 && in[5] == 0.0)
+                                                     out[0] = in[0];
+                                                 else
+                                                     out[0] = sigmoid(in[2]) * tanh(in[1]);  // FLUSH on the wrong gate
+                                             })),
+                    ConfigError);
+    // the same math under the same names is accepted
+    const BroadcastKernel<double> ok(2, 1, "mul", [](auto in, auto out) { out[0] = in[0] * in[1]; });
+    CHECK(ok.has_host_body());
+    const BroadcastKernel<float> okf(2, 1, "user_soft_gate", soft_gate_body);
+    CHECK(okf.name() == "user_soft_gate");
+}
+
+TEST_CASE("registering a second body under a taken name is refused by the C-ABI") {
+    static const bcad_cu_kernel_entry shadow = BCAD_ENTRY(ShadowMul);
+    CHECK(bcad_cu_register_kernel(&shadow) == BCAD_CU_ERR_CONFIG);
+    CHECK(std::string(bcad_cu_last_error()).find("already registered") != std::string::npos);
+    // "mul" still multiplies
+    const BroadcastKernel<double> k(2, 1, "mul");
+    const double p[2] = {3.0, 4.0};
+    double y = 0;
+    k.eval(std::span<const double>(p, 2), std::span<double>(&y, 1));
+    CHECK(y == 12.0);
+}
+
+TEST_CASE("a device-only kernel evaluates on the device, reals and duals") {
+    const BroadcastKernel<double> dev(2, 1, "user_soft_gate");
+    const BroadcastKernel<double> host(2, 1, "user_soft_gate", soft_gate_body);
+    CHECK(!dev.has_host_body());
+    const double p[2] = {0.3, -0.8};
+    double yd = 0, yh = 0;
+    dev.eval(std::span<const double>(p, 2), std::span<double>(&yd, 1));
+    host.eval(std::span<const double>(p, 2), std::span<double>(&yh, 1));
+    CHECK(mini::close(yd, yh, 1e-14, 0));
+    const Tag tag = fresh_tag();
+    Dual<double> in[2], od[1], oh[1];
+    seed_into<double>(std::span<const double>(p, 2), tag, std::span<Dual<double>>(in, 2));
+    dev.eval(std::span<const Dual<double>>(in, 2), std::span<Dual<double>>(od, 1));
+    host.eval(std::span<const Dual<double>>(in, 2), std::span<Dual<double>>(oh, 1));
+    for (int j = 0; j < 2; ++j) CHECK(mini::close(od[0].partial_for(tag, j), oh[0].partial_for(tag, j), 1e-13, 1e-15));
+}
+
+TEST_CASE("a may-raise user body reports the failing output index") {
+    const BroadcastKernel<double> k(2, 2, "user_log_ratio");
+    CHECK(k.may_raise());
+    const Tensor<double> a = Tensor<double>::from(Shape{2, 2}, {1.0, 2.0, -3.0, 4.0});
+    const Tensor<double> b = Tensor<double>::from(Shape{2, 2}, {1.0, 1.0, 1.0, 1.0});
+    try {
+        (void)broadcast_diag_jacobian(k, false, a, b);
+        CHECK(false);
+    } catch (const DomainError& e) {
+        CHECK(std::string(e.what()).find("(1, 0)") != std::string::npos);
+    }
+    const Tensor<double> z = Tensor<double>::from(Shape{2, 2}, {1.0, 0.0, 1.0, 1.0});
+    CHECK_THROWS_AS((void)broadcast_diag_jacobian(k, false, b, z), DivisionByZero);
+}
+
+int main() { return mini::run_all(); }

@@ -327,3 +327,55 @@ def test_tanh_product_arity_vs_oracle(gpu, oracle_lib, dtype, A):
                 for j in range(A):
                     assert_close(got_d[j], want_d[j], rtol, atol, tag + f" D{j}")
             assert_grads(got_g, want_g, want_a64, shapes, (B, H), dtype, tag, terms=terms)
+
+
+def test_concurrent_may_raise_calls_keep_their_own_status():
+    """Each may-raise call owns its device error word: two host
+    threads on two streams, one failing forward (DivisionByZero at (1)) and
+    one clean forward of the same kernel, repeated; every call reports its
+    own status and index, never the other's."""
+    import threading
+    import torch
+    from paper_1810_08297_b200 import native
+    k = native.Kernel("div")
+    n = 1 << 16
+    a = torch.ones(n, dtype=torch.float64, device="cuda")
+    b_bad = torch.ones(n, dtype=torch.float64, device="cuda")
+    b_bad[1] = 0.0
+    b_ok = torch.full((n,), 2.0, dtype=torch.float64, device="cuda")
+    results = {"bad": [], "ok": []}
+
+    def run(tag, b):
+        s = torch.cuda.Stream()
+        prim = [torch.empty(n, dtype=torch.float64, device="cuda")]
+        parts = [torch.empty(n, dtype=torch.float64, device="cuda") for _ in range(2)]
+        for _ in range(200):
+            try:
+                native.forward(k, [a, b], prim, parts, stream=s)
+                results[tag].append("ok")
+            except native.DivisionByZero as e:
+                results[tag].append(str(e))
+
+    ts = [threading.Thread(target=run, args=("bad", b_bad)), threading.Thread(target=run, args=("ok", b_ok))]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    assert results["ok"] == ["ok"] * 200
+    assert len(results["bad"]) == 200 and all("at output index (1)" in r for r in results["bad"])
+
+
+def test_may_raise_kernel_refuses_graph_capture():
+    """A may-raise forward decodes its error word synchronously, which graph
+    capture cannot do: it returns ConfigError instead of enqueuing."""
+    import torch
+    from paper_1810_08297_b200 import native
+    k = native.Kernel("div")
+    a = torch.ones(64, dtype=torch.float64, device="cuda")
+    prim = [torch.empty(64, dtype=torch.float64, device="cuda")]
+    parts = [torch.empty(64, dtype=torch.float64, device="cuda") for _ in range(2)]
+    s = torch.cuda.Stream()
+    g = torch.cuda.CUDAGraph()
+    with pytest.raises(native.ConfigError, match="cannot be captured"):
+        with torch.cuda.graph(g, stream=s):
+            native.forward(k, [a, a], prim, parts, stream=s)

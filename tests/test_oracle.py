@@ -230,3 +230,7 @@ def test_doctest_shim_reports_failures(tmp_path):
     assert r.returncode == 1
     assert "test cases: 3 | 1 passed | 2 failed" in r.stdout
     assert "assertions: 7 | 3 passed | 4 failed" in r.stdout
+    # doctest's -tce exclusion (names or '*' globs, comma-separated)
+    r = subprocess.run([str(exe), "-tce=bad*"], capture_output=True, text=True)
+    assert r.returncode == 0
+    assert "test cases: 1 | 1 passed | 0 failed | 2 skipped" in r.stdout
