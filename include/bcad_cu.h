@@ -126,14 +126,20 @@ int bcad_cu_forward(bcad_cu_kernel k, int dtype, int n_in, const void* const* in
                     void* const* partials_out, void* stream);
 
 /* Bytes of device workspace bcad_cu_pullback needs for this problem: the
- * fp64 per-tile partials of reductions that span several CTAs (combined by a
- * second, programmatically dependent launch). It needs no initialisation and
- * carries no state between calls; concurrent pullbacks need separate ones. */
+ * fp64 per-tile partials of reductions that span several CTAs, and the
+ * completion tickets with which the last-arriving CTA of each strip combines
+ * them inside the same launch. A workspace must be zero-filled once after
+ * allocation (bcad_cu_pullback_workspace_init); every pullback leaves its
+ * tickets zero again, so it can be reused by any later pullback without
+ * re-initialisation. Concurrent pullbacks need separate workspaces. */
 int bcad_cu_pullback_workspace(bcad_cu_kernel k, int dtype, int n_in, const bcad_cu_shape* in_shapes,
                                int m_out, size_t* bytes);
+/* Zero-fills a freshly allocated workspace (stream-ordered memset). */
+int bcad_cu_pullback_workspace_init(void* workspace, size_t bytes, void* stream);
 
 /* Device kernel launches one bcad_cu_pullback of this problem issues with
- * aligned pointers (1: K2; 2: K2 and its finisher K2f; 0: generic path). */
+ * aligned pointers (1: K2, including any cross-CTA combination; 0: the
+ * generic rank-N path). */
 int bcad_cu_pullback_launches(bcad_cu_kernel k, int dtype, int n_in, const bcad_cu_shape* in_shapes, int m_out,
                               int* launches);
 

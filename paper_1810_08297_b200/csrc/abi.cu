@@ -414,6 +414,13 @@ int bcad_cu_pullback_workspace(bcad_cu_kernel k, int dtype, int n_in, const bcad
     return BCAD_CU_OK;
 }
 
+int bcad_cu_pullback_workspace_init(void* workspace, size_t bytes, void* stream) {
+    if (bytes == 0) return BCAD_CU_OK;
+    if (!workspace) return fail(BCAD_CU_ERR_CONFIG, "null workspace");
+    CU_TRY(cudaMemsetAsync(workspace, 0, bytes, static_cast<cudaStream_t>(stream)), "cudaMemsetAsync(workspace)");
+    return BCAD_CU_OK;
+}
+
 int bcad_cu_pullback_launches(bcad_cu_kernel k, int dtype, int n_in, const bcad_cu_shape* in_shapes, int m_out,
                               int* launches) {
     int rc = arity_check(k, n_in, m_out);

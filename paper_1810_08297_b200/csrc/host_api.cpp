@@ -219,6 +219,7 @@ void prepare_step(StepBuffers<Real>& S, bcad_cu_kernel k, int n_in, const bcad_c
         std::size_t b = 0;
         check(bcad_cu_pullback_workspace(k, dt, n_in, cs.data(), m_out, &b));
         S.ws.emplace_back(r, std::make_unique<detail::DeviceBuffer>(b, comp));
+        check(bcad_cu_pullback_workspace_init(S.ws.back().second->ptr, b, comp));
         S.ws_bytes.push_back(b);
         S.device_bytes += b;
     }

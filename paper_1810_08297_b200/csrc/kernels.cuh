@@ -9,13 +9,14 @@
 //                   for FULL arguments and sum-reduced over broadcast axes
 //                   for ROW (warp shuffles), COL (CTA shared-memory tiles)
 //                   and SCALAR arguments; a reduction spanning several CTAs
-//                   leaves fp64 per-tile partials that K2f combines in fixed
-//                   order. No floating-point atomics; bitwise deterministic
-//                   run to run. With kRecompute the partials are re-derived
+//                   leaves fp64 per-tile partials that the last-arriving CTA
+//                   of each strip / tile combines in fixed order (completion
+//                   tickets in the workspace). No floating-point atomics;
+//                   bitwise deterministic run to run. With kRecompute the partials are re-derived
 //                   from the inputs in the same pass (RecomputeReverse,
 //                   mixed.hpp:75-90) instead of read.
-//   pull_finish K2f the cross-CTA combination, a programmatically dependent
-//                   launch after K2 (only when a reduction spans CTAs).
+//   pull_finish K2f the same combination as a separate dependent launch, for
+//                   callers whose workspace carries no ticket region.
 //   fwd_generic / pull_generic   rank-N fallbacks (3+ irreducible axis
 //                   groups; odd widths and unaligned views run fwd2d /
 //                   pull2d at one cell per thread instead).
@@ -369,12 +370,125 @@ struct Pull2DParams {
     double* ws_row;       // [n_row_args][n_col_tiles][rows]
     double* ws_col;       // [n_col_args][n_row_tiles][cols]
     double* ws_scalar;    // [n_scalar_args][n_ctas]
+    // Completion tickets of the in-kernel combination ([n_col_tiles] column
+    // strips, [n_row_tiles] row tiles, [1] whole grid); null = K2f combines.
+    unsigned int* tickets;
     unsigned long long* err;
 };
 
 template <class T>
 __device__ __forceinline__ T finish(double s, const T* slot_ptr, bool accumulate) {
     return accumulate ? T(double(*slot_ptr) + s) : T(s);
+}
+
+// The cross-CTA combination of one group of up to 32 consecutive reduced
+// elements (items [it0, it_end) of the row or column partials): lane =
+// element, so every load is coalesced across the warp; the 8 warps split the
+// tile partials into 8 contiguous groups whose sums are added in group order.
+// Fixed association: bitwise run-to-run deterministic. Called uniformly by
+// all threads of a CTA (it synchronises). Loads bypass L1 (__ldcg): inside
+// K2 the partials were written by other CTAs of the same grid.
+template <int N, int M, class T>
+__device__ void combine_group(const Pull2DParams<N, M, T>& p, bool is_row, int64_t it0, int64_t it_end, double* part) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t it = it0 + lane, len = is_row ? p.rows : p.cols;
+    const int n = is_row ? p.n_col_tiles : p.n_row_tiles;
+    const bool valid = it < it_end;
+    const int a = valid ? int(it / len) : 0;
+    const int64_t e = valid ? it % len : 0;
+    const double* base = (is_row ? p.ws_row : p.ws_col) + size_t(a) * n * len + e;
+    const int per = (n + 7) / 8, q0 = warp * per, q1 = min(n, q0 + per);
+    double acc = 0.0;
+    if (valid) {
+        int q = q0;
+        for (; q + 8 <= q1; q += 8) {
+            double v[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) v[u] = __ldcg(base + size_t(q + u) * len);
+#pragma unroll
+            for (int u = 0; u < 8; ++u) acc += v[u];
+        }
+        for (; q < q1; ++q) acc += __ldcg(base + size_t(q) * len);
+    }
+    __syncthreads();  // part[] may still be read by a previous group
+    part[warp * 32 + lane] = acc;
+    __syncthreads();
+    if (warp == 0 && valid) {
+        double sum = 0.0;
+#pragma unroll
+        for (int g = 0; g < 8; ++g) sum += part[g * 32 + lane];
+        const int j = is_row ? p.row_j[a] : p.col_j[a];
+        p.adj[j][e] = finish<T>(sum, p.adj[j] + e, (p.acc_mask >> j) & 1u);
+    }
+}
+
+// One scalar argument's combination over all CTAs' partials (strided sums,
+// a fixed-shape tree). Called uniformly by all threads of a CTA.
+template <int N, int M, class T>
+__device__ void combine_scalar(const Pull2DParams<N, M, T>& p, int a, double* part) {
+    const int64_t n_ctas = int64_t(p.n_row_tiles) * p.n_col_tiles;
+    double acc = 0.0;
+    for (int64_t q = threadIdx.x; q < n_ctas; q += kThreads) acc += __ldcg(p.ws_scalar + size_t(a) * n_ctas + q);
+    __syncthreads();
+    part[threadIdx.x] = acc;
+    __syncthreads();
+    for (int stride = kThreads / 2; stride > 0; stride >>= 1) {
+        if (threadIdx.x < stride) part[threadIdx.x] += part[threadIdx.x + stride];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        const int j = p.scal_j[a];
+        p.adj[j][0] = finish<T>(part[0], p.adj[j], (p.acc_mask >> j) & 1u);
+    }
+}
+
+// In-kernel combination of one strip / row tile by its last-arriving CTA:
+// the elements e in [e0, e1) of `count` reduced arguments (row or column
+// partials), each summed over all n tiles in tile order. The CTA's threads
+// work on all elements at once: with few elements, G contiguous tile groups
+// per element (thread = (group, element)), the group sums then added in group
+// order, so the association depends only on the sizes, never on arrival.
+template <int N, int M, class T>
+__device__ void combine_set(const Pull2DParams<N, M, T>& p, bool is_row, int count, int64_t e0, int64_t e1,
+                            double* part) {
+    const int64_t len = is_row ? p.rows : p.cols;
+    const int n = is_row ? p.n_col_tiles : p.n_row_tiles;
+    const int width = int(e1 - e0), n_el = count * width;
+    int w = 1;
+    while (w < n_el && w < kThreads) w <<= 1;
+    const int G = min(kThreads / w, n);  // tile groups per element
+    const int per = (n + G - 1) / G;
+    for (int base = 0; base < n_el; base += w) {
+        const int g = threadIdx.x / w, el = base + int(threadIdx.x % w);
+        const bool valid = g < G && el < n_el;
+        double acc = 0.0;
+        int a = 0;
+        int64_t e = 0;
+        if (valid) {
+            a = el / width;
+            e = e0 + el % width;
+            const double* src = (is_row ? p.ws_row : p.ws_col) + size_t(a) * n * len + e;
+            const int q0 = g * per, q1 = min(n, q0 + per);
+            int q = q0;
+            for (; q + 8 <= q1; q += 8) {
+                double v[8];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) v[u] = __ldcg(src + size_t(q + u) * len);
+#pragma unroll
+                for (int u = 0; u < 8; ++u) acc += v[u];
+            }
+            for (; q < q1; ++q) acc += __ldcg(src + size_t(q) * len);
+        }
+        __syncthreads();
+        if (valid) part[g * w + int(threadIdx.x % w)] = acc;
+        __syncthreads();
+        if (g == 0 && valid) {
+            double sum = 0.0;
+            for (int k = 0; k < G; ++k) sum += part[k * w + int(threadIdx.x % w)];
+            const int j = is_row ? p.row_j[a] : p.col_j[a];
+            p.adj[j][e] = finish<T>(sum, p.adj[j] + e, (p.acc_mask >> j) & 1u);
+        }
+    }
 }
 
 // Shared-memory layout of K2 (dynamic, doubles):
@@ -388,8 +502,14 @@ __host__ __device__ inline size_t pull_smem_doubles(int n_col, int n_row, int n_
 // K2: terms w_i * D_ij rounded to T exactly like backprop_diag's tensor_zip
 // (mixed.hpp:34-38); FULL slots get the reference's element arithmetic,
 // reduced slots an fp64 sum of those terms in a fixed order.
-template <class Body, class T, int V, bool kRecompute, class S, bool kDense>
-__global__ void __launch_bounds__(kThreads, kRecompute ? kRecomputeCtasPerSm : kCtasPerSm) pull2d_kernel(const __grid_constant__ Pull2DParams<Body::kIn, Body::kOut, T> p) {
+//
+// kPipe (small grids, at most two CTAs per SM): the next row's streams are
+// loaded into registers before the current row is reduced, so every thread
+// keeps two rows of loads in flight (as K1 does); up to 128 registers, which
+// costs no occupancy when the grid cannot fill more than two CTAs per SM.
+// Reduction order is unchanged, so results are bit-identical to kPipe=false.
+template <class Body, class T, int V, bool kRecompute, class S, bool kDense, bool kPipe = false>
+__global__ void __launch_bounds__(kThreads, kPipe ? 2 : (kRecompute ? kRecomputeCtasPerSm : kCtasPerSm)) pull2d_kernel(const __grid_constant__ Pull2DParams<Body::kIn, Body::kOut, T> p) {
     constexpr int N = Body::kIn, M = Body::kOut;
     constexpr bool kAnyRow = !S::kStatic || S::has(kRow);
     constexpr bool kAnyCol = !S::kStatic || S::has(kCol);
@@ -494,6 +614,9 @@ __global__ void __launch_bounds__(kThreads, kRecompute ? kRecomputeCtasPerSm : k
     // (per-cell branch) recompute has no registers to spare for them either.
     constexpr bool kPrefetch = kRecompute && S::kStatic && !(Body::kSelectForm && !vec_eval_ok<Body, S>());
     const int64_t r0 = int64_t(rt) * p.tile_rows + ty;
+    Pack<T, V> wn[kPipe ? M : 1], qn[kPipe ? kStreams : 1];
+    if constexpr (kPipe)
+        if (active && r0 < p.rows) load_row(r0, wn, qn);
     // Every lane runs the same rpt iterations (rows past the end are masked),
     // so the ROW shuffles always see complete lane groups.
     for (int k = 0; k < p.rpt; ++k) {
@@ -501,7 +624,16 @@ __global__ void __launch_bounds__(kThreads, kRecompute ? kRecomputeCtasPerSm : k
         const bool live = active && r < p.rows;
 
         Pack<T, V> w[M], q[kStreams];
-        if (live) load_row(r, w, q);
+        if constexpr (kPipe) {
+#pragma unroll
+            for (int i = 0; i < M; ++i) w[i] = wn[i];
+#pragma unroll
+            for (int t = 0; t < kStreams; ++t) q[t] = qn[t];
+            const int64_t rn = r + p.ty;
+            if (active && k + 1 < p.rpt && rn < p.rows) load_row(rn, wn, qn);
+        } else {
+            if (live) load_row(r, w, q);
+        }
         if (kPrefetch && k == 0 && active)  // behind the first row's loads
             for (int kk = 1; kk <= p.prefetch && kk < p.rpt; ++kk)
                 if (r0 + int64_t(kk) * p.ty < p.rows) prefetch_row(r0 + int64_t(kk) * p.ty);
@@ -623,72 +755,65 @@ __global__ void __launch_bounds__(kThreads, kRecompute ? kRecomputeCtasPerSm : k
                 }
             }
         }
+        // ---- cross-CTA combination inside K2 (distributed completion
+        // tickets): the last CTA of each column strip combines the strip's
+        // column partials over all row tiles, the last CTA of each row tile
+        // the tile's row partials over all column tiles, the last CTA of the
+        // grid the scalar partials; each resets its ticket to zero for the
+        // next pullback on this workspace. Writers publish with a fence
+        // before their ticket; the summation order is fixed by tile index,
+        // not by arrival, so results are bitwise deterministic.
+        if (p.tickets) {
+            __shared__ unsigned int s_last[3];
+            __shared__ double part[kThreads];
+            const bool col_x = kAnyCol && p.n_row_tiles > 1 && p.n_col_args > 0;
+            const bool row_x = kAnyRow && p.n_col_tiles > 1 && p.n_row_args > 0;
+            const bool scal_x = kAnyScal && n_ctas > 1 && p.n_scalar_args > 0;
+            __syncthreads();  // every partial of this CTA is written
+            if (tid == 0) {
+                __threadfence();
+                s_last[0] = col_x && atomicAdd(p.tickets + ct, 1u) == unsigned(p.n_row_tiles - 1);
+                s_last[1] = row_x && atomicAdd(p.tickets + p.n_col_tiles + rt, 1u) == unsigned(p.n_col_tiles - 1);
+                s_last[2] = scal_x && atomicAdd(p.tickets + p.n_col_tiles + p.n_row_tiles, 1u) == unsigned(n_ctas - 1);
+                if (s_last[0] | s_last[1] | s_last[2]) __threadfence();
+            }
+            __syncthreads();
+            if (s_last[0]) {
+                const int64_t c0 = int64_t(ct) * ccols;
+                combine_set(p, false, p.n_col_args, c0, min(p.cols, c0 + ccols), part);
+                if (tid == 0) p.tickets[ct] = 0u;
+            }
+            if (s_last[1]) {
+                const int64_t r0t = int64_t(rt) * p.tile_rows;
+                combine_set(p, true, p.n_row_args, r0t, min(p.rows, r0t + p.tile_rows), part);
+                if (tid == 0) p.tickets[p.n_col_tiles + rt] = 0u;
+            }
+            if (s_last[2]) {
+                for (int a = 0; a < p.n_scalar_args; ++a) combine_scalar(p, a, part);
+                if (tid == 0) p.tickets[p.n_col_tiles + p.n_row_tiles] = 0u;
+            }
+        }
     }
 }
 
-// K2f: the cross-CTA combination of K2's fp64 tile partials as a separate,
-// programmatically dependent launch (it waits for K2's grid, so no fences or
-// tickets in K2 itself). A CTA owns 32 consecutive reduced output elements
-// (lane = element, so every load is coalesced across the warp); its 8 warps
-// split the tile partials into 8 contiguous groups, and the group sums are
-// added in group order. Scalar arguments get one CTA each (strided sums, a
-// fixed-shape tree). Fixed association: bitwise run-to-run deterministic.
+// K2f: the same cross-CTA combination as a separate, programmatically
+// dependent launch (it waits for K2's grid, so K2 needs no tickets): one CTA
+// per group of 32 reduced elements, one per scalar argument. Used when the
+// caller's workspace has no ticket region (pull_layout, tickets = false).
 template <int N, int M, class T>
 __global__ void __launch_bounds__(kThreads) pull_finish_kernel(const __grid_constant__ Pull2DParams<N, M, T> p) {
     pdl_wait();
     __shared__ double part[kThreads];
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int64_t n_ctas = int64_t(p.n_row_tiles) * p.n_col_tiles;
     const int64_t row_items = p.n_col_tiles > 1 ? int64_t(p.n_row_args) * p.rows : 0;
     const int64_t col_items = p.n_row_tiles > 1 ? int64_t(p.n_col_args) * p.cols : 0;
     const int64_t row_blocks = (row_items + 31) / 32, col_blocks = (col_items + 31) / 32;
     const int64_t b = blockIdx.x;
-    if (b >= row_blocks + col_blocks) {  // one scalar argument
-        const int a = int(b - row_blocks - col_blocks);
-        double acc = 0.0;
-        for (int64_t q = threadIdx.x; q < n_ctas; q += kThreads) acc += p.ws_scalar[size_t(a) * n_ctas + q];
-        part[threadIdx.x] = acc;
-        __syncthreads();
-        for (int stride = kThreads / 2; stride > 0; stride >>= 1) {
-            if (threadIdx.x < stride) part[threadIdx.x] += part[threadIdx.x + stride];
-            __syncthreads();
-        }
-        if (threadIdx.x == 0) {
-            const int j = p.scal_j[a];
-            p.adj[j][0] = finish<T>(part[0], p.adj[j], (p.acc_mask >> j) & 1u);
-        }
+    if (b >= row_blocks + col_blocks) {
+        combine_scalar(p, int(b - row_blocks - col_blocks), part);
         return;
     }
     const bool is_row = b < row_blocks;
-    const int64_t it = (is_row ? b : b - row_blocks) * 32 + lane;
-    const int64_t items = is_row ? row_items : col_items, len = is_row ? p.rows : p.cols;
-    const int n = is_row ? p.n_col_tiles : p.n_row_tiles;
-    const bool valid = it < items;
-    const int a = valid ? int(it / len) : 0;
-    const int64_t e = valid ? it % len : 0;
-    const double* base = (is_row ? p.ws_row : p.ws_col) + size_t(a) * n * len + e;
-    const int per = (n + 7) / 8, q0 = warp * per, q1 = min(n, q0 + per);
-    double acc = 0.0;
-    if (valid) {
-        int q = q0;
-        for (; q + 8 <= q1; q += 8) {
-            double v[8];
-#pragma unroll
-            for (int u = 0; u < 8; ++u) v[u] = base[size_t(q + u) * len];
-#pragma unroll
-            for (int u = 0; u < 8; ++u) acc += v[u];
-        }
-        for (; q < q1; ++q) acc += base[size_t(q) * len];
-    }
-    part[warp * 32 + lane] = acc;
-    __syncthreads();
-    if (warp == 0 && valid) {
-        double s = 0.0;
-#pragma unroll
-        for (int g = 0; g < 8; ++g) s += part[g * 32 + lane];
-        const int j = is_row ? p.row_j[a] : p.col_j[a];
-        p.adj[j][e] = finish<T>(s, p.adj[j] + e, (p.acc_mask >> j) & 1u);
-    }
+    combine_group(p, is_row, (is_row ? b : b - row_blocks) * 32, is_row ? row_items : col_items, part);
 }
 
 // Blocks of pull_finish_kernel for a tiling (0 = nothing to combine).

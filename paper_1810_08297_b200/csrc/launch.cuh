@@ -194,6 +194,14 @@ inline int pull_prefetch_rows(bool recompute, const Tiling& t) {
     return recompute && t.rpt >= 3 ? 1 : 0;
 }
 
+// Register double buffer of the pullback (kPipe): on small grids whose CTAs
+// cannot fill more than two per SM, where the launch is latency-bound, and
+// only with at least two rows per thread to overlap.
+inline bool pull_pipe(const Tiling& t) {
+    if (t.pipe >= 0) return t.pipe > 0;
+    return t.rpt >= 2 && t.n_ctas <= 2 * int64_t(sm_count());
+}
+
 // The tiled 2-D pullback at VV cells per thread (VV = the 128-bit width, or
 // 1 for widths / pointers that do not allow vectors) with signature
 // dispatch over Sigs (none: runtime classes only).
@@ -243,17 +251,27 @@ int launch_pull2d(const PullArgs& a, std::string* err) {
     p.ws_col = reinterpret_cast<double*>(ws + L.ws_col);
     p.ws_scalar = reinterpret_cast<double*>(ws + L.ws_scalar);
     p.err = a.err;
-    const int64_t fin_blocks = bcad_dev::pull_finish_blocks(plan.rows, plan.cols, p.n_row_tiles, p.n_col_tiles, nr, nc, ns);
+    int64_t fin_blocks = bcad_dev::pull_finish_blocks(plan.rows, plan.cols, p.n_row_tiles, p.n_col_tiles, nr, nc, ns);
+    // cross-CTA reductions combined inside K2 (completion tickets) unless the
+    // tiling asks for the separate K2f launch
+    if (fin_blocks > 0 && pull_combine_in_kernel(t, nr, nc, ns)) {
+        p.tickets = reinterpret_cast<unsigned int*>(ws + L.ws_tickets);
+        fin_blocks = 0;
+    }
     const size_t smem = pull_smem_bytes(nc, nr, ns, t);
     const dim3 grid(unsigned(t.n_col_tiles), unsigned(t.n_row_tiles));
     bool dense = p.acc_mask == 0;  // every w and adjoint present, nothing accumulated
     for (int i = 0; i < M; ++i) dense = dense && p.w[i];
     for (int j = 0; j < N; ++j) dense = dense && p.adj[j];
+    const bool pipe = pull_pipe(t);
     return with_sig<Sigs...>(plan, [&](auto sig) {
         using S = decltype(sig);
         void (*kern)(bcad_dev::Pull2DParams<N, M, T>);
         if constexpr (S::kStatic) {
-            if (dense) kern = recompute ? &bcad_dev::pull2d_kernel<Body, T, VV, true, S, true> : &bcad_dev::pull2d_kernel<Body, T, VV, false, S, true>;
+            if (dense && pipe)
+                kern = recompute ? &bcad_dev::pull2d_kernel<Body, T, VV, true, S, true, true>
+                                 : &bcad_dev::pull2d_kernel<Body, T, VV, false, S, true, true>;
+            else if (dense) kern = recompute ? &bcad_dev::pull2d_kernel<Body, T, VV, true, S, true> : &bcad_dev::pull2d_kernel<Body, T, VV, false, S, true>;
             else kern = recompute ? &bcad_dev::pull2d_kernel<Body, T, VV, true, S, false> : &bcad_dev::pull2d_kernel<Body, T, VV, false, S, false>;
         } else {
             kern = recompute ? &bcad_dev::pull2d_kernel<Body, T, VV, true, S, false> : &bcad_dev::pull2d_kernel<Body, T, VV, false, S, false>;
@@ -263,7 +281,7 @@ int launch_pull2d(const PullArgs& a, std::string* err) {
             if (e != cudaSuccess) return cuda_status(e, err);
         }
         int rc = cuda_status(launch_pdl(kern, grid, smem, a.stream, p), err);
-        if (rc || fin_blocks == 0) return rc;
+        if (rc || fin_blocks == 0 || t.skip_finish) return rc;
         return cuda_status(launch_pdl(&bcad_dev::pull_finish_kernel<N, M, T>, dim3(unsigned(fin_blocks)), 0,
                                       a.stream, p), err);
     });

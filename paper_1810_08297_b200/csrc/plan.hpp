@@ -150,6 +150,9 @@ struct Tiling {
     int64_t tile_rows = 8;
     int64_t n_row_tiles = 1, n_col_tiles = 1, n_ctas = 1;
     int prefetch = -1;  // pullback: rows ahead prefetched into L2 (-1 = the launcher's default)
+    int pipe = -1;      // pullback: next row loaded into registers (kPipe; -1 = the launcher's default)
+    bool skip_finish = false;  // lab timing only: omit K2f (reduced adjoints left incomplete)
+    int combine = -1;   // cross-CTA reductions: -1 / 1 in K2 (tickets), 0 the separate K2f launch
 };
 
 // SM count of the current device (cached per ordinal; 148 on B200, and the
@@ -254,14 +257,16 @@ inline Tiling choose_tiling(const Plan& p, int V, const ClassMix& mix, bool fine
     return t;
 }
 
-// Workspace (global, fp64 tile partials read by the finisher K2f) and
-// dynamic shared memory of the 2-D pullback. Offsets are sized for every
-// argument of a class, so a workspace queried once serves any subset of
-// wanted adjoints. Every partial is written before it is read: no
-// initialisation and no state carried between pullbacks.
+// Workspace (global: fp64 tile partials of reductions that span CTAs, then
+// the completion tickets of their in-kernel combination) and dynamic shared
+// memory of the 2-D pullback. Offsets are sized for every argument of a
+// class, so a workspace queried once serves any subset of wanted adjoints.
+// Every partial is written before it is read; the tickets must be zero before
+// the first pullback (bcad_cu_pullback_workspace_init zero-fills the
+// workspace) and every pullback leaves them zero again.
 struct PullLayout {
     int n_row_args = 0, n_col_args = 0, n_scalar_args = 0;
-    size_t ws_row = 0, ws_col = 0, ws_scalar = 0, total = 0;
+    size_t ws_row = 0, ws_col = 0, ws_scalar = 0, ws_tickets = 0, n_tickets = 0, total = 0;
     size_t smem = 0;
 };
 
@@ -286,6 +291,11 @@ inline PullLayout pull_layout(const Plan& p, const Tiling& t) {
     if (t.n_row_tiles > 1) off += align256(size_t(L.n_col_args) * t.n_row_tiles * p.cols * 8);
     L.ws_scalar = off;
     if (t.n_ctas > 1) off += align256(size_t(L.n_scalar_args) * t.n_ctas * 8);
+    L.ws_tickets = off;
+    if (off > 0) {  // some reduction spans CTAs
+        L.n_tickets = size_t(t.n_col_tiles + t.n_row_tiles + 1);
+        off += align256(L.n_tickets * 4);
+    }
     L.total = off;
     L.smem = pull_smem_bytes(L.n_col_args, L.n_row_args, L.n_scalar_args, t);
     return L;
@@ -322,9 +332,24 @@ size_t pull_ws_t(const Plan& plan) {
     return ws;
 }
 
+// Where the cross-CTA reductions are combined: by default in the finisher
+// launch K2f (programmatically dependent: its CTAs are scheduled while K2
+// drains); with Tiling::combine = 1 inside K2 by the last-arriving CTA of
+// each strip / row tile (completion tickets). Measured at config 3
+// (scripts/lab step3, profiles/r02/lab_step3_combine.jsonl): step 29.7 us
+// with K2f, 31.7 us with tickets (every CTA pays a fence and two ticket
+// atomics at its end, and the last CTA's combine sits on the tail), 26.6 us
+// with no combination at all — so K2f stays the default and tickets an option.
+inline bool pull_combine_in_kernel(const Tiling& t, int nr, int nc, int ns) {
+    (void)nr;
+    (void)nc;
+    (void)ns;
+    return t.combine > 0;
+}
+
 // Kernel launches of one pullback on the tiled path with aligned pointers:
-// K2, plus the finisher K2f when a reduction spans CTAs (mirrors
-// bcad_dev::pull_finish_blocks). 0 when the problem takes the generic path.
+// K2, plus the finisher K2f when a reduction spans CTAs and is not combined
+// inside K2 (mirrors launch_pull2d). 0 when the problem takes the generic path.
 template <class T>
 int pull_launches_t(const Plan& plan) {
     int V = vec_width<T>();
@@ -340,7 +365,7 @@ int pull_launches_t(const Plan& plan) {
         ns += plan.cls[j] == kScalar;
     }
     const bool fin = (t.n_col_tiles > 1 && nr > 0) || (t.n_row_tiles > 1 && nc > 0) || (t.n_ctas > 1 && ns > 0);
-    return fin ? 2 : 1;
+    return fin && !pull_combine_in_kernel(t, nr, nc, ns) ? 2 : 1;
 }
 
 }  // namespace bcad_cu_impl

@@ -123,6 +123,7 @@ PROTOS = {
     "bcad_cu_broadcast_shape": (I, [I, VP, VP]),
     "bcad_cu_forward": (I, [VP, I, I, VP, VP, I, VP, VP, VP]),
     "bcad_cu_pullback_workspace": (I, [VP, I, I, VP, I, C.POINTER(SZ)]),
+    "bcad_cu_pullback_workspace_init": (I, [VP, SZ, VP]),
     "bcad_cu_pullback_launches": (I, [VP, I, I, VP, I, C.POINTER(I)]),
     "bcad_cu_pullback": (I, [VP, I, I, VP, I, VP, VP, VP, VP, VP, VP, SZ, VP]),
     "bcad_cu_scatter_add": (I, [I, VP, VP, VP, VP, I, VP]),
@@ -306,8 +307,9 @@ def pullback_launches(kernel: Kernel, shapes, dtype_code: int) -> int:
 
 
 def new_workspace(kernel: Kernel, shapes, dtype, device="cuda"):
-    """Workspace of the size bcad_cu_pullback_workspace reports (zero-filled,
-    though the kernels need no initialisation)."""
+    """Workspace of the size bcad_cu_pullback_workspace reports, zero-filled
+    as the C-ABI requires before its first pullback (its completion tickets;
+    every pullback leaves them zero again)."""
     import torch
     code = F32 if dtype == torch.float32 else F64
     nbytes = pullback_workspace(kernel, shapes, code)

@@ -108,10 +108,11 @@ struct Flush {
 
 static Flush* g_flush;
 static bool g_recompute = false;  // pull(): RecomputeReverse (partials re-derived) instead of cached
-static bool g_primal_only = false;  // fwd(): primal only (K1p, broadcast_apply)
+static bool g_primal_only = false;
+static bool g_skip_finish_variants = false;  // step_ab: also time every variant without K2f  // fwd(): primal only (K1p, broadcast_apply)
 static cudaStream_t g_s;
 
-double time_us(const std::function<void()>& fn, int reps = 25) {
+double time_us(const std::function<void()>& fn, int reps = 61) {
     std::vector<cudaEvent_t> a(reps), b(reps);
     for (int k = 0; k < reps; ++k) {
         CK(cudaEventCreate(&a[k]));
@@ -136,8 +137,17 @@ double time_us(const std::function<void()>& fn, int reps = 25) {
         cudaEventDestroy(a[k]);
         cudaEventDestroy(b[k]);
     }
+    // CUDA event timestamps on this GPU advance in 2.048 us steps (every
+    // median of a short kernel lands on a multiple); the flush before each
+    // launch randomises the phase, so the MEAN of the quantised samples is an
+    // unbiased estimate (outliers above 2x the median dropped).
     std::sort(t.begin(), t.end());
-    return t[reps / 2];
+    const double med = t[reps / 2];
+    double s = 0;
+    int n = 0;
+    for (double v : t)
+        if (v <= 2 * med) { s += v; ++n; }
+    return s / n;
 }
 
 template <class T>
@@ -440,7 +450,9 @@ void k2_check(const char* tag, bool bias, int64_t B, int64_t H, const std::vecto
     for (auto [txv, rpt] : all) {
         Tiling t = txv == 0 ? choose_tiling(P.plan, V, class_mix(P.plan)) : make_tiling(P.plan, V, txv, rpt, 1);
         if (t.n_row_tiles > 65535) continue;
-        CK(cudaMemset(P.ws, 0xff, P.ws_bytes));
+        CK(cudaMemset(P.ws, 0xff, P.ws_bytes));  // partials poisoned; tickets zero as the C-ABI requires
+        const PullLayout L = pull_layout(P.plan, t);
+        if (L.n_tickets) CK(cudaMemset(static_cast<char*>(P.ws) + L.ws_tickets, 0, L.n_tickets * 4));
         pull<Body, T, Sig>(P, &t);
         const auto got = snapshot(P.adj, ns);
         CK(cudaMemset(P.ws, 0x00, P.ws_bytes));
@@ -494,6 +506,72 @@ void k2_prefetch(const char* tag, bool bias, int64_t B, int64_t H) {
     g_recompute = false;
 }
 
+// Whole step (K1 -> K2 [-> K2f], stream launches after an L2 flush) under
+// pullback variants: the launcher default, kPipe forced off / on, and given
+// (txv, rpt) tilings with and without kPipe. Outputs checked against the
+// default's (full-shape adjoints bit-exact; reduced ones bit-exact too when
+// the tiling is the default's, else 1e-5 relative).
+template <class Body, class T, class Sig>
+void step_ab(const char* tag, bool bias, int64_t B, int64_t H, const std::vector<std::array<int, 2>>& tilings) {
+    Problem<T> P(bias, B, H);
+    constexpr int V = vec_width<T>();
+    const Tiling def = choose_tiling(P.plan, V, class_mix(P.plan));
+    fwd<Body, T, Sig>(P, nullptr);
+    pull<Body, T, Sig>(P, &def);
+    std::vector<size_t> ns;
+    for (auto& s : P.shapes) ns.push_back(size_t(Problem<T>::vol(s)));
+    const auto ref = snapshot(P.adj, ns);
+    std::vector<std::pair<std::string, Tiling>> vars;
+    vars.push_back({"default", def});
+    for (int pipe : {0, 1}) {
+        Tiling t = def;
+        t.pipe = pipe;
+        vars.push_back({pipe ? "default_pipe" : "default_nopipe", t});
+    }
+    for (auto [txv, rpt] : tilings)
+        for (int pipe : {0, 1}) {
+            Tiling t = make_tiling(P.plan, V, txv, rpt, 1);
+            t.pipe = pipe;
+            vars.push_back({pipe ? "tiled_pipe" : "tiled_nopipe", t});
+        }
+    if (g_skip_finish_variants)
+        for (size_t k = 0, n = vars.size(); k < n; ++k) {
+            Tiling t = vars[k].second;
+            t.combine = 0;  // the separate K2f launch instead of in-kernel tickets
+            vars.push_back({vars[k].first + "_k2f", t});
+            t.skip_finish = true;  // K2f omitted: the cost of the combination itself
+            vars.push_back({vars[k].first + "_nofinish", t});
+        }
+    for (int rep = 0; rep < 2; ++rep)
+        for (auto& [name, t] : vars) {
+            for (T* a : P.adj) CK(cudaMemset(a, 0, sizeof(T)));
+            CK(cudaMemset(P.ws, 0, P.ws_bytes));
+            pull<Body, T, Sig>(P, &t);
+            const auto got = snapshot(P.adj, ns);
+            const bool same_tiling = t.txv == def.txv && t.rpt == def.rpt && !t.skip_finish;  // same order, bitwise
+            bool same = true;
+            for (size_t k = 0; k < got.size() && same; ++k)
+                for (size_t e = 0; e < got[k].size() && same; ++e) {
+                    const double x = got[k][e], y = ref[k][e];
+                    if (t.skip_finish && ns[k] != size_t(B * H)) continue;
+                    if (ns[k] == size_t(B * H) || same_tiling ? x != y
+                                                              : std::abs(x - y) > 1e-5 * std::max(std::abs(x), std::abs(y)) + 1e-30)
+                        same = false;
+                }
+            const double us = time_us([&] {
+                fwd<Body, T, Sig>(P, nullptr);
+                pull<Body, T, Sig>(P, &t);
+            }, 61);
+            const double k2 = time_us([&] { pull<Body, T, Sig>(P, &t); }, 61);
+            std::printf("{\"exp\": \"%s\", \"rep\": %d, \"variant\": \"%s\", \"txv\": %d, \"rpt\": %d, \"grid\": [%lld, %lld], "
+                        "\"pipe\": %d, \"combine\": \"%s\", \"step_us\": %.3f, \"step_frac\": %.3f, \"k2_cold_us\": %.3f, \"same\": %s}\n",
+                        tag, rep, name.c_str(), t.txv, t.rpt, (long long)t.n_col_tiles, (long long)t.n_row_tiles,
+                        int(pull_pipe(t)), t.skip_finish ? "none" : t.combine == 0 ? "k2f" : "tickets", us,
+                        double(P.step_bytes) / (us * 1e-6) / 6538e9, k2, same ? "true" : "false");
+            std::fflush(stdout);
+        }
+}
+
 int main(int argc, char** argv) {
     std::string which = argc > 1 ? argv[1] : "all";
     if (which.size() > 2 && which.compare(which.size() - 2, 2, ":r") == 0) {
@@ -515,6 +593,16 @@ int main(int argc, char** argv) {
                             rpt, uc, ub);
                 std::fflush(stdout);
             }
+    }
+    if (which == "step3") {  // config 3 only, with K2f-less timing variants
+        g_skip_finish_variants = true;
+        step_ab<KHmlstmBias, float, SigHmlstmBias>("step_cfg3", true, 1024, 1024, {{16, 2}, {32, 2}, {32, 1}, {64, 2}});
+        g_skip_finish_variants = false;
+    }
+    if (which == "step") {
+        step_ab<KHmlstmBias, float, SigHmlstmBias>("step_cfg3", true, 1024, 1024,
+                                                   {{16, 2}, {16, 4}, {16, 8}, {32, 2}, {32, 4}, {8, 4}, {8, 8}});
+        step_ab<KHmlstm, float, SigHmlstmCanonical>("step_cfg2", false, 1024, 1024, {{256, 2}, {256, 4}, {128, 2}});
     }
     if (which == "floor") {
         k1_sweep<KHmlstm, float, SigHmlstmCanonical>("k1_cfg2", false, 1024, 1024, {{256, 1}, {256, 2}});
