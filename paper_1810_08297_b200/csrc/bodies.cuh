@@ -74,7 +74,8 @@ struct KHmlstm {  // hmlstm.hpp:56-61
     static constexpr const char* kName = "hmlstm_update";
     static constexpr int kIn = 6, kOut = 1;
     static constexpr bool kMayRaise = false;
-    static constexpr uint32_t kPredicateArgs = 0x30u;  // z1, z2
+    static constexpr uint32_t kPredicateArgs = 0x30u;      // z1, z2
+    static constexpr uint32_t kPredicateOnlyArgs = 0x30u;  // ... and nothing else reads them
     static constexpr bool kSelectForm = true;
     template <class S>
     BCAD_HD static void body(const S* in, S* out) {
@@ -89,7 +90,8 @@ struct KHmlstmBias {  // cell_update(c, f + bf, i + bi, g + bg, z1, z2), SURVEY 
     static constexpr const char* kName = "hmlstm_update_bias";
     static constexpr int kIn = 9, kOut = 1;
     static constexpr bool kMayRaise = false;
-    static constexpr uint32_t kPredicateArgs = 0x180u;  // z1, z2
+    static constexpr uint32_t kPredicateArgs = 0x180u;      // z1, z2
+    static constexpr uint32_t kPredicateOnlyArgs = 0x180u;  // ... and nothing else reads them
     static constexpr bool kSelectForm = true;
     template <class S>
     BCAD_HD static void body(const S* in, S* out) {

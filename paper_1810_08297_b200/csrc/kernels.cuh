@@ -188,6 +188,22 @@ __host__ __device__ constexpr bool vec_eval_ok() {
     return true;
 }
 
+// Arguments that only feed branch predicates (Body::kPredicateOnlyArgs, bit
+// j): no arithmetic reads them, so every partial with respect to them is a
+// structural zero. The RecomputeReverse pullback skips forming their terms
+// (w * 0); the cached pullback reads and sums the stored zeros as the
+// reference-faithful byte count requires.
+// (-DBCAD_NO_PREDICATE_ONLY=1 disables the skip, for A/B runs.)
+template <class Body>
+__host__ __device__ constexpr uint32_t predicate_only_args() {
+#if defined(BCAD_NO_PREDICATE_ONLY) && BCAD_NO_PREDICATE_ONLY
+    return 0u;
+#else
+    if constexpr (requires { Body::kPredicateOnlyArgs; }) return Body::kPredicateOnlyArgs;
+    else return 0u;
+#endif
+}
+
 // The dual evaluation of one thread's V cells: primals y[M] (nullable) and
 // partials d[M*N] from inputs x[N], seeded x_j + e_j (forward.hpp:121-126).
 template <class Body, class T, int V, class S>
@@ -514,6 +530,7 @@ __global__ void __launch_bounds__(kThreads, kPipe ? 2 : (kRecompute ? kRecompute
     constexpr bool kAnyRow = !S::kStatic || S::has(kRow);
     constexpr bool kAnyCol = !S::kStatic || S::has(kCol);
     constexpr bool kAnyScal = !S::kStatic || S::has(kScalar);
+    constexpr uint32_t kZeroPartials = kRecompute ? predicate_only_args<Body>() : 0u;
     extern __shared__ double smem[];
     pdl_wait();
     pdl_trigger();  // lets the finisher (if any) be scheduled; it waits for this grid to complete
@@ -650,6 +667,10 @@ __global__ void __launch_bounds__(kThreads, kPipe ? 2 : (kRecompute ? kRecompute
             if (!kDense && !p.adj[j]) continue;
             const int cls = arg_class<S>(p.cls, j);
             const bool acc = !kDense && ((p.acc_mask >> j) & 1u);
+            // RecomputeReverse: an argument that only feeds branch predicates
+            // has structurally zero partials, so its terms are exact zeros and
+            // are not formed (compile-time per unrolled j)
+            const bool zero_d = (kZeroPartials >> j) & 1u;
             if (cls == kFull) {
                 if (!live) continue;
                 T* dst = p.adj[j] + off;
@@ -658,12 +679,19 @@ __global__ void __launch_bounds__(kThreads, kPipe ? 2 : (kRecompute ? kRecompute
 #pragma unroll
                 for (int v = 0; v < V; ++v) {
                     T a = acc ? out.x[v] : T(0);
+                    if (!zero_d)
 #pragma unroll
-                    for (int i = 0; i < M; ++i)
-                        if (kDense || p.w[i]) a = a + w[i].x[v] * D[i * N + j].x[v];
+                        for (int i = 0; i < M; ++i)
+                            if (kDense || p.w[i]) a = a + w[i].x[v] * D[i * N + j].x[v];
                     out.x[v] = a;
                 }
                 st_vec<T, V>(dst, out);
+                continue;
+            }
+            if (zero_d) {  // reduced class, all terms zero: the row sum is 0, column / scalar sums unchanged
+                if constexpr (kAnyRow)
+                    if (cls == kRow && (tid & (lanes - 1)) == 0)
+                        row_acc[(arg_slot<S, kDense>(p.slot, j) * trows + k * p.ty) * wpr + row_base] = 0.0;
                 continue;
             }
             // reduced classes: fp64 sum of the rounded terms

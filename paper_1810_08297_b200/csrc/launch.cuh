@@ -194,12 +194,17 @@ inline int pull_prefetch_rows(bool recompute, const Tiling& t) {
     return recompute && t.rpt >= 3 ? 1 : 0;
 }
 
-// Register double buffer of the pullback (kPipe): on small grids whose CTAs
-// cannot fill more than two per SM, where the launch is latency-bound, and
-// only with at least two rows per thread to overlap.
-inline bool pull_pipe(const Tiling& t) {
+// Register double buffer of the pullback (kPipe): on small, latency-bound
+// grids, and only with at least two rows per thread to overlap. Measured
+// (scripts/lab step / stepr, profiles/r02/lab_step_pipe.jsonl,
+// lab_stepr_pipe.jsonl), config-sized steps with stream launches:
+//   cached    config 3 (256 CTAs) 33.9 -> 29.6 us; config 2 (512 CTAs) 19.4 -> 20.1 us (worse: not used)
+//   recompute config 2 (512 CTAs) 21.1 -> 19.4 us; config 3 (256 CTAs) 30.9 -> 27.6 us
+// The recompute pullback already runs at three CTAs per SM (80 registers),
+// so dropping to two costs it less than it costs the cached one at four.
+inline bool pull_pipe(const Tiling& t, bool recompute) {
     if (t.pipe >= 0) return t.pipe > 0;
-    return t.rpt >= 2 && t.n_ctas <= 2 * int64_t(sm_count());
+    return t.rpt >= 2 && t.n_ctas <= (recompute ? 4 : 2) * int64_t(sm_count());
 }
 
 // The tiled 2-D pullback at VV cells per thread (VV = the 128-bit width, or
@@ -263,7 +268,7 @@ int launch_pull2d(const PullArgs& a, std::string* err) {
     bool dense = p.acc_mask == 0;  // every w and adjoint present, nothing accumulated
     for (int i = 0; i < M; ++i) dense = dense && p.w[i];
     for (int j = 0; j < N; ++j) dense = dense && p.adj[j];
-    const bool pipe = pull_pipe(t);
+    const bool pipe = pull_pipe(t, recompute);
     return with_sig<Sigs...>(plan, [&](auto sig) {
         using S = decltype(sig);
         void (*kern)(bcad_dev::Pull2DParams<N, M, T>);

@@ -566,7 +566,7 @@ void step_ab(const char* tag, bool bias, int64_t B, int64_t H, const std::vector
             std::printf("{\"exp\": \"%s\", \"rep\": %d, \"variant\": \"%s\", \"txv\": %d, \"rpt\": %d, \"grid\": [%lld, %lld], "
                         "\"pipe\": %d, \"combine\": \"%s\", \"step_us\": %.3f, \"step_frac\": %.3f, \"k2_cold_us\": %.3f, \"same\": %s}\n",
                         tag, rep, name.c_str(), t.txv, t.rpt, (long long)t.n_col_tiles, (long long)t.n_row_tiles,
-                        int(pull_pipe(t)), t.skip_finish ? "none" : t.combine == 0 ? "k2f" : "tickets", us,
+                        int(pull_pipe(t, g_recompute)), t.skip_finish ? "none" : t.combine == 0 ? "k2f" : "tickets", us,
                         double(P.step_bytes) / (us * 1e-6) / 6538e9, k2, same ? "true" : "false");
             std::fflush(stdout);
         }
@@ -593,6 +593,21 @@ int main(int argc, char** argv) {
                             rpt, uc, ub);
                 std::fflush(stdout);
             }
+    }
+    if (which == "k2r5") {  // RecomputeReverse pullback alone at config 5 and a mid size (default tilings)
+        g_recompute = true;
+        k2_sweep<KHmlstmBias, float, SigHmlstmBias>("k2r_cfg5", true, 65536, 4096, {});
+        k2_sweep<KHmlstmBias, float, SigHmlstmBias>("k2r_16384x1024", true, 16384, 1024, {});
+        k2_sweep<KHmlstm, float, SigHmlstmCanonical>("k2r_canon_65536x4096", false, 65536, 4096, {});
+        g_recompute = false;
+    }
+    if (which == "stepr") {  // RecomputeReverse steps (K1p + K2r) at the small configs
+        g_recompute = true;
+        g_primal_only = true;
+        step_ab<KHmlstm, float, SigHmlstmCanonical>("stepr_cfg2", false, 1024, 1024, {{256, 2}, {256, 4}, {128, 2}, {128, 4}, {64, 4}});
+        step_ab<KHmlstmBias, float, SigHmlstmBias>("stepr_cfg3", true, 1024, 1024, {{16, 2}, {16, 4}, {32, 2}, {32, 4}});
+        g_recompute = false;
+        g_primal_only = false;
     }
     if (which == "step3") {  // config 3 only, with K2f-less timing variants
         g_skip_finish_variants = true;

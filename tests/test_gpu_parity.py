@@ -379,3 +379,36 @@ def test_may_raise_kernel_refuses_graph_capture():
     with pytest.raises(native.ConfigError, match="cannot be captured"):
         with torch.cuda.graph(g, stream=s):
             native.forward(k, [a, a], prim, parts, stream=s)
+
+
+@pytest.mark.parametrize("variant,zj", [("canonical", (4, 5)), ("bias", (7, 8))])
+def test_predicate_only_arguments_have_exactly_zero_partials(oracle_lib, variant, zj):
+    """KHmlstm / KHmlstmBias declare z1, z2 predicate-only (kPredicateOnlyArgs):
+    the RecomputeReverse pullback then skips their terms. Pins the declaration
+    on the device: K1 stores exactly +0 for those partials (random inputs,
+    every branch class), and both policies give exactly zero z adjoints with
+    bit-identical other adjoints."""
+    import torch
+    from paper_1810_08297_b200 import native
+    B, H = 256, 512
+    ins = O.hmlstm_inputs(oracle_lib, B, H, np.float32, variant)
+    name = O.hmlstm_kernel(variant)
+    k = native.Kernel(name)
+    dins = [torch.from_numpy(a).cuda() for a in ins]
+    shapes = [a.shape for a in ins]
+    prim = [torch.empty((B, H), device="cuda")]
+    parts = [torch.empty((B, H), device="cuda") for _ in range(k.n_in)]
+    native.forward(k, dins, prim, parts)
+    for j in zj:
+        d = parts[j].cpu().numpy()
+        assert np.all(d == 0) and not np.any(np.signbit(d)), f"partial {j} not exactly +0"
+    seed = [torch.rand((B, H), device="cuda") * 2 - 1]
+    got = []
+    for policy_parts in (parts, None):
+        adj = [torch.full(s, 7.0, device="cuda") for s in shapes]
+        native.pullback(k, shapes, seed, policy_parts, dins, adj, workspace=native.new_workspace(k, shapes, torch.float32))
+        got.append([a.cpu().numpy() for a in adj])
+    for j in range(k.n_in):
+        assert np.array_equal(got[0][j], got[1][j]), f"adjoint {j} differs between policies"
+    for j in zj:
+        assert np.all(got[1][j] == 0)
