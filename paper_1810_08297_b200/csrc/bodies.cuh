@@ -158,6 +158,16 @@ struct KTanhProduct {  // arity_workload.hpp:19-28
     // K1 rows per thread on large problems (lab k1rpt, 4096^2 fp32: A=4
     // 2 rows 0.83 -> 8 rows 0.87 of the copy peak, A=16 0.66 -> 0.71; A=1 flat)
     static constexpr int kFwdRows = 8;
+    // A = 32: no next-row register pipeline and at least three CTAs per SM
+    // (80 registers, 56 B of spill) instead of the pipeline at two CTAs per
+    // SM (128 registers): 1136 -> 1077 us at 4096^2 (scripts/lab "arity",
+    // profiles/r02/lab_arity_variants.jsonl). A = 16 / 18 already fit 80
+    // registers with the pipeline, where dropping it does not help.
+#ifndef BCAD_ARITY_VARIANT
+#define BCAD_ARITY_VARIANT 2
+#endif
+    static constexpr bool kFwdPipeline = !(BCAD_ARITY_VARIANT >= 1 && A >= 32);
+    static constexpr int kFwdMinBlocks = (BCAD_ARITY_VARIANT >= 2 && A >= 32) ? 3 : 0;
     template <class S>
     BCAD_HD static void body_select(const S* in, S* out) { body(in, out); }
     template <class S>

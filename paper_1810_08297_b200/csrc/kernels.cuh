@@ -282,8 +282,26 @@ struct Fwd2DParams {
 // storing whichever of primal / partials pointers are non-null (kDense: all
 // of them, no checks). The next row's loads are issued before the current
 // row is evaluated, so every thread keeps two rows of loads in flight.
+//
+// Bodies whose per-cell dual state is wide (tanh_product_<A> at large A) can
+// ask for K1 without the next-row register pipeline (Body::kFwdPipeline =
+// false) and for a minimum of resident CTAs per SM (Body::kFwdMinBlocks),
+// trading the second row of loads in flight for occupancy.
+template <class Body>
+__host__ __device__ constexpr bool fwd_pipeline() {
+    if constexpr (requires { Body::kFwdPipeline; }) return Body::kFwdPipeline;
+    else return true;
+}
+// 0 = no minimum (the compiler's own register heuristic; an explicit 1
+// lets ptxas use up to 255 registers, measured 2x slower for A >= 16)
+template <class Body>
+__host__ __device__ constexpr int fwd_min_blocks() {
+    if constexpr (requires { Body::kFwdMinBlocks; }) return Body::kFwdMinBlocks;
+    else return 0;
+}
+
 template <class Body, class T, int V, bool kReal, class S, bool kDense>
-__global__ void __launch_bounds__(kThreads) fwd2d_kernel(const __grid_constant__ Fwd2DParams<Body::kIn, Body::kOut, T> p) {
+__global__ void __launch_bounds__(kThreads, fwd_min_blocks<Body>()) fwd2d_kernel(const __grid_constant__ Fwd2DParams<Body::kIn, Body::kOut, T> p) {
     constexpr int N = Body::kIn, M = Body::kOut;
     pdl_wait();
     pdl_trigger();
@@ -323,13 +341,15 @@ __global__ void __launch_bounds__(kThreads) fwd2d_kernel(const __grid_constant__
     };
     int64_t r = int64_t(blockIdx.y) * p.tile_rows + ty;
     if (r >= p.rows) return;
+    constexpr bool kPipe = fwd_pipeline<Body>();
     Pack<T, V> x[N];
     load_row(r, x);
     for (int k = 0; k < p.rpt; ++k) {
         const int64_t rn = r + p.ty;
         const bool has_next = k + 1 < p.rpt && rn < p.rows;
-        Pack<T, V> xn[N];
-        if (has_next) load_row(rn, xn);
+        Pack<T, V> xn[kPipe ? N : 1];
+        if constexpr (kPipe)
+            if (has_next) load_row(rn, xn);
         const int64_t off = r * p.cols + c0;
         if constexpr (kReal) {
             Pack<T, V> y[M];
@@ -359,8 +379,12 @@ __global__ void __launch_bounds__(kThreads) fwd2d_kernel(const __grid_constant__
             }
         }
         if (!has_next) break;
+        if constexpr (kPipe) {
 #pragma unroll
-        for (int j = 0; j < N; ++j) x[j] = xn[j];
+            for (int j = 0; j < N; ++j) x[j] = xn[j];
+        } else {
+            load_row(rn, x);
+        }
         r = rn;
     }
 }

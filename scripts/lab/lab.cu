@@ -594,6 +594,13 @@ int main(int argc, char** argv) {
                 std::fflush(stdout);
             }
     }
+    if (which == "arity") {  // tanh_product_<A> K1 at 4096^2 fp32 (bench extra.arity), rows per thread
+        const std::vector<std::array<int, 2>> t = {{256, 4}, {256, 8}, {256, 16}};
+        k1_sweep<KTanhProduct<8>, float, DynSig>("k1_tp8_4096", false, 4096, 4096, t, 8);
+        k1_sweep<KTanhProduct<16>, float, DynSig>("k1_tp16_4096", false, 4096, 4096, t, 16);
+        k1_sweep<KTanhProduct<18>, float, DynSig>("k1_tp18_4096", false, 4096, 4096, t, 18);
+        k1_sweep<KTanhProduct<32>, float, DynSig>("k1_tp32_4096", false, 4096, 4096, t, 32);
+    }
     if (which == "k2r5") {  // RecomputeReverse pullback alone at config 5 and a mid size (default tilings)
         g_recompute = true;
         k2_sweep<KHmlstmBias, float, SigHmlstmBias>("k2r_cfg5", true, 65536, 4096, {});
