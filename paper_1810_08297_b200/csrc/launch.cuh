@@ -6,7 +6,9 @@
 #pragma once
 
 #include <cstdint>
+#include <mutex>
 #include <string>
+#include <unordered_map>
 
 #include "kernels.cuh"
 #include "registry.hpp"
@@ -46,6 +48,34 @@ cudaError_t launch_pdl(void (*kern)(Params), dim3 grid, size_t smem, cudaStream_
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     return cudaLaunchKernelEx(&cfg, kern, p);
+}
+
+// Resident 256-thread CTAs per SM of a kernel (occupancy API, cached per
+// kernel; kCtasPerSm if the query fails, e.g. without a device).
+inline std::mutex& occupancy_mutex() {
+    static std::mutex m;
+    return m;
+}
+inline std::unordered_map<const void*, int>& occupancy_cache() {
+    static std::unordered_map<const void*, int> c;
+    return c;
+}
+template <class Params>
+int ctas_per_sm(void (*kern)(Params)) {
+    const void* key = reinterpret_cast<const void*>(kern);
+    {
+        std::lock_guard<std::mutex> lock(occupancy_mutex());
+        auto it = occupancy_cache().find(key);
+        if (it != occupancy_cache().end()) return it->second;
+    }
+    int n = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kern, kThreads, 0) != cudaSuccess || n < 1) {
+        (void)cudaGetLastError();
+        return kCtasPerSm;
+    }
+    std::lock_guard<std::mutex> lock(occupancy_mutex());
+    occupancy_cache()[key] = n;
+    return n;
 }
 
 template <class S>
@@ -111,9 +141,6 @@ int launch_fwd2d(const FwdArgs& a, std::string* err) {
     constexpr int N = Body::kIn, M = Body::kOut;
     const Plan& plan = *a.plan;
     const bool real = a.partials == nullptr;
-    // no reductions in K1: wide row tiles
-    const Tiling t = a.tiling ? *a.tiling
-                              : choose_tiling(plan, VV, ClassMix{}, /*fine=*/true, real ? kFwdRowsPrimalOnly : fwd_rows<Body>());
     bcad_dev::Fwd2DParams<N, M, T> p{};
     for (int j = 0; j < N; ++j) {
         p.in[j] = static_cast<const T*>(a.in[j]);
@@ -125,13 +152,7 @@ int launch_fwd2d(const FwdArgs& a, std::string* err) {
     }
     p.rows = plan.rows;
     p.cols = plan.cols;
-    p.vcols = int(t.vcols);
-    p.txv_shift = __builtin_ctz(unsigned(t.txv));
-    p.ty = t.ty;
-    p.rpt = t.rpt;
-    p.tile_rows = t.tile_rows;
     p.err = a.err;
-    const dim3 grid(unsigned(t.n_col_tiles), unsigned(t.n_row_tiles));
     bool dense = true;  // every output pointer present: no per-store checks
     for (int i = 0; i < M; ++i) {
         dense = dense && p.primal[i];
@@ -146,6 +167,17 @@ int launch_fwd2d(const FwdArgs& a, std::string* err) {
         } else {
             kern = real ? &bcad_dev::fwd2d_kernel<Body, T, VV, true, S, false> : &bcad_dev::fwd2d_kernel<Body, T, VV, false, S, false>;
         }
+        // no reductions in K1: wide row tiles, one wave of this kernel's
+        // resident CTAs on small problems
+        const Tiling t = a.tiling ? *a.tiling
+                                  : choose_tiling(plan, VV, ClassMix{}, /*fine=*/true,
+                                                  real ? kFwdRowsPrimalOnly : fwd_rows<Body>(), ctas_per_sm(kern));
+        p.vcols = int(t.vcols);
+        p.txv_shift = __builtin_ctz(unsigned(t.txv));
+        p.ty = t.ty;
+        p.rpt = t.rpt;
+        p.tile_rows = t.tile_rows;
+        const dim3 grid(unsigned(t.n_col_tiles), unsigned(t.n_row_tiles));
         return cuda_status(launch_pdl(kern, grid, 0, a.stream, p), err);
     });
 }

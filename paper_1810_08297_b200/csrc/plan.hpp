@@ -212,15 +212,25 @@ inline ClassMix class_mix(const Plan& p) {
 // Small problems (at most two waves at one row per thread) run as one wave:
 // config-2 K1 at two rows per thread 12.3 us against 14.3 us at one
 // (interleaved A/B, scripts/lab k1ab; config 3 unchanged).
-inline Tiling choose_tiling(const Plan& p, int V, const ClassMix& mix, bool fine = false, int fine_rows = 2) {
+//
+// K1 (fine) passes the kernel's own resident CTAs per SM (fwd_ctas_per_sm,
+// from the occupancy API) so a small problem really is ONE wave, and keeps
+// rows at most 128 vector-columns wide there. Measured at config 3 (bias K1,
+// 74 registers, 3 CTAs per SM; scripts/lab k1small, means): 256 x 2 rows
+// (512 CTAs, 1.15 waves) 15.9 us, 256 x 3 (342 CTAs) 15.1 us, 128 x 3 14.5 us;
+// config 2 (4 CTAs per SM): 256 x 2 12.6 us, 128 x 2 12.5 us.
+inline Tiling choose_tiling(const Plan& p, int V, const ClassMix& mix, bool fine = false, int fine_rows = 2,
+                            int fwd_ctas_per_sm = kCtasPerSm) {
     Tiling t;
     t.V = V;
     t.vcols = p.cols / V;
-    const int cap = mix.col ? 32 : 256;
+    const int sms = sm_count();
+    const int64_t slots = int64_t(sms) * (fine ? fwd_ctas_per_sm : kCtasPerSm);
+    // K1 runs small problems (up to three rows per thread) as one wave
+    const bool fine_small = fine && ceil_div(p.rows * std::max<int64_t>(t.vcols, 1), 256) <= 3 * slots;
+    int cap = mix.col ? 32 : fine_small ? 128 : 256;
     int txv = 1;
     while (txv < cap && txv < t.vcols) txv <<= 1;
-    const int sms = sm_count();
-    const int64_t slots = int64_t(sms) * kCtasPerSm;
     // Column reductions ((1,H) arguments): at least 4 rows per thread, which
     // amortises each CTA's shared-memory setup and combine; small problems
     // also take 16-lane column tiles (64 fp32 columns) and about two CTAs per
@@ -241,7 +251,8 @@ inline Tiling choose_tiling(const Plan& p, int V, const ClassMix& mix, bool fine
     // eight waves, at most 16 rows per thread. Measured at config 5 (lab k5,
     // bias 65536 x 4096 fp32): K1 55 -> 2 rows 0.94 -> 1.02 of the copy peak,
     // K2 55 -> 16 rows 0.94 -> 0.97.
-    int64_t rpt = work <= 2 * slots ? ceil_div(work, slots) : (fine ? fine_rows : work / (8 * slots));
+    int64_t rpt = (fine ? fine_small : work <= 2 * slots) ? ceil_div(work, slots)
+                                                           : (fine ? fine_rows : work / (8 * slots));
     if (col_small) rpt = ceil_div(work, 2 * sms);
     else if (mix.col && !fine && rpt < 4) rpt = 4;
     if (rpt < 1) rpt = 1;

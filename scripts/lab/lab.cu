@@ -594,6 +594,12 @@ int main(int argc, char** argv) {
                 std::fflush(stdout);
             }
     }
+    if (which == "k1small") {  // K1 rows per thread at configs 2 / 3 (means), incl. single-wave rpt = 3
+        const std::vector<std::array<int, 2>> t = {{256, 1}, {256, 2}, {256, 3}, {256, 4}, {128, 2}, {128, 3}, {64, 3}};
+        k1_sweep<KHmlstm, float, SigHmlstmCanonical>("k1_cfg2", false, 1024, 1024, t);
+        k1_sweep<KHmlstmBias, float, SigHmlstmBias>("k1_cfg3", true, 1024, 1024, t);
+        step_ab<KHmlstmBias, float, SigHmlstmBias>("step_cfg3", true, 1024, 1024, {{16, 3}, {16, 5}, {32, 3}});
+    }
     if (which == "arity") {  // tanh_product_<A> K1 at 4096^2 fp32 (bench extra.arity), rows per thread
         const std::vector<std::array<int, 2>> t = {{256, 4}, {256, 8}, {256, 16}};
         k1_sweep<KTanhProduct<8>, float, DynSig>("k1_tp8_4096", false, 4096, 4096, t, 8);
@@ -689,6 +695,16 @@ int main(int argc, char** argv) {
         fwd<KHmlstm, float, SigHmlstmCanonical>(P, nullptr);
         for (int k = 0; k < 3; ++k) pull<KHmlstm, float, SigHmlstmCanonical>(P, nullptr);
         CK(cudaDeviceSynchronize());
+    }
+    if (which == "k2tick") {  // config-3 and mixed-layout pullbacks with the in-kernel ticket combine, for sanitizers
+        for (auto [B, H] : {std::pair<int64_t, int64_t>{1024, 1024}, {64, 256}, {3000, 1024}}) {
+            Problem<float> P(true, B, H);
+            fwd<KHmlstmBias, float, SigHmlstmBias>(P, nullptr);
+            Tiling t = choose_tiling(P.plan, 4, class_mix(P.plan));
+            t.combine = 1;
+            for (int k = 0; k < 2; ++k) pull<KHmlstmBias, float, SigHmlstmBias>(P, &t);
+            CK(cudaDeviceSynchronize());
+        }
     }
     if (which == "k2mix") {  // several reduction layouts in one process: small / tall / wide bias problems
         for (auto [B, H] : {std::pair<int64_t, int64_t>{64, 256}, {4096, 128}, {16, 8192}, {3000, 1024}}) {
