@@ -155,16 +155,18 @@ struct KTanhProduct {  // arity_workload.hpp:19-28
     // cells per K1 thread: the product's dual keeps all A partials live, so
     // wide arities evaluate fewer cells at once (register study, paper Fig. 3)
     static constexpr int kMaxVec = A >= 16 ? 1 : A >= 8 ? 2 : 4;
-    // K1 rows per thread on large problems (lab k1rpt, 4096^2 fp32: A=4
-    // 2 rows 0.83 -> 8 rows 0.87 of the copy peak, A=16 0.66 -> 0.71; A=1 flat)
-    static constexpr int kFwdRows = 8;
-    // A = 32: no next-row register pipeline and at least three CTAs per SM
-    // (80 registers, 56 B of spill) instead of the pipeline at two CTAs per
-    // SM (128 registers): 1136 -> 1077 us at 4096^2 (scripts/lab "arity",
-    // profiles/r02/lab_arity_variants.jsonl). A = 16 / 18 already fit 80
-    // registers with the pipeline, where dropping it does not help.
+    // K1 rows per thread on large problems, measured with the all-full-shape
+    // signature (reg_arity.cu) at 4096^2 fp32 (scripts/lab "arity",
+    // "arity32", means; profiles/r02/lab_arity_static.jsonl): A <= 8 best at
+    // 2 rows (A4 0.96, A8 0.99 of the copy peak), A = 16 / 18 at 4 (0.93 /
+    // 0.92), A = 32 at 8 (0.79).
+    static constexpr int kFwdRows = A >= 32 ? 8 : A >= 16 ? 4 : 2;
+    // lab A/B of the K1 register pipeline for wide bodies: 0 = next-row
+    // pipeline (default; with the static signature A = 32 runs 0.793 with it
+    // against 0.778 without it at >= 3 CTAs per SM); 1 = no pipeline for
+    // A >= 32; 2 = no pipeline and >= 3 CTAs per SM for A >= 32
 #ifndef BCAD_ARITY_VARIANT
-#define BCAD_ARITY_VARIANT 2
+#define BCAD_ARITY_VARIANT 0
 #endif
     static constexpr bool kFwdPipeline = !(BCAD_ARITY_VARIANT >= 1 && A >= 32);
     static constexpr int kFwdMinBlocks = (BCAD_ARITY_VARIANT >= 2 && A >= 32) ? 3 : 0;

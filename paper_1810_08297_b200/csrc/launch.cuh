@@ -9,6 +9,7 @@
 #include <mutex>
 #include <string>
 #include <unordered_map>
+#include <utility>
 
 #include "kernels.cuh"
 #include "registry.hpp"
@@ -402,6 +403,17 @@ int launch_pull_any(const PullArgs& a, std::string* err) {
 using SigHmlstmCanonical = Sig<kFull, kFull, kFull, kFull, kRow, kRow>;
 using SigHmlstmDivergence = Sig<kFull, kFull, kFull, kFull, kFull, kFull>;
 using SigHmlstmBias = Sig<kFull, kFull, kFull, kFull, kCol, kCol, kCol, kRow, kRow>;
+// Every argument full-shape (an elementwise problem, e.g. the arity workload):
+// compile-time classes drop the per-argument class branches and, with every
+// output wanted, the per-store null checks.
+template <int N, class Seq = std::make_integer_sequence<int, N>>
+struct SigAllFullT;
+template <int N, int... I>
+struct SigAllFullT<N, std::integer_sequence<int, I...>> {
+    using type = Sig<((void)I, int(kFull))...>;
+};
+template <int N>
+using SigAllFull = typename SigAllFullT<N>::type;
 
 }  // namespace bcad_cu_impl
 

@@ -600,12 +600,23 @@ int main(int argc, char** argv) {
         k1_sweep<KHmlstmBias, float, SigHmlstmBias>("k1_cfg3", true, 1024, 1024, t);
         step_ab<KHmlstmBias, float, SigHmlstmBias>("step_cfg3", true, 1024, 1024, {{16, 3}, {16, 5}, {32, 3}});
     }
+    if (which == "arity32") {  // A = 32 static signature, rows per thread
+        const std::vector<std::array<int, 2>> t = {{256, 2}, {256, 4}, {256, 8}, {128, 4}, {128, 8}};
+        k1_sweep<KTanhProduct<32>, float, SigAllFull<32>>("k1_tp32_4096_static", false, 4096, 4096, t, 32);
+        k1_sweep<KTanhProduct<1>, float, SigAllFull<1>>("k1_tp1_4096_static", false, 4096, 4096, t, 1);
+        k1_sweep<KTanhProduct<4>, float, SigAllFull<4>>("k1_tp4_4096_static", false, 4096, 4096, t, 4);
+        k1_sweep<KTanhProduct<4>, float, DynSig>("k1_tp4_4096", false, 4096, 4096, t, 4);
+    }
     if (which == "arity") {  // tanh_product_<A> K1 at 4096^2 fp32 (bench extra.arity), rows per thread
         const std::vector<std::array<int, 2>> t = {{256, 4}, {256, 8}, {256, 16}};
         k1_sweep<KTanhProduct<8>, float, DynSig>("k1_tp8_4096", false, 4096, 4096, t, 8);
         k1_sweep<KTanhProduct<16>, float, DynSig>("k1_tp16_4096", false, 4096, 4096, t, 16);
         k1_sweep<KTanhProduct<18>, float, DynSig>("k1_tp18_4096", false, 4096, 4096, t, 18);
         k1_sweep<KTanhProduct<32>, float, DynSig>("k1_tp32_4096", false, 4096, 4096, t, 32);
+        k1_sweep<KTanhProduct<8>, float, SigAllFull<8>>("k1_tp8_4096_static", false, 4096, 4096, t, 8);
+        k1_sweep<KTanhProduct<16>, float, SigAllFull<16>>("k1_tp16_4096_static", false, 4096, 4096, t, 16);
+        k1_sweep<KTanhProduct<18>, float, SigAllFull<18>>("k1_tp18_4096_static", false, 4096, 4096, t, 18);
+        k1_sweep<KTanhProduct<32>, float, SigAllFull<32>>("k1_tp32_4096_static", false, 4096, 4096, t, 32);
     }
     if (which == "k2r5") {  // RecomputeReverse pullback alone at config 5 and a mid size (default tilings)
         g_recompute = true;
