@@ -36,7 +36,11 @@ UNIT_SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1e
 
 
 def raw(report):
-    out = subprocess.run(["ncu", "-i", report, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    if report.endswith(".csv.gz"):  # raw page exported on the GPU box (scripts/gpu_profile.sh)
+        import gzip
+        out = gzip.open(report, "rt").read()
+    else:
+        out = subprocess.run(["ncu", "-i", report, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
     head, units = rows[0], rows[1]
     res = []
@@ -84,13 +88,15 @@ def main():
              "L2-resident after K1 at config 2). Algorithmic bytes per launch are SURVEY §8(d)'s reference-faithful "
              "counts (paper_1810_08297_b200/workloads.py); peak = MEASURED_PEAKS.json hbm_gbs of this container.", ""]
     traffic = {}
-    peak = 6459.0
+    peak = 6538.0
     try:
         peak = float(json.load(open("MEASURED_PEAKS.json"))["hbm_gbs"])
     except Exception:
         pass
     for cfg in ("cfg2", "cfg3", "cfg5", "cfg4div"):
         rep = os.path.join(src, f"full_{cfg}.ncu-rep")
+        if not os.path.exists(rep):
+            rep = os.path.join(src, f"full_{cfg}.raw.csv.gz")
         if not os.path.exists(rep):
             continue
         w = WORKLOADS[cfg]
