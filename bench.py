@@ -11,8 +11,9 @@ allreduce of batch-broadcast adjoints when sharded), BASELINE.json metric
 torch.distributed.run with N ranks (one per GPU); under torchrun WORLD_SIZE
 must equal --gpus. Default workload: config 2 (1024x1024 fp32, BASELINE's
 "on 1 B200" config) at N = 1; config 5 (65536x4096 fp32 bias variant,
-batch-sharded, NCCL allreduce of the 3 (1,H) adjoints, strong scaling) at
-N > 1. --dry-run runs the N-rank plumbing on CPU over gloo (no GPU work).
+batch-sharded, strong scaling) at N > 1, the 3 (1,H) adjoints allreduced
+inside the pullback's finisher over NVLink peer memory (--allreduce fused,
+default; --allreduce nccl for ncclAllReduce after the pullback). --dry-run runs the N-rank plumbing on CPU over gloo (no GPU work).
 
 One step = one pass of the hot path over one batch: bcad_cu_forward (primal +
 M*N partials) then bcad_cu_pullback (all input adjoints) — what the
@@ -344,7 +345,7 @@ def run_native(args, w: Workload, rank: int, world: int):
     import torch.distributed as dist
     from paper_1810_08297_b200 import native
 
-    local = int(os.environ.get("LOCAL_RANK", "0"))
+    local = 0 if args.share_device else int(os.environ.get("LOCAL_RANK", "0"))
     if torch.cuda.device_count() <= local:
         raise SystemExit(f"bench.py: rank {rank} needs cuda:{local} but {torch.cuda.device_count()} GPU(s) are "
                          f"visible; run --gpus N with at most the visible GPU count")
@@ -364,8 +365,32 @@ def run_native(args, w: Workload, rank: int, world: int):
     sp = int(stream.cuda_stream)
 
     comm = None
+    peer = None
     nccl_nranks = None
-    if world > 1 and w.variant == "bias":
+    fused_error = None
+    if world > 1 and w.variant == "bias" and args.allreduce == "fused":
+        # K2f fused with the allreduce: fp64 column sums stored into every
+        # rank's buffer over NVLink (CUDA IPC), summed in rank order. If any
+        # rank cannot set the group up (no peer access / IPC), every rank
+        # falls back to the NCCL allreduce.
+        ok = 1
+        try:
+            peer = native.PeerGroup(rank, world, 3 * w.H)
+            blobs = [None] * world
+            dist.all_gather_object(blobs, peer.blob)
+            peer.connect(blobs)
+        except Exception as e:  # noqa: BLE001 - reported in the line, NCCL used instead
+            ok, fused_error, peer = 0, repr(e)[:200], None
+        flags = [None] * world
+        dist.all_gather_object(flags, ok)
+        if min(flags) == 1:
+            case.step = native.PreparedStep(case.k, case.ins, case.primal, case.partials, [case.seed], case.adj,
+                                            case.ws, policy=args.policy, peer=peer)
+        else:
+            peer = None
+            fused_error = fused_error or "a peer rank could not join the peer group"
+        dist.barrier()
+    if world > 1 and w.variant == "bias" and peer is None:
         uid = [native.nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(uid, src=0)
         comm = native.Comm(world, uid[0], rank)
@@ -473,7 +498,7 @@ def run_native(args, w: Workload, rank: int, world: int):
     ar_ms = [e[2].elapsed_time(e[3]) for e in evb]
     total_ms = sum(step_ms)
     if world > 1:
-        t = torch.tensor([total_ms], device=device, dtype=torch.float64)
+        t = torch.tensor([total_ms], device=device if dist.get_backend() == "nccl" else "cpu", dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         total_ms = float(t.item())
     ms_per_step = total_ms / K
@@ -483,7 +508,8 @@ def run_native(args, w: Workload, rank: int, world: int):
     # ---- end to end through the C-ABI with host buffers
     e2e = run_e2e(case, stream, args.e2e_steps, device)
     if world > 1:
-        t = torch.tensor([e2e["ms_per_step"]], device=device, dtype=torch.float64)
+        t = torch.tensor([e2e["ms_per_step"]], device=device if dist.get_backend() == "nccl" else "cpu",
+                         dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e["ms_per_step"] = float(t.item())
     e2e_value = cells_per_step / (e2e["ms_per_step"] * 1e-3)
@@ -563,6 +589,12 @@ def run_native(args, w: Workload, rank: int, world: int):
     }
     if world > 1:
         line["multi_gpu"] = {"nccl_nranks": nccl_nranks, "world_size": world,
+                             "allreduce": ("fused: K2f-AR stores fp64 column sums into every rank's buffer over "
+                                           "NVLink peer memory (CUDA IPC), flag exchange, rank-order sum "
+                                           "(bcad_cu_pullback_allreduce)" if peer is not None
+                                           else "NCCL ncclAllReduce of the 3 x H fp32 bias adjoints after K2f"
+                                           if comm is not None else None),
+                             "fused_fallback_reason": fused_error,
                              "allreduce_us_per_step": (statistics.mean(ar_ms) * 1e3 if comm is not None else None),
                              "allreduce_bytes": (case.bias_adj.numel() * case.bias_adj.element_size()
                                                  if comm is not None else 0),
@@ -825,6 +857,13 @@ def main():
                     help="default cfg2 at one GPU, cfg5 (strong scaling, NCCL allreduce) at N > 1")
     ap.add_argument("--impl", default="native", choices=["native", "reference"])
     ap.add_argument("--policy", type=int, default=0, help="0 CacheForward, 1 RecomputeReverse")
+    ap.add_argument("--share-device", action="store_true",
+                    help="test aid: every rank on cuda:0 (exercises the N-rank path and the fused peer allreduce on "
+                         "a one-GPU box; NCCL refuses it; timings are meaningless)")
+    ap.add_argument("--allreduce", choices=("nccl", "fused"), default="fused",
+                    help="N > 1, bias variant: the pullback's finisher fused with the allreduce over NVLink peer "
+                         "memory (bcad_cu_pullback_allreduce; default, falls back to NCCL if a rank cannot join), "
+                         "or the NCCL allreduce after the pullback")
     ap.add_argument("--e2e-steps", type=int, default=10)
     ap.add_argument("--graph", type=int, default=1, help="1: replay the step as a captured CUDA graph")
     ap.add_argument("--extra", default="cfg3,cfg4,cfg4div,cfg5,cfg2:r,cfg5:r,tape,arity,shards",
@@ -861,8 +900,12 @@ def main():
     if world > 1:
         import torch
         import torch.distributed as dist
-        torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")))
-        dist.init_process_group("nccl", device_id=torch.device("cuda", int(os.environ.get("LOCAL_RANK", "0"))))
+        if args.share_device:  # NCCL refuses two ranks on one GPU; plumbing over gloo
+            torch.cuda.set_device(0)
+            dist.init_process_group("gloo")
+        else:
+            torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")))
+            dist.init_process_group("nccl", device_id=torch.device("cuda", int(os.environ.get("LOCAL_RANK", "0"))))
     try:
         run_native(args, w, rank, world)
     finally:

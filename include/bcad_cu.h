@@ -222,6 +222,33 @@ int bcad_cu_comm_count(void* comm, int* nranks);
 int bcad_cu_allreduce_adjoints(void* const* bufs, const size_t* counts, int n_bufs, int dtype, void* comm,
                                void* stream);
 
+/* ------------------------------------------ fused pullback allreduce
+ * A peer-memory group for the compute+collective form of the sharded
+ * pullback: K2's cross-CTA finisher (K2f) stores its fp64 column sums
+ * straight into every rank's buffer over NVLink and, after a flag exchange,
+ * each rank adds the world's sums in rank order — the allreduce of the
+ * batch-broadcast ((1,H)-class) adjoints happens inside the pullback's own
+ * last kernel, with no separate collective launch, identical bits on every
+ * rank and one fp32 rounding of the fp64 world sum (the NCCL path rounds each
+ * rank's partial). One group per rank (one process per GPU, or several ranks
+ * in one process): create returns this rank's handle blob, every rank
+ * gathers all blobs in rank order (e.g. torch.distributed all_gather) and
+ * connects. max_elems bounds the reduced elements of one pullback
+ * (n_col_args * H). Every rank must issue the same sequence of
+ * bcad_cu_pullback_allreduce calls; a rank whose peers never arrive traps
+ * after 30 s (no silent hang). Replaces bcad_cu_pullback +
+ * bcad_cu_allreduce_adjoints for the sharded step. */
+#define BCAD_CU_PEER_HANDLE_BYTES 128
+typedef struct bcad_cu_peer_group_s* bcad_cu_peer_group;
+int bcad_cu_peer_group_create(int rank, int world, size_t max_elems, bcad_cu_peer_group* out,
+                              unsigned char handle[BCAD_CU_PEER_HANDLE_BYTES]);
+int bcad_cu_peer_group_connect(bcad_cu_peer_group group, const unsigned char* handles);
+int bcad_cu_peer_group_destroy(bcad_cu_peer_group group);
+int bcad_cu_pullback_allreduce(bcad_cu_kernel k, int dtype, int n_in, const bcad_cu_shape* in_shapes, int m_out,
+                               const void* const* out_adj, const void* const* partials, const void* const* in,
+                               void* const* in_adj, const unsigned char* accumulate, void* workspace,
+                               size_t workspace_bytes, bcad_cu_peer_group group, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

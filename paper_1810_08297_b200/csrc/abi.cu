@@ -2,6 +2,7 @@
 // launches, error-word decoding, device memory, streams and NCCL.
 #include <cuda_runtime.h>
 #include <dlfcn.h>
+#include <unistd.h>
 
 #include <cstdint>
 #include <cstring>
@@ -43,8 +44,9 @@ struct Registry {
     std::mutex mu;
     std::vector<const bcad_cu_kernel_entry*> all;
     Registry() {
-        int (*groups[])(const bcad_cu_kernel_entry**) = {&bcad_reg_hmlstm, &bcad_reg_pool, &bcad_reg_probe, &bcad_reg_prims,
-                                                         &bcad_reg_arity};
+        int (*groups[])(const bcad_cu_kernel_entry**) = {&bcad_reg_hmlstm, &bcad_reg_pool,       &bcad_reg_probe,
+                                                         &bcad_reg_prims,  &bcad_reg_arity,      &bcad_reg_arity_wide,
+                                                         &bcad_reg_arity_wide32};
         for (auto g : groups) {
             const bcad_cu_kernel_entry* e = nullptr;
             const int n = g(&e);
@@ -433,10 +435,26 @@ int bcad_cu_pullback_launches(bcad_cu_kernel k, int dtype, int n_in, const bcad_
     return BCAD_CU_OK;
 }
 
+namespace {
+int pullback_impl(bcad_cu_kernel k, int dtype, int n_in, const bcad_cu_shape* in_shapes, int m_out,
+                  const void* const* out_adj, const void* const* partials, const void* const* in,
+                  void* const* in_adj, const unsigned char* accumulate, void* workspace, size_t workspace_bytes,
+                  void* stream, const PeerParams* peer);
+}
+
 int bcad_cu_pullback(bcad_cu_kernel k, int dtype, int n_in, const bcad_cu_shape* in_shapes, int m_out,
                      const void* const* out_adj, const void* const* partials, const void* const* in,
                      void* const* in_adj, const unsigned char* accumulate, void* workspace, size_t workspace_bytes,
                      void* stream) {
+    return pullback_impl(k, dtype, n_in, in_shapes, m_out, out_adj, partials, in, in_adj, accumulate, workspace,
+                         workspace_bytes, stream, nullptr);
+}
+
+namespace {
+int pullback_impl(bcad_cu_kernel k, int dtype, int n_in, const bcad_cu_shape* in_shapes, int m_out,
+                  const void* const* out_adj, const void* const* partials, const void* const* in,
+                  void* const* in_adj, const unsigned char* accumulate, void* workspace, size_t workspace_bytes,
+                  void* stream, const PeerParams* peer) {
     int rc = arity_check(k, n_in, m_out);
     if (rc) return rc;
     if ((rc = dtype_check(dtype))) return rc;
@@ -472,10 +490,12 @@ int bcad_cu_pullback(bcad_cu_kernel k, int dtype, int n_in, const bcad_cu_shape*
     }
     unsigned long long* word = ew.get();
     PullArgs a{dtype, out_adj, partials, in, in_adj, accumulate, workspace, workspace_bytes, s, word, &plan};
+    a.peer = peer;
     if ((rc = k->pull(a, &err))) return fail(rc, err);
     if (check) return check_error_word(word, s, plan);
     return BCAD_CU_OK;
 }
+}  // namespace
 
 int bcad_cu_scatter_add(int dtype, void* acc, const bcad_cu_shape* acc_shape, const void* contrib,
                         const bcad_cu_shape* contrib_shape, int zero_first, void* stream) {
@@ -706,6 +726,131 @@ int bcad_cu_stream_wait_event(void* stream, void* event) {
     CU_TRY(cudaStreamWaitEvent(static_cast<cudaStream_t>(stream), static_cast<cudaEvent_t>(event), 0),
            "cudaStreamWaitEvent");
     return BCAD_CU_OK;
+}
+
+// ------------------------------------------------------ peer groups
+// One buffer per rank, exported by CUDA IPC and mapped by every other rank
+// (ranks in the same process pass the raw pointer). Layout (PeerParams):
+// slots [2][world][n] fp64 | flags [world] u64 | step counter u64 | arrival u32.
+struct bcad_cu_peer_group_s {
+    int rank = 0, world = 0, device = 0;
+    size_t n = 0;
+    void* buf = nullptr;  // this rank's buffer
+    std::vector<void*> opened;  // peers' buffers mapped by IPC (closed on destroy)
+    PeerParams params{};
+    bool connected = false;
+};
+
+namespace {
+struct PeerHandle {  // BCAD_CU_PEER_HANDLE_BYTES, rank-order array in connect
+    uint64_t magic;
+    int32_t pid, device;
+    uint64_t ptr, n, world;
+    cudaIpcMemHandle_t ipc;
+};
+static_assert(sizeof(PeerHandle) <= BCAD_CU_PEER_HANDLE_BYTES, "peer handle blob too small");
+constexpr uint64_t kPeerMagic = 0x62636164'70656572ull;  // "bcadpeer"
+
+size_t peer_bytes(int world, size_t n) { return (2 * size_t(world) * n + world + 2) * 8; }
+
+void peer_pointers(void* base, int world, size_t n, double** slots, unsigned long long** flags,
+                   unsigned long long** epoch, unsigned int** arrive) {
+    char* b = static_cast<char*>(base);
+    *slots = reinterpret_cast<double*>(b);
+    *flags = reinterpret_cast<unsigned long long*>(b + 2 * size_t(world) * n * 8);
+    *epoch = *flags + world;
+    *arrive = reinterpret_cast<unsigned int*>(*epoch + 1);
+}
+}  // namespace
+
+int bcad_cu_peer_group_create(int rank, int world, size_t max_elems, bcad_cu_peer_group* out,
+                              unsigned char handle[BCAD_CU_PEER_HANDLE_BYTES]) {
+    if (!out || !handle) return fail(BCAD_CU_ERR_CONFIG, "null argument");
+    if (world < 1 || world > kMaxPeers || rank < 0 || rank >= world)
+        return fail(BCAD_CU_ERR_CONFIG, "peer group: rank / world outside [0, world) / [1, 8]");
+    if (max_elems < 1) return fail(BCAD_CU_ERR_CONFIG, "peer group: max_elems must be >= 1");
+    auto* g = new bcad_cu_peer_group_s();
+    g->rank = rank;
+    g->world = world;
+    g->n = max_elems;
+    if (cudaGetDevice(&g->device) != cudaSuccess || cudaMalloc(&g->buf, peer_bytes(world, max_elems)) != cudaSuccess ||
+        cudaMemset(g->buf, 0, peer_bytes(world, max_elems)) != cudaSuccess || cudaDeviceSynchronize() != cudaSuccess) {
+        const cudaError_t e = cudaGetLastError();
+        if (g->buf) cudaFree(g->buf);
+        delete g;
+        return cuda_fail(e, "peer group buffer");
+    }
+    PeerHandle h{};
+    h.magic = kPeerMagic;
+    h.pid = int32_t(getpid());
+    h.device = g->device;
+    h.ptr = reinterpret_cast<uint64_t>(g->buf);
+    h.n = max_elems;
+    h.world = uint64_t(world);
+    if (cudaIpcGetMemHandle(&h.ipc, g->buf) != cudaSuccess) {
+        const cudaError_t e = cudaGetLastError();
+        cudaFree(g->buf);
+        delete g;
+        return cuda_fail(e, "cudaIpcGetMemHandle");
+    }
+    std::memset(handle, 0, BCAD_CU_PEER_HANDLE_BYTES);
+    std::memcpy(handle, &h, sizeof(h));
+    *out = g;
+    return BCAD_CU_OK;
+}
+
+int bcad_cu_peer_group_connect(bcad_cu_peer_group g, const unsigned char* handles) {
+    if (!g || !handles) return fail(BCAD_CU_ERR_CONFIG, "null argument");
+    if (g->connected) return fail(BCAD_CU_ERR_CONFIG, "peer group already connected");
+    PeerParams& q = g->params;
+    q = PeerParams{};
+    q.rank = g->rank;
+    q.world = g->world;
+    q.n = int64_t(g->n);
+    for (int k = 0; k < g->world; ++k) {
+        PeerHandle h;
+        std::memcpy(&h, handles + size_t(k) * BCAD_CU_PEER_HANDLE_BYTES, sizeof(h));
+        if (h.magic != kPeerMagic || h.world != uint64_t(g->world) || h.n != g->n)
+            return fail(BCAD_CU_ERR_CONFIG, "peer handle " + std::to_string(k) + " is not from a group of the same world / size");
+        void* base = nullptr;
+        if (k == g->rank) {
+            base = g->buf;
+        } else if (h.pid == int32_t(getpid())) {
+            base = reinterpret_cast<void*>(h.ptr);  // a rank in this process
+        } else {
+            CU_TRY(cudaIpcOpenMemHandle(&base, h.ipc, cudaIpcMemLazyEnablePeerAccess), "cudaIpcOpenMemHandle");
+            g->opened.push_back(base);
+        }
+        double* slots;
+        unsigned long long *flags, *epoch;
+        unsigned int* arrive;
+        peer_pointers(base, g->world, g->n, &slots, &flags, &epoch, &arrive);
+        q.slots[k] = slots;
+        q.flags[k] = flags;
+        if (k == g->rank) {
+            q.epoch = epoch;
+            q.arrive = arrive;
+        }
+    }
+    g->connected = true;
+    return BCAD_CU_OK;
+}
+
+int bcad_cu_peer_group_destroy(bcad_cu_peer_group g) {
+    if (!g) return BCAD_CU_OK;
+    for (void* p : g->opened) cudaIpcCloseMemHandle(p);
+    if (g->buf) cudaFree(g->buf);
+    delete g;
+    return BCAD_CU_OK;
+}
+
+int bcad_cu_pullback_allreduce(bcad_cu_kernel k, int dtype, int n_in, const bcad_cu_shape* in_shapes, int m_out,
+                               const void* const* out_adj, const void* const* partials, const void* const* in,
+                               void* const* in_adj, const unsigned char* accumulate, void* workspace,
+                               size_t workspace_bytes, bcad_cu_peer_group group, void* stream) {
+    if (!group || !group->connected) return fail(BCAD_CU_ERR_CONFIG, "peer group not connected");
+    return pullback_impl(k, dtype, n_in, in_shapes, m_out, out_adj, partials, in, in_adj, accumulate, workspace,
+                         workspace_bytes, stream, &group->params);
 }
 
 // ------------------------------------------------------------------ NCCL

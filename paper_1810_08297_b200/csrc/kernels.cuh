@@ -413,6 +413,7 @@ struct Pull2DParams {
     // Completion tickets of the in-kernel combination ([n_col_tiles] column
     // strips, [n_row_tiles] row tiles, [1] whole grid); null = K2f combines.
     unsigned int* tickets;
+    int col_to_ws;        // column sums always leave fp64 partials (fused peer allreduce)
     unsigned long long* err;
 };
 
@@ -788,7 +789,7 @@ __global__ void __launch_bounds__(kThreads, kPipe ? 2 : (kRecompute ? kRecompute
                 double sacc = 0.0;
                 for (int y = 0; y < p.ty; ++y) sacc += col_acc[(size_t(a) * kThreads + (y << p.txv_shift) + txi) * V + v];
                 const int j = p.col_j[a];
-                if (p.n_row_tiles == 1) p.adj[j][c] = finish<T>(sacc, p.adj[j] + c, (p.acc_mask >> j) & 1u);
+                if (p.n_row_tiles == 1 && !p.col_to_ws) p.adj[j][c] = finish<T>(sacc, p.adj[j] + c, (p.acc_mask >> j) & 1u);
                 else p.ws_col[(size_t(a) * p.n_row_tiles + rt) * p.cols + c] = sacc;
             }
         }
@@ -866,6 +867,103 @@ __global__ void __launch_bounds__(kThreads) pull_finish_kernel(const __grid_cons
     }
     const bool is_row = b < row_blocks;
     combine_group(p, is_row, (is_row ? b : b - row_blocks) * 32, is_row ? row_items : col_items, part);
+}
+
+// ------------------------------------------------ fused peer allreduce
+__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p) {
+    unsigned long long v;
+    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned long long v) {
+    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long global_ns() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+
+// K2f-AR: K2's cross-CTA combination fused with the allreduce of the
+// batch-broadcast (column-class) adjoints over a peer-memory group, in place
+// of K2f + ncclAllReduce. Row-class groups are combined locally as in K2f.
+// Each column group's CTA sums its 32 elements' tile partials (fp64, fixed
+// order) and stores them straight into slot `rank` of EVERY rank's buffer
+// (NVLink peer stores; the buffers were exchanged once by CUDA IPC). The last
+// arriving CTA publishes a step-counter flag to every rank (release, system
+// scope), waits for every rank's flag (acquire), then adds the world's slots
+// in rank order — identical bits on every rank — and writes the adjoints
+// (one fp32 rounding of the fp64 world sum). Double-buffered by step parity:
+// a rank can run at most one step ahead of another, so a fast rank's next
+// stores never land in the slots being read. A peer that never arrives traps
+// after 30 s instead of hanging the device.
+template <int N, int M, class T>
+__global__ void __launch_bounds__(kThreads) pull_finish_ar_kernel(const __grid_constant__ Pull2DParams<N, M, T> p,
+                                                                  const __grid_constant__ bcad_cu_impl::PeerParams q) {
+    pdl_wait();
+    __shared__ double part[kThreads];
+    __shared__ unsigned long long s_epoch;
+    __shared__ int s_last;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t row_items = p.n_col_tiles > 1 ? int64_t(p.n_row_args) * p.rows : 0;
+    const int64_t col_items = int64_t(p.n_col_args) * p.cols;
+    const int64_t row_blocks = (row_items + 31) / 32, col_blocks = (col_items + 31) / 32;
+    const int64_t b = blockIdx.x;
+    if (b < row_blocks) {
+        combine_group(p, true, b * 32, row_items, part);
+        return;
+    }
+    if (threadIdx.x == 0) s_epoch = *reinterpret_cast<volatile unsigned long long*>(q.epoch);
+    // local fp64 sums of this group's 32 column elements (combine_group's order)
+    const int64_t it = (b - row_blocks) * 32 + lane;
+    const bool valid = it < col_items;
+    const int a = valid ? int(it / p.cols) : 0;
+    const int64_t e = valid ? it % p.cols : 0;
+    const int n = p.n_row_tiles;
+    const double* base = p.ws_col + size_t(a) * n * p.cols + e;
+    const int per = (n + 7) / 8, q0 = warp * per, q1 = min(n, q0 + per);
+    double acc = 0.0;
+    if (valid)
+        for (int k = q0; k < q1; ++k) acc += base[size_t(k) * p.cols];
+    part[warp * 32 + lane] = acc;
+    __syncthreads();
+    const unsigned long long next = s_epoch + 1;
+    const size_t par = size_t(next & 1u);
+    if (warp == 0 && valid) {
+        double sum = 0.0;
+#pragma unroll
+        for (int g = 0; g < 8; ++g) sum += part[g * 32 + lane];
+        for (int k = 0; k < q.world; ++k) q.slots[k][(par * q.world + q.rank) * size_t(q.n) + it] = sum;
+        __threadfence_system();
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) s_last = atomicAdd(q.arrive, 1u) == unsigned(col_blocks - 1);
+    __syncthreads();
+    if (!s_last) return;
+    // the last CTA of this rank: publish, wait for every rank, add in rank order
+    if (threadIdx.x == 0) __threadfence_system();
+    __syncthreads();
+    if (threadIdx.x < q.world) {
+        st_release_sys(q.flags[threadIdx.x] + q.rank, next);
+        const unsigned long long t0 = global_ns();
+        while (ld_acquire_sys(q.flags[q.rank] + threadIdx.x) < next)
+            if (global_ns() - t0 > 30000000000ull) __trap();  // a peer never arrived
+    }
+    __syncthreads();
+    const double* mine = q.slots[q.rank] + par * q.world * size_t(q.n);
+    for (int64_t i = threadIdx.x; i < col_items; i += kThreads) {
+        double sum = 0.0;
+        for (int k = 0; k < q.world; ++k) sum += __ldcv(mine + size_t(k) * q.n + i);
+        const int aa = int(i / p.cols);
+        const int64_t c = i % p.cols;
+        const int j = p.col_j[aa];
+        p.adj[j][c] = finish<T>(sum, p.adj[j] + c, (p.acc_mask >> j) & 1u);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        *q.arrive = 0u;
+        *reinterpret_cast<volatile unsigned long long*>(q.epoch) = next;
+    }
 }
 
 // Blocks of pull_finish_kernel for a tiling (0 = nothing to combine).

@@ -292,8 +292,26 @@ int launch_pull2d(const PullArgs& a, std::string* err) {
     int64_t fin_blocks = bcad_dev::pull_finish_blocks(plan.rows, plan.cols, p.n_row_tiles, p.n_col_tiles, nr, nc, ns);
     // cross-CTA reductions combined inside K2 (completion tickets) unless the
     // tiling asks for the separate K2f launch
-    if (fin_blocks > 0 && pull_combine_in_kernel(t, nr, nc, ns)) {
+    if (fin_blocks > 0 && pull_combine_in_kernel(t, nr, nc, ns) && !a.peer) {
         p.tickets = reinterpret_cast<unsigned int*>(ws + L.ws_tickets);
+        fin_blocks = 0;
+    }
+    // fused allreduce over a peer group: column sums always leave fp64
+    // partials, and K2f-AR replaces K2f (+ the collective)
+    int64_t ar_blocks = 0;
+    if (a.peer) {
+        if (nc == 0 || (ns > 0 && t.n_ctas > 1)) {
+            *err = "fused peer allreduce: the problem needs (1,H)-class (column) reductions and no scalar ones";
+            return BCAD_CU_ERR_CONFIG;
+        }
+        if (int64_t(nc) * plan.cols > a.peer->n) {
+            *err = "fused peer allreduce: " + std::to_string(int64_t(nc) * plan.cols) +
+                   " reduced elements exceed the peer group's " + std::to_string(a.peer->n);
+            return BCAD_CU_ERR_CONFIG;
+        }
+        p.col_to_ws = 1;
+        ar_blocks = (t.n_col_tiles > 1 && nr > 0 ? (int64_t(nr) * plan.rows + 31) / 32 : 0) +
+                    (int64_t(nc) * plan.cols + 31) / 32;
         fin_blocks = 0;
     }
     const size_t smem = pull_smem_bytes(nc, nr, ns, t);
@@ -319,7 +337,20 @@ int launch_pull2d(const PullArgs& a, std::string* err) {
             if (e != cudaSuccess) return cuda_status(e, err);
         }
         int rc = cuda_status(launch_pdl(kern, grid, smem, a.stream, p), err);
-        if (rc || fin_blocks == 0 || t.skip_finish) return rc;
+        if (rc) return rc;
+        if (ar_blocks > 0) {
+            cudaLaunchConfig_t cfg = {};
+            cfg.gridDim = dim3(unsigned(ar_blocks));
+            cfg.blockDim = dim3(kThreads);
+            cfg.stream = a.stream;
+            cudaLaunchAttribute attr[1];
+            attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+            attr[0].val.programmaticStreamSerializationAllowed = 1;
+            cfg.attrs = attr;
+            cfg.numAttrs = 1;
+            return cuda_status(cudaLaunchKernelEx(&cfg, &bcad_dev::pull_finish_ar_kernel<N, M, T>, p, *a.peer), err);
+        }
+        if (fin_blocks == 0 || t.skip_finish) return rc;
         return cuda_status(launch_pdl(&bcad_dev::pull_finish_kernel<N, M, T>, dim3(unsigned(fin_blocks)), 0,
                                       a.stream, p), err);
     });
@@ -342,6 +373,10 @@ int launch_pull_t(const PullArgs& a, std::string* err) {
     for (int j = 0; j < N && recompute && vec; ++j)
         if ((plan.cls[j] == kFull || plan.cls[j] == kCol) && !aligned16(a.in[j])) vec = false;
     if (vec) return launch_pull2d<Body, T, V, Sigs...>(a, err);
+    if (a.peer && !pull_scalar2d_ok<T>(plan)) {
+        *err = "fused peer allreduce needs a 2-D (rows x cols) problem";
+        return BCAD_CU_ERR_CONFIG;
+    }
     // odd widths / unaligned views of a 2-D problem: the same tiled kernel, one
     // cell per thread (when the caller's workspace fits that layout)
     if (pull_scalar2d_ok<T>(plan) &&
@@ -422,4 +457,13 @@ using SigAllFull = typename SigAllFullT<N>::type;
         Body::kName, Body::kIn, Body::kOut, Body::kMayRaise,                                           \
             &bcad_cu_impl::launch_fwd_any<Body __VA_OPT__(, ) __VA_ARGS__>,                             \
             &bcad_cu_impl::launch_pull_any<Body __VA_OPT__(, ) __VA_ARGS__>                             \
+    }
+
+// A registered body whose forward also gets signature S but whose pullback
+// dispatches on runtime classes only (wide bodies: their static pullback
+// instantiations dominate compile time for no benchmarked use).
+#define BCAD_ENTRY_FWD_SIG(Body, S)                                                                    \
+    bcad_cu_kernel_entry {                                                                             \
+        Body::kName, Body::kIn, Body::kOut, Body::kMayRaise, &bcad_cu_impl::launch_fwd_any<Body, S>,    \
+            &bcad_cu_impl::launch_pull_any<Body>                                                       \
     }

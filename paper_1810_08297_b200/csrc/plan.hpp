@@ -299,7 +299,8 @@ inline PullLayout pull_layout(const Plan& p, const Tiling& t) {
     L.ws_row = off;
     if (t.n_col_tiles > 1) off += align256(size_t(L.n_row_args) * t.n_col_tiles * p.rows * 8);
     L.ws_col = off;
-    if (t.n_row_tiles > 1) off += align256(size_t(L.n_col_args) * t.n_row_tiles * p.cols * 8);
+    // (one tile row too: the fused peer allreduce reads fp64 column partials)
+    if (L.n_col_args > 0) off += align256(size_t(L.n_col_args) * t.n_row_tiles * p.cols * 8);
     L.ws_scalar = off;
     if (t.n_ctas > 1) off += align256(size_t(L.n_scalar_args) * t.n_ctas * 8);
     L.ws_tickets = off;
@@ -313,6 +314,21 @@ inline PullLayout pull_layout(const Plan& p, const Tiling& t) {
 }
 
 constexpr size_t kMaxPullSmem = 160 * 1024;
+
+// Peer-memory group of the fused pullback allreduce (abi.cu
+// bcad_cu_peer_group_*, kernels.cuh pull_finish_ar_kernel): every rank's
+// buffer holds, per parity of the step counter, [world][n] fp64 slots (rank
+// k's local column sums land in slot k of every rank), then [world] arrival
+// flags, the local step counter and the local CTA arrival counter.
+constexpr int kMaxPeers = 8;
+struct PeerParams {
+    double* slots[kMaxPeers];                // rank k's slot region [2][world][n]
+    unsigned long long* flags[kMaxPeers];    // rank k's flags [world]
+    unsigned long long* epoch;               // this rank's step counter
+    unsigned int* arrive;                    // this rank's CTA arrival counter
+    int rank, world;
+    int64_t n;                               // elements per slot (max_elems of the group)
+};
 
 template <class T>
 constexpr int vec_width() { return 16 / int(sizeof(T)); }

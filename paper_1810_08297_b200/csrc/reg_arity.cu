@@ -1,4 +1,6 @@
-// Registration group: the arity-scaling workload tanh_product_<A>
+// Registration group: the arity-scaling workload tanh_product_<A>, A <= 8
+// (the wide arities are in reg_arity_wide*.cu: separate translation units
+// compile in parallel)
 // (proj/include/bcad/arity_workload.hpp:19-28; paper Fig. 3 register study).
 #include "bodies.cuh"
 #include "launch.cuh"
@@ -10,10 +12,8 @@
 // A16 0.71 -> 0.93, A18 0.71 -> 0.92, A32 0.62 -> 0.79.
 using bcad_cu_impl::SigAllFull;
 static const bcad_cu_kernel_entry kEntries[] = {
-    BCAD_ENTRY(bcad_dev::KTanhProduct<1>, SigAllFull<1>),   BCAD_ENTRY(bcad_dev::KTanhProduct<2>, SigAllFull<2>),
-    BCAD_ENTRY(bcad_dev::KTanhProduct<4>, SigAllFull<4>),   BCAD_ENTRY(bcad_dev::KTanhProduct<8>, SigAllFull<8>),
-    BCAD_ENTRY(bcad_dev::KTanhProduct<16>, SigAllFull<16>), BCAD_ENTRY(bcad_dev::KTanhProduct<18>, SigAllFull<18>),
-    BCAD_ENTRY(bcad_dev::KTanhProduct<32>, SigAllFull<32>),
+    BCAD_ENTRY(bcad_dev::KTanhProduct<1>, SigAllFull<1>), BCAD_ENTRY(bcad_dev::KTanhProduct<2>, SigAllFull<2>),
+    BCAD_ENTRY(bcad_dev::KTanhProduct<4>, SigAllFull<4>), BCAD_ENTRY(bcad_dev::KTanhProduct<8>, SigAllFull<8>),
 };
 
 int bcad_reg_arity(const bcad_cu_kernel_entry** out) {

@@ -36,6 +36,7 @@ struct PullArgs {
     unsigned long long* err;
     const Plan* plan;
     const Tiling* tiling = nullptr;  // tuning override (tests / scripts/lab); null = choose_tiling
+    const PeerParams* peer = nullptr;  // fused allreduce of the (1,H)-class adjoints over a peer group
 };
 
 size_t pull_ws_any(const Plan& plan, int dtype);
@@ -55,4 +56,6 @@ int bcad_reg_hmlstm(const bcad_cu_kernel_entry** out);
 int bcad_reg_pool(const bcad_cu_kernel_entry** out);
 int bcad_reg_probe(const bcad_cu_kernel_entry** out);
 int bcad_reg_arity(const bcad_cu_kernel_entry** out);
+int bcad_reg_arity_wide(const bcad_cu_kernel_entry** out);
+int bcad_reg_arity_wide32(const bcad_cu_kernel_entry** out);
 int bcad_reg_prims(const bcad_cu_kernel_entry** out);

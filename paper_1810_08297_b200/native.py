@@ -156,6 +156,10 @@ PROTOS = {
     "bcad_cu_comm_destroy": (I, [VP]),
     "bcad_cu_comm_count": (I, [VP, C.POINTER(I)]),
     "bcad_cu_allreduce_adjoints": (I, [VP, VP, I, I, VP, VP]),
+    "bcad_cu_peer_group_create": (I, [I, I, SZ, C.POINTER(VP), C.c_char_p]),
+    "bcad_cu_peer_group_connect": (I, [VP, C.c_char_p]),
+    "bcad_cu_peer_group_destroy": (I, [VP]),
+    "bcad_cu_pullback_allreduce": (I, [VP, I, I, VP, I, VP, VP, VP, VP, VP, VP, SZ, VP, VP]),
 }
 
 
@@ -350,12 +354,52 @@ class Comm:
             self.handle = VP()
 
 
+PEER_HANDLE_BYTES = 128
+
+
+class PeerGroup:
+    """Peer-memory group of the fused pullback allreduce
+    (bcad_cu_peer_group_*): create on every rank, gather every rank's
+    `handle` in rank order, connect."""
+
+    def __init__(self, rank: int, world: int, max_elems: int):
+        self.handle = VP()
+        buf = C.create_string_buffer(PEER_HANDLE_BYTES)
+        check(LIB.bcad_cu_peer_group_create(rank, world, max_elems, C.byref(self.handle), buf))
+        self.blob = buf.raw
+        self.rank, self.world = rank, world
+
+    def connect(self, blobs):
+        assert len(blobs) == self.world and all(len(b) == PEER_HANDLE_BYTES for b in blobs)
+        check(LIB.bcad_cu_peer_group_connect(self.handle, b"".join(blobs)))
+
+    def close(self):
+        if self.handle:
+            check(LIB.bcad_cu_peer_group_destroy(self.handle))
+            self.handle = VP()
+
+
+def pullback_allreduce(kernel: Kernel, shapes, out_adj, partials, inputs, in_adj, group: PeerGroup,
+                       accumulate=None, workspace=None, stream=None):
+    """bcad_cu_pullback_allreduce: the pullback with the (1,H)-class adjoints
+    summed over the peer group inside its last kernel."""
+    n = len(shapes)
+    acc = (C.c_ubyte * max(1, n))(*[int(bool(a)) for a in (accumulate or [0] * n)])
+    ws_bytes = 0 if workspace is None else workspace.numel() * workspace.element_size()
+    check(LIB.bcad_cu_pullback_allreduce(kernel.handle, _dtype_code(out_adj[0]), n, _shape_array(shapes), kernel.m_out,
+                                         _ptr_array([_dptr(t) for t in out_adj]),
+                                         _ptr_array([_dptr(t) for t in partials]) if partials is not None else None,
+                                         _ptr_array([_dptr(t) for t in inputs]) if inputs is not None else None,
+                                         _ptr_array([_dptr(t) for t in in_adj]), acc, _dptr(workspace), ws_bytes,
+                                         group.handle, _stream_ptr(stream)))
+
+
 class PreparedStep:
     """A mixed-node step with every ctypes argument array built once, so the
     per-step host cost is two foreign calls (bench / graph capture)."""
 
     def __init__(self, kernel: Kernel, inputs, primal, partials, seeds, in_adj, workspace, accumulate=None,
-                 policy: int = CACHE_FORWARD):
+                 policy: int = CACHE_FORWARD, peer: "PeerGroup | None" = None):
         self.k = kernel
         self.dt = _dtype_code(inputs[0])
         self.n = len(inputs)
@@ -368,6 +412,7 @@ class PreparedStep:
         self.acc = (C.c_ubyte * max(1, self.n))(*[int(bool(a)) for a in (accumulate or [0] * self.n)])
         self.ws = _dptr(workspace)
         self.ws_bytes = workspace.numel() * workspace.element_size()
+        self.peer = peer
         self._keep = (inputs, primal, partials, seeds, in_adj, workspace)
 
     def forward(self, stream_ptr):
@@ -375,5 +420,10 @@ class PreparedStep:
                                   self.parts, stream_ptr))
 
     def pullback(self, stream_ptr):
+        if self.peer is not None:  # fused K2f + allreduce over the peer group
+            check(LIB.bcad_cu_pullback_allreduce(self.k.handle, self.dt, self.n, self.shapes, self.k.m_out, self.seeds,
+                                                 self.parts, self.ins, self.adj, self.acc, self.ws, self.ws_bytes,
+                                                 self.peer.handle, stream_ptr))
+            return
         check(LIB.bcad_cu_pullback(self.k.handle, self.dt, self.n, self.shapes, self.k.m_out, self.seeds, self.parts,
                                    self.ins, self.adj, self.acc, self.ws, self.ws_bytes, stream_ptr))
