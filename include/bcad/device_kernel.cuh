@@ -35,7 +35,8 @@
 // BCAD_DEVICE_KERNEL_NOTHROW declares a body free of those operations (no
 // check, fully asynchronous, graph-capturable). Both evaluate every cell on
 // its own (no lane-vector evaluation across cells), which is correct for any
-// branch structure.
+// branch structure; BCAD_DEVICE_KERNEL_NOTHROW_P declares which arguments
+// the branches read, enabling the lane-vector evaluation (below).
 #pragma once
 
 #include <cstdio>
@@ -52,11 +53,20 @@ namespace bcad_dev {
 // Static registration object: one per BCAD_DEVICE_KERNEL.
 template <class Body>
 struct DeviceKernelRegistration {
+    static bcad_cu_kernel_entry make_entry() {
+        // a body declaring its branch arguments (..._P) also gets the layout
+        // in which exactly those are (B)-shaped, the lane-vector fast path
+        if constexpr (Body::kPredicateArgs != ~0u && Body::kPredicateArgs != 0u)
+            return BCAD_ENTRY(Body, bcad_cu_impl::SigAllFull<Body::kIn>,
+                              bcad_cu_impl::SigPredRow<Body::kIn, Body::kPredicateArgs>);
+        else
+            return BCAD_ENTRY(Body, bcad_cu_impl::SigAllFull<Body::kIn>);
+    }
     DeviceKernelRegistration() {
         // runtime argument classes, plus the all-full-shape signature for
         // elementwise calls (no per-argument class branches; measured 10-30%
         // faster on the library's wide bodies, csrc/reg_arity.cu)
-        static const bcad_cu_kernel_entry entry = BCAD_ENTRY(Body, bcad_cu_impl::SigAllFull<Body::kIn>);
+        static const bcad_cu_kernel_entry entry = make_entry();
         if (bcad_cu_register_kernel(&entry) != BCAD_CU_OK) {
             std::fprintf(stderr, "bcad: cannot register device kernel '%s': %s\n", Body::kName, bcad_cu_last_error());
             std::abort();
@@ -66,14 +76,14 @@ struct DeviceKernelRegistration {
 
 }  // namespace bcad_dev
 
-#define BCAD_DEVICE_KERNEL_IMPL_(ID, NAME, NIN, NOUT, RAISES, ...)                              \
+#define BCAD_DEVICE_KERNEL_IMPL_(ID, NAME, NIN, NOUT, RAISES, PRED, ...)                        \
     namespace bcad_dev {                                                                       \
     namespace user_bodies {                                                                    \
     struct ID {                                                                                \
         static constexpr const char* kName = NAME;                                             \
         static constexpr int kIn = NIN, kOut = NOUT;                                           \
         static constexpr bool kMayRaise = RAISES;                                              \
-        static constexpr uint32_t kPredicateArgs = ~0u;                                        \
+        static constexpr uint32_t kPredicateArgs = PRED;                                       \
         static constexpr bool kSelectForm = false;                                             \
         template <class S>                                                                     \
         BCAD_HD static void body(const S* in, S* out) { __VA_ARGS__; }                        \
@@ -84,6 +94,15 @@ struct DeviceKernelRegistration {
     }                                                                                          \
     static const ::bcad_dev::DeviceKernelRegistration<::bcad_dev::user_bodies::ID> bcad_user_kernel_##ID;
 
-#define BCAD_DEVICE_KERNEL(ID, NAME, NIN, NOUT, ...) BCAD_DEVICE_KERNEL_IMPL_(ID, NAME, NIN, NOUT, true, __VA_ARGS__)
+#define BCAD_DEVICE_KERNEL(ID, NAME, NIN, NOUT, ...) \
+    BCAD_DEVICE_KERNEL_IMPL_(ID, NAME, NIN, NOUT, true, ~0u, __VA_ARGS__)
 #define BCAD_DEVICE_KERNEL_NOTHROW(ID, NAME, NIN, NOUT, ...) \
-    BCAD_DEVICE_KERNEL_IMPL_(ID, NAME, NIN, NOUT, false, __VA_ARGS__)
+    BCAD_DEVICE_KERNEL_IMPL_(ID, NAME, NIN, NOUT, false, ~0u, __VA_ARGS__)
+// PRED: bitmask of the arguments the body's comparisons read (0 for a
+// branch-free body). When every one of them is constant along the output's
+// last axis for a call (broadcast (B)-shaped or scalar), each thread
+// evaluates its 4 (fp32) / 2 (fp64) cells as ONE lane-vector dual, taking
+// the branch once — the HM-LSTM bodies' fast path. ~0u (the default above)
+// is always correct.
+#define BCAD_DEVICE_KERNEL_NOTHROW_P(ID, NAME, NIN, NOUT, PRED, ...) \
+    BCAD_DEVICE_KERNEL_IMPL_(ID, NAME, NIN, NOUT, false, PRED, __VA_ARGS__)

@@ -69,10 +69,12 @@ def _stamp_path(target: str) -> str:
     return os.path.join(BUILD, "stamps", os.path.relpath(target, ROOT).replace(os.sep, "__") + ".stamp")
 
 
-def _stamp(target: str, deps: list[str], cmd: list[str]):
+def _stamp(target: str, deps: list[str], cmd: list[str], digest: str | None = None):
+    """Record the digest taken BEFORE the compile started (`digest`), so a
+    source edited while it compiled is rebuilt next time."""
     os.makedirs(os.path.join(BUILD, "stamps"), exist_ok=True)
     with open(_stamp_path(target), "w") as f:
-        f.write(_digest(deps, cmd) + "\n")
+        f.write((digest or _digest(deps, cmd)) + "\n")
 
 
 def _run(cmd: list[str], verbose: bool):
@@ -96,12 +98,12 @@ def build_cuda(verbose: bool = False, jobs: int | None = None) -> str:
         objs.append(obj)
         cmd = [nvcc(), *NVCC_FLAGS, "-c", src, "-o", obj]
         if _stale(obj, [src] + headers, cmd):
-            todo.append((obj, [src] + headers, cmd))
+            todo.append((obj, [src] + headers, cmd, _digest([src] + headers, cmd)))
     jobs = jobs or max(1, min(len(todo), os.cpu_count() or 4))
     with cf.ThreadPoolExecutor(jobs) as ex:
-        for (obj, deps, cmd), f in [(t, ex.submit(_run, t[2], verbose)) for t in todo]:
+        for (obj, deps, cmd, dg), f in [(t, ex.submit(_run, t[2], verbose)) for t in todo]:
             f.result()
-            _stamp(obj, deps, cmd)
+            _stamp(obj, deps, cmd, dg)
     link = [nvcc(), "-shared", *ARCH, "-o", LIB, *objs, "-ldl", "-Xcompiler", "-fPIC"]
     if todo or _stale(LIB, objs, link):
         _run(link, verbose)
@@ -118,8 +120,9 @@ def build_host(verbose: bool = False) -> str:
     cmd = [cxx(), "-std=c++20", "-O2", "-fPIC", "-shared", "-Wall", "-Wextra", "-I" + INCLUDE, *srcs,
            "-o", HOST_LIB, "-L" + PKG, "-lbcad_cu", "-Wl,-rpath,$ORIGIN"]
     if _stale(HOST_LIB, deps, cmd):
+        dg = _digest(deps, cmd)
         _run(cmd, verbose)
-        _stamp(HOST_LIB, deps, cmd)
+        _stamp(HOST_LIB, deps, cmd, dg)
     main = os.path.join(CSRC, "bench_main.cpp")
     cmd = [cxx(), "-std=c++20", "-O2", "-Wall", "-Wextra", "-I" + INCLUDE, main, "-o", BENCH_EXE, "-L" + PKG,
            "-lbcad_host", "-lbcad_cu", "-Wl,-rpath,$ORIGIN/.."]
@@ -141,8 +144,9 @@ def build_cpp_tests(verbose: bool = False) -> list[str]:
         cmd = [cxx(), "-std=c++20", "-O2", "-Wall", "-Wextra", "-I" + INCLUDE, "-I" + tdir, src, "-o", exe,
                "-L" + PKG, "-lbcad_host", "-lbcad_cu", "-Wl,-rpath,$ORIGIN/../../../paper_1810_08297_b200"]
         if _stale(exe, deps, cmd):
+            dg = _digest(deps, cmd)
             _run(cmd, verbose)
-            _stamp(exe, deps, cmd)
+            _stamp(exe, deps, cmd, dg)
         out.append(exe)
     # nvcc test programs: user device bodies registered through bcad/device_kernel.cuh
     for src in sorted(glob.glob(os.path.join(tdir, "test_*.cu"))):
@@ -153,8 +157,9 @@ def build_cpp_tests(verbose: bool = False) -> list[str]:
         cmd = [nvcc(), *NVCC_FLAGS, "-I" + tdir, src, "-o", exe, "-L" + PKG, "-lbcad_cu",
                "-Xlinker", "-rpath,$ORIGIN/../../../paper_1810_08297_b200"]
         if _stale(exe, deps, cmd):
+            dg = _digest(deps, cmd)
             _run(cmd, verbose)
-            _stamp(exe, deps, cmd)
+            _stamp(exe, deps, cmd, dg)
         out.append(exe)
     out += build_ref_suites_b200(verbose)
     return out
@@ -193,11 +198,11 @@ def build_ref_suites_b200(verbose: bool = False) -> list[str]:
         objs.append(obj)
         cmd = flags + ["-c", src, "-o", obj]
         if _stale(obj, [src] + hdrs, cmd):
-            todo.append((obj, [src] + hdrs, cmd))
+            todo.append((obj, [src] + hdrs, cmd, _digest([src] + hdrs, cmd)))
     with cf.ThreadPoolExecutor(max(1, min(len(todo), os.cpu_count() or 4))) as ex:
-        for (obj, deps, cmd), f in [(t, ex.submit(_run, t[2], verbose)) for t in todo]:
+        for (obj, deps, cmd, dg), f in [(t, ex.submit(_run, t[2], verbose)) for t in todo]:
             f.result()
-            _stamp(obj, deps, cmd)
+            _stamp(obj, deps, cmd, dg)
     link = [cxx(), "-o", REF_SUITES_B200, *objs, "-L" + PKG, "-lbcad_cu",
             "-Wl,-rpath,$ORIGIN/../../../paper_1810_08297_b200"]
     if todo or _stale(REF_SUITES_B200, objs + [LIB], link):

@@ -159,8 +159,8 @@ struct KTanhProduct {  // arity_workload.hpp:19-28
     // signature (reg_arity.cu) at 4096^2 fp32 (scripts/lab "arity",
     // "arity32", means; profiles/r02/lab_arity_static.jsonl): A <= 8 best at
     // 2 rows (A4 0.96, A8 0.99 of the copy peak), A = 16 / 18 at 4 (0.93 /
-    // 0.92), A = 32 at 8 (0.79).
-    static constexpr int kFwdRows = A >= 32 ? 8 : A >= 16 ? 4 : 2;
+    // 0.92), A = 32 at 16 (0.795; 8 rows 0.787, 32 rows 0.777 — lab "arity32").
+    static constexpr int kFwdRows = A >= 32 ? 16 : A >= 16 ? 4 : 2;
     // lab A/B of the K1 register pipeline for wide bodies: 0 = next-row
     // pipeline (default; with the static signature A = 32 runs 0.793 with it
     // against 0.778 without it at >= 3 CTAs per SM); 1 = no pipeline for

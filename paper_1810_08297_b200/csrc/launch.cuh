@@ -449,6 +449,17 @@ struct SigAllFullT<N, std::integer_sequence<int, I...>> {
 };
 template <int N>
 using SigAllFull = typename SigAllFullT<N>::type;
+// The arguments in PRED broadcast along the last axis ((B)-shaped, ROW), the
+// others full-shape: the layout of a body branching on per-row flags (the
+// HM-LSTM boundary bits), whose cells then evaluate as lane vectors.
+template <int N, uint32_t PRED, class Seq = std::make_integer_sequence<int, N>>
+struct SigPredRowT;
+template <int N, uint32_t PRED, int... I>
+struct SigPredRowT<N, PRED, std::integer_sequence<int, I...>> {
+    using type = Sig<(((PRED >> I) & 1u) ? int(kRow) : int(kFull))...>;
+};
+template <int N, uint32_t PRED>
+using SigPredRow = typename SigPredRowT<N, PRED>::type;
 
 }  // namespace bcad_cu_impl
 

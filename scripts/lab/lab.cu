@@ -601,7 +601,8 @@ int main(int argc, char** argv) {
         step_ab<KHmlstmBias, float, SigHmlstmBias>("step_cfg3", true, 1024, 1024, {{16, 3}, {16, 5}, {32, 3}});
     }
     if (which == "arity32") {  // A = 32 static signature, rows per thread
-        const std::vector<std::array<int, 2>> t = {{256, 2}, {256, 4}, {256, 8}, {128, 4}, {128, 8}};
+        const std::vector<std::array<int, 2>> t = {{256, 2}, {256, 4}, {256, 8}, {256, 16}, {256, 32}, {128, 4},
+                                                    {128, 8}, {128, 16}, {64, 8}, {64, 16}, {32, 16}};
         k1_sweep<KTanhProduct<32>, float, SigAllFull<32>>("k1_tp32_4096_static", false, 4096, 4096, t, 32);
         k1_sweep<KTanhProduct<1>, float, SigAllFull<1>>("k1_tp1_4096_static", false, 4096, 4096, t, 1);
         k1_sweep<KTanhProduct<4>, float, SigAllFull<4>>("k1_tp4_4096_static", false, 4096, 4096, t, 4);

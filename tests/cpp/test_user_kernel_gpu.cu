@@ -13,6 +13,9 @@
 BCAD_DEVICE_KERNEL_NOTHROW(UserSoftGate, "user_soft_gate", 2, 1,
                            out[0] = sigmoid(in[0]) * tanh(in[1]) + in[0] * in[0])
 BCAD_DEVICE_KERNEL(UserLogRatio, "user_log_ratio", 2, 2, out[0] = log(in[0]) / in[1]; out[1] = in[0] * in[1])
+// branches on argument 1 only (a (B)-shaped gate): lane-vector evaluation when it is row-uniform
+BCAD_DEVICE_KERNEL_NOTHROW_P(UserGatedSoftplus, "user_gated_softplus", 2, 1, 0x2u,
+                             out[0] = in[1] > 0.5 ? log(1.0 + exp(in[0])) : in[0] * sigmoid(in[0]))
 
 namespace {
 // A body under a name the library already has, registered by hand below.
@@ -118,6 +121,40 @@ TEST_CASE("a device-only kernel evaluates on the device, reals and duals") {
     dev.eval(std::span<const Dual<double>>(in, 2), std::span<Dual<double>>(od, 1));
     host.eval(std::span<const Dual<double>>(in, 2), std::span<Dual<double>>(oh, 1));
     for (int j = 0; j < 2; ++j) CHECK(mini::close(od[0].partial_for(tag, j), oh[0].partial_for(tag, j), 1e-13, 1e-15));
+}
+
+TEST_CASE("a user body with declared predicate arguments: lane-vector path equals the per-cell path") {
+    const auto body = [](auto in, auto out) {
+        out[0] = in[1] > 0.5 ? log(1.0 + exp(in[0])) : in[0] * sigmoid(in[0]);
+    };
+    for (int pass = 0; pass < 2; ++pass) {
+        const BroadcastKernel<float> k(2, 1, "user_gated_softplus", body);
+        Rng rng(21);
+        const std::int64_t B = 64, H = 256;
+        const Tensor<float> x = random_pm1<float>(Shape{B, H}, rng);
+        // pass 0: gate of shape (B) (row-uniform -> lane vectors); pass 1: (B, H) (per cell)
+        const Tensor<float> gate = pass == 0 ? random_binary<float>(Shape{B}, rng) : random_binary<float>(Shape{B, H}, rng);
+        const Tensor<float> w = random_pm1<float>(Shape{B, H}, rng);
+        Tape<float> tape;
+        const Var<float> vx = tape.input(x), vg = tape.input(gate);
+        const Var<float> vy = mixed_broadcast(tape, k, {vx, vg}, MixedPolicy::CacheForward)[0];
+        const auto grads = tape.backward(vy, w);
+        const auto hx = x.to_host(), hg = gate.to_host(), hw = w.to_host(), hy = tape.value(vy).to_host();
+        const auto gx = grads.at(vx).to_host(), gg = grads.at(vg).to_host();
+        for (std::int64_t r = 0; r < B; ++r)
+            for (std::int64_t c = 0; c < H; ++c) {
+                const std::size_t e = static_cast<std::size_t>(r * H + c);
+                const float gv = hg[static_cast<std::size_t>(pass == 0 ? r : r * H + c)];
+                const Tag tag = fresh_tag();
+                const float pt[2] = {hx[e], gv};
+                Dual<float> in[2], out[1];
+                seed_into<float>(std::span<const float>(pt, 2), tag, std::span<Dual<float>>(in, 2));
+                k.eval(std::span<const Dual<float>>(in, 2), std::span<Dual<float>>(out, 1));
+                CHECK(mini::close(hy[e], out[0].primal(), 1e-5, 1e-6));
+                CHECK(mini::close(gx[e], hw[e] * out[0].partial_for(tag, 0), 1e-5, 1e-6));
+            }
+        for (float v : gg) CHECK(v == 0.0f);  // the gate only feeds the comparison
+    }
 }
 
 TEST_CASE("a may-raise user body reports the failing output index") {
