@@ -130,7 +130,31 @@ def bench_config(w: Workload, world: int, policy: int) -> dict:
             "policy": "CacheForward" if policy == 0 else "RecomputeReverse",
             "parallelism": (f"batch rows sharded over {world} ranks, allreduce of batch-broadcast adjoints"
                             if world > 1 else "single GPU"),
-            "l2": L2Flush.DESCRIPTION}
+            "l2": l2_description(w, world, policy)}
+
+
+# B200 L2 (126 MB); steps whose bytes are below 4 x this rotate buffer sets.
+L2_BYTES = 126 * 2**20
+
+
+def rotation_sets(step_bytes: int) -> int:
+    """Independent batch buffer sets the timed steps cycle through so that
+    no step starts with its operands in L2: each set is revisited only after
+    >= 2 x L2 of other steps' traffic (R = 1 when one step moves > 4 x L2)."""
+    if step_bytes >= 4 * L2_BYTES:
+        return 1
+    return max(3, math.ceil(2 * L2_BYTES / step_bytes) + 1)
+
+
+def l2_description(w: Workload, world: int, policy: int) -> str:
+    B_local = w.B if scaling_of(w) == "weak" or world == 1 else -(-w.B // world)
+    R = rotation_sets(w.step_bytes(B_local, policy))
+    if R == 1:
+        return ("inputs larger than L2: one step moves > 4 x the 126 MB L2; the K steps run back to back as one "
+                "CUDA graph, no flush")
+    return (f"inputs larger than L2: {R} independent batch buffer sets, step k on set k % {R} (each set revisited "
+            f"after >= 2 x the 126 MB L2 of other steps' traffic); the K steps run back to back as one CUDA graph, "
+            f"no flush")
 
 
 def scaling_of(w: Workload) -> str:
@@ -397,106 +421,111 @@ def run_native(args, w: Workload, rank: int, world: int):
         nccl_nranks = comm.nranks
         assert nccl_nranks == world, (nccl_nranks, world)
 
-    l2 = L2Flush(device)
     K, W = args.steps, args.warmup
-    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(2)] for _ in range(K)]
-    evb = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(K)]
+    # Inputs larger than L2 (the contract's alternative to flushing): R
+    # independent batch buffer sets, step k runs on set k % R, so every set is
+    # revisited only after at least 2 x L2 of other steps' traffic and starts
+    # each step out of L2; R = 1 when one step alone moves > 4 x L2.
+    R = rotation_sets(w.step_bytes(B_local, args.policy))
+    cases = [case] + [Case(w, device, rows=(b0, b1), policy=args.policy, inputs="rng") for _ in range(R - 1)]
+    if peer is not None:
+        for c in cases[1:]:
+            c.step = native.PreparedStep(c.k, c.ins, c.primal, c.partials, [c.seed], c.adj, c.ws,
+                                         policy=args.policy, peer=peer)
 
-    def one_step(evs=None):
-        # timed step: only a start and an end event around the launches; the
-        # per-kernel breakdown is measured in a separate pass (evs of 4)
+    def one_step(c, evs=None):
+        # K1 -> K2 [-> allreduce] of buffer set c; evs: external events
+        # around K1, K2 and the collective (breakdown graphs only)
         if evs:
             evs[0].record(stream)
-        case.step.forward(sp)
-        if evs and len(evs) == 4:
+        c.step.forward(sp)
+        if evs:
             evs[1].record(stream)
-        case.step.pullback(sp)
-        if evs and len(evs) == 4:
+        c.step.pullback(sp)
+        if evs:
             evs[2].record(stream)
         if comm is not None:
-            comm.allreduce([case.bias_adj], stream=stream)
+            comm.allreduce([c.bias_adj], stream=stream)
         if evs:
-            evs[-1].record(stream)
+            evs[3].record(stream)
 
     with torch.cuda.stream(stream):
-        for _ in range(W):
-            l2()
-            one_step()
+        for k in range(max(W, 2 * R)):
+            one_step(cases[k % R])
     torch.cuda.synchronize(device)
     if world > 1:
         dist.barrier()
 
-    graph = None
-    if args.graph:
-        # The step (K1 -> K2 [-> allreduce]) captured once as a CUDA graph and
-        # replayed: one launch per step, kernel-to-kernel edges kept
-        # programmatic (PDL). The native calls run on the capturing stream.
-        graph = torch.cuda.CUDAGraph()
-        with torch.cuda.stream(stream):
-            with torch.cuda.graph(graph, stream=stream):
-                one_step()
-            for _ in range(W):
-                l2()
-                graph.replay()
-        torch.cuda.synchronize(device)
-        raw_step = one_step
-
-        def one_step(evs=None):  # noqa: F811
-            if evs is None or len(evs) == 4:
-                return raw_step(evs)
-            evs[0].record(stream)
-            graph.replay()
-            evs[-1].record(stream)
-
+    # The K timed steps, back to back, captured as ONE CUDA graph (K1 -> K2
+    # edges programmatic, PDL) and replayed once untimed, then once between
+    # a start and an end event with a barrier + synchronize on both sides.
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.stream(stream):
+        with torch.cuda.graph(graph, stream=stream):
+            for k in range(K):
+                one_step(cases[k % R])
+        graph.replay()
+    torch.cuda.synchronize(device)
+    ev_start, ev_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     clocks = ClockSampler(local)
     clocks.start()
     torch.cuda.synchronize(device)
     if world > 1:
         dist.barrier()
     with torch.cuda.stream(stream):
-        for k in range(K):
-            l2()
-            one_step(ev[k])
+        ev_start.record(stream)
+        graph.replay()
+        ev_end.record(stream)
     torch.cuda.synchronize(device)
     if world > 1:
         dist.barrier()
     clock_info = clocks.stop()
-    with torch.cuda.stream(stream):  # breakdown pass (not the reported number)
-        for k in range(K):
-            l2()
-            one_step(evb[k])
-    torch.cuda.synchronize(device)
+    total_ms = ev_start.elapsed_time(ev_end)
+    del graph
 
-    # the same split inside a captured step graph: external timing events as
-    # graph nodes around K1 and K2 (no host launch gap in front of K1), L2
-    # flushed before each replay
-    k1_graph, k2_graph = [], []
-    if args.graph:
-        ge = [torch.cuda.Event(enable_timing=True, external=True) for _ in range(3)]
-        gsplit = torch.cuda.CUDAGraph()
+    # Breakdown (not the reported number): each piece of the step alone, K
+    # launches back to back over the same rotating sets as one graph between
+    # events (steady state, operands out of L2; K2 alone then reads the
+    # partials from HBM, where inside the step they are still in L2).
+    def alone(piece):
+        g = torch.cuda.CUDAGraph()
         with torch.cuda.stream(stream):
-            with torch.cuda.graph(gsplit, stream=stream):
-                ge[0].record(stream)
-                case.step.forward(sp)
-                ge[1].record(stream)
-                case.step.pullback(sp)
-                ge[2].record(stream)
-            for k in range(3 + K):
-                l2()
-                gsplit.replay()
-                stream.synchronize()
-                if k >= 3:
-                    k1_graph.append(ge[0].elapsed_time(ge[1]))
-                    k2_graph.append(ge[1].elapsed_time(ge[2]))
-        del gsplit
-    step_ms = [e[0].elapsed_time(e[1]) for e in ev]
-    k1_ms = [e[0].elapsed_time(e[1]) for e in evb]
-    k2_ms = [e[1].elapsed_time(e[2]) for e in evb]
-    k1_stream, k2_stream = list(k1_ms), list(k2_ms)
-    if k1_graph and min(k1_graph) > 0 and min(k2_graph) > 0:
-        k1_ms, k2_ms = k1_graph, k2_graph
-    ar_ms = [e[2].elapsed_time(e[3]) for e in evb]
-    total_ms = sum(step_ms)
+            with torch.cuda.graph(g, stream=stream):
+                for k in range(K):
+                    piece(cases[k % R])
+            g.replay()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            g.replay()
+            b.record(stream)
+        torch.cuda.synchronize(device)
+        del g
+        return a.elapsed_time(b) / K
+
+    k1_alone = alone(lambda c: c.step.forward(sp))
+    k2_alone = alone(lambda c: c.step.pullback(sp))
+    ar_alone = alone(lambda c: comm.allreduce([c.bias_adj], stream=stream)) if comm is not None else None
+    k1_ms, k2_ms = [k1_alone], [k2_alone]
+    ar_ms = [ar_alone] if ar_alone is not None else []
+    # For comparison only: the round-1 method — L2 flushed, every step timed
+    # alone (events around one replay of a 1-step graph), which adds the
+    # launch latency of a step that starts from an idle stream.
+    l2 = L2Flush(device)
+    g1 = torch.cuda.CUDAGraph()
+    with torch.cuda.stream(stream):
+        with torch.cuda.graph(g1, stream=stream):
+            one_step(case)
+        iso = [[torch.cuda.Event(enable_timing=True) for _ in range(2)] for _ in range(K)]
+        for k in range(3 + K):
+            l2()
+            if k >= 3:
+                iso[k - 3][0].record(stream)
+            g1.replay()
+            if k >= 3:
+                iso[k - 3][1].record(stream)
+    torch.cuda.synchronize(device)
+    iso_ms = statistics.mean(a.elapsed_time(b) for a, b in iso)
+    del g1, l2
     if world > 1:
         t = torch.tensor([total_ms], device=device if dist.get_backend() == "nccl" else "cpu", dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -556,21 +585,23 @@ def run_native(args, w: Workload, rank: int, world: int):
         "n_gpus": world, "steps": K, "warmup": W, "ms_per_step": ms_per_step, "higher_is_better": True,
         "scaling": scaling_of(w), "vs_baseline": None, "dtype": w.dtype, "data": DATA,
         "config": bench_config(w, world, args.policy),
-        "run": {"B_per_gpu": B_local, "rows_rank0": [b0, b1],
-                "launch": "CUDA graph replay of K1->K2 (PDL edges)" if args.graph else "stream launches (PDL)"},
+        "run": {"B_per_gpu": B_local, "rows_rank0": [b0, b1], "buffer_sets": R,
+                "launch": "the K steps as one CUDA graph replay (K1 -> K2 edges programmatic, PDL)"},
         "breakdown_ms": {"K1_forward": k1_avg, "K2_pullback": k2_avg,
-                         "timing": ("events captured in the step's CUDA graph" if k1_ms is k1_graph
-                                    else "events around stream launches"),
-                         "K1_forward_stream_launch": statistics.mean(k1_stream),
-                         "K2_pullback_stream_launch": statistics.mean(k2_stream),
-                         "allreduce": statistics.mean(ar_ms) if comm is not None else None,
-                         "step_min": min(step_ms), "step_median": statistics.median(step_ms)},
-        "step_roofline": {"bytes": step_bytes, "achieved_GBps": step_bytes / (statistics.mean(step_ms) * 1e-3) / 1e9,
-                          "frac": step_bytes / (statistics.mean(step_ms) * 1e-3) / 1e9 / peak},
+                         "timing": "each kernel alone: K launches over the rotating sets as one CUDA graph between "
+                                   "events, divided by K (K2 alone reads its partials from HBM)",
+                         "allreduce": statistics.mean(ar_ms) if ar_ms else None},
+        "isolated_step": {"ms_per_step": iso_ms, "value": cells_per_step / (iso_ms * 1e-3),
+                          "method": "round-1 method, for comparison: L2 flushed before every step, each step timed "
+                                    "alone (one 1-step graph replay between events) — adds the launch latency of "
+                                    "a step issued to an idle stream"},
+        "step_roofline": {"bytes": step_bytes, "achieved_GBps": step_bytes / (ms_per_step * 1e-3) / 1e9,
+                          "frac": step_bytes / (ms_per_step * 1e-3) / 1e9 / peak},
         "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic, "algorithmic_bytes_per_launch": dom_bytes,
-                     "kernel_timing": ("CUDA events captured in the step's graph around the launch, L2 flushed"
-                                       if k1_ms is k1_graph else "CUDA events around the stream launch, L2 flushed"),
+                     "kernel_timing": "K launches of the kernel alone over the rotating buffer sets as one CUDA "
+                                      "graph between CUDA events on its stream, divided by K (steady state, operands "
+                                      "out of L2)",
                      "peak_source": peak_src},
         "e2e": {"value": e2e_value, "unit": "grad elements/s", "h2d_bytes_per_step": e2e["h2d"],
                 "d2h_bytes_per_step": e2e["d2h"], "ms_per_step": e2e["ms_per_step"],
@@ -595,7 +626,7 @@ def run_native(args, w: Workload, rank: int, world: int):
                                            else "NCCL ncclAllReduce of the 3 x H fp32 bias adjoints after K2f"
                                            if comm is not None else None),
                              "fused_fallback_reason": fused_error,
-                             "allreduce_us_per_step": (statistics.mean(ar_ms) * 1e3 if comm is not None else None),
+                             "allreduce_us_per_step": (statistics.mean(ar_ms) * 1e3 if ar_ms else None),
                              "allreduce_bytes": (case.bias_adj.numel() * case.bias_adj.element_size()
                                                  if comm is not None else 0),
                              "timing": "max over ranks of the K-step device time (CUDA events, barrier + sync "
@@ -669,59 +700,50 @@ def run_e2e(case: Case, stream, steps: int, device):
 
 
 def measure_secondary(w: Workload, device, stream, steps: int, policy: int, graph_step: bool = True):
+    """A secondary config measured like the headline: `steps` steps back to
+    back as one CUDA graph over rotating buffer sets (inputs larger than L2);
+    K1 and K2 each alone the same way for the per-kernel split."""
     import torch
-    case = Case(w, device, policy=policy, inputs="philox", seed=99)
-    l2 = L2Flush(device)
+    R = rotation_sets(w.step_bytes(policy=policy))
+    cases = [Case(w, device, policy=policy, inputs="philox", seed=99 + r) for r in range(R)]
     sp = int(stream.cuda_stream)
-    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(steps)]
-    ev2 = [[torch.cuda.Event(enable_timing=True) for _ in range(2)] for _ in range(steps)]
+    K = steps
     with torch.cuda.stream(stream):
-        # per-kernel split: stream launches with events between K1 and K2
-        for k in range(3 + steps):
-            l2()
-            e = ev[k - 3] if k >= 3 else None
-            if e:
-                e[0].record(stream)
-            case.step.forward(sp)
-            if e:
-                e[1].record(stream)
-            case.step.pullback(sp)
-            if e:
-                e[2].record(stream)
-    graph = None
-    if graph_step:  # the step as the headline runs it: one CUDA-graph replay (PDL edges kept)
-        graph = torch.cuda.CUDAGraph()
+        for k in range(2 * R):
+            cases[k % R].step.forward(sp)
+            cases[k % R].step.pullback(sp)
+
+    def timed(piece):
+        g = torch.cuda.CUDAGraph()
         with torch.cuda.stream(stream):
-            with torch.cuda.graph(graph, stream=stream):
-                case.step.forward(sp)
-                case.step.pullback(sp)
+            with torch.cuda.graph(g, stream=stream):
+                for k in range(K):
+                    piece(cases[k % R])
+            g.replay()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            g.replay()
+            b.record(stream)
         torch.cuda.synchronize(device)
-    with torch.cuda.stream(stream):
-        for k in range(3 + steps):
-            l2()
-            e = ev2[k - 3] if k >= 3 else None
-            if e:
-                e[0].record(stream)
-            if graph is not None:
-                graph.replay()
-            else:
-                case.step.forward(sp)
-                case.step.pullback(sp)
-            if e:
-                e[1].record(stream)
-    torch.cuda.synchronize(device)
-    del graph
+        del g
+        return a.elapsed_time(b) / K
+
+    def both(c):
+        c.step.forward(sp)
+        c.step.pullback(sp)
+
+    step = timed(both)
+    k1 = timed(lambda c: c.step.forward(sp))
+    k2 = timed(lambda c: c.step.pullback(sp))
     peak, _ = hbm_peak()
-    step = statistics.mean(e[0].elapsed_time(e[1]) for e in ev2)
-    k1 = statistics.mean(e[0].elapsed_time(e[1]) for e in ev)
-    k2 = statistics.mean(e[1].elapsed_time(e[2]) for e in ev)
     b1, b2 = w.k1_bytes(policy=policy), w.k2_bytes(policy=policy)
     out = {"workload": w.describe, "ms_per_step": step, "value": w.E / (step * 1e-3), "unit": "grad elements/s",
-           "launch": "step: CUDA graph replay; K1/K2 split: stream launches" if graph_step else "stream launches",
+           "launch": f"{K} steps back to back as one CUDA graph over {R} rotating buffer set(s); K1 / K2 each alone "
+                     f"the same way",
            "K1_ms": k1, "K2_ms": k2, "K1_frac_hbm": b1 / (k1 * 1e-3) / 1e9 / peak,
            "K2_frac_hbm": b2 / (k2 * 1e-3) / 1e9 / peak,
            "step_frac_hbm": (b1 + b2) / (step * 1e-3) / 1e9 / peak}
-    del case
+    del cases
     torch.cuda.empty_cache()
     return out
 
@@ -772,9 +794,10 @@ def measure_shards(device, stream, steps: int):
     """Config 5 strong scaling, the compute side, on one GPU: the step of the
     batch shard one of G GPUs owns (B = 65536 / G rows of the bias variant,
     partition.plan) timed here for G = 1, 2, 4, 8. The projected G-GPU step
-    is the shard step plus the NCCL allreduce of the 3 x H reduced (1,H)
-    adjoints (48 KB), which this single-GPU run cannot time; efficiency is
-    reported without it. A projection, not a multi-GPU measurement."""
+    is the shard step plus the allreduce of the 3 x H reduced (1,H)
+    adjoints (48 KB; fused into the pullback's finisher in the multi-GPU run),
+    which this single-GPU run cannot time; efficiency is reported without it.
+    A projection, not a multi-GPU measurement."""
     base = WORKLOADS["cfg5"]
     out = {"workload": base.describe, "note": "per-shard step on one B200; allreduce of 3*H fp32 not included"}
     t1 = None

@@ -266,6 +266,13 @@ int main() {
     };
     const size_t sm_in = 4 * 256 * 16, sm_out = 7 * 256 * 16;
     CK(cudaFuncSetAttribute(bulk_row_kernel<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm_in + sm_out)));
+    for (int blocks : {1, 148, 296, 592, 1024, 2048})
+        for (int threads : {32, 256}) {
+            const double us = time_us([&] { empty_kernel<<<blocks, threads, 0, g_s>>>(nullptr); }, true);
+            std::printf("{\"exp\": \"empty_grid\", \"blocks\": %d, \"threads\": %d, \"flush\": 1, \"us\": %.3f}\n",
+                        blocks, threads, us);
+            std::fflush(stdout);
+        }
     for (int rep = 0; rep < 2; ++rep)
         for (bool flush : {true, false}) {
             emit("empty_1024x256", time_us([&] { empty_kernel<<<1024, 256, 0, g_s>>>(nullptr); }, flush), flush);

@@ -572,6 +572,52 @@ void step_ab(const char* tag, bool bias, int64_t B, int64_t H, const std::vector
         }
 }
 
+// Steady-state step time (the bench's method): R rotating problems, K steps
+// back to back captured as one CUDA graph, one timed replay (mean over reps).
+template <class Body, class T, class Sig>
+void step_steady(const char* tag, bool bias, int64_t B, int64_t H, const std::vector<std::array<int, 3>>& variants) {
+    constexpr int R = 4, K = 40;
+    std::vector<Problem<T>*> P;
+    for (int r = 0; r < R; ++r) P.push_back(new Problem<T>(bias, B, H));
+    constexpr int V = vec_width<T>();
+    for (auto [txv, rpt, pipe] : variants) {
+        Tiling t = txv == 0 ? choose_tiling(P[0]->plan, V, class_mix(P[0]->plan)) : make_tiling(P[0]->plan, V, txv, rpt, 1);
+        if (pipe >= 0) t.pipe = pipe;
+        for (auto* p : P) CK(cudaMemset(p->ws, 0, p->ws_bytes));
+        cudaGraph_t g;
+        cudaGraphExec_t ge;
+        CK(cudaStreamBeginCapture(g_s, cudaStreamCaptureModeGlobal));
+        for (int k = 0; k < K; ++k) {
+            fwd<Body, T, Sig>(*P[k % R], nullptr);
+            pull<Body, T, Sig>(*P[k % R], &t);
+        }
+        CK(cudaStreamEndCapture(g_s, &g));
+        CK(cudaGraphInstantiate(&ge, g, 0));
+        std::vector<double> us;
+        cudaEvent_t a, b;
+        CK(cudaEventCreate(&a));
+        CK(cudaEventCreate(&b));
+        for (int rep = 0; rep < 9; ++rep) {
+            CK(cudaEventRecord(a, g_s));
+            CK(cudaGraphLaunch(ge, g_s));
+            CK(cudaEventRecord(b, g_s));
+            CK(cudaStreamSynchronize(g_s));
+            float ms;
+            CK(cudaEventElapsedTime(&ms, a, b));
+            if (rep > 0) us.push_back(ms * 1e3 / K);
+        }
+        double m = 0;
+        for (double u : us) m += u;
+        m /= us.size();
+        std::printf("{\"exp\": \"%s\", \"txv\": %d, \"rpt\": %d, \"pipe\": %d, \"grid\": [%lld, %lld], \"step_us\": %.3f, "
+                    "\"step_frac\": %.3f}\n", tag, t.txv, t.rpt, int(pull_pipe(t, g_recompute)), (long long)t.n_col_tiles,
+                    (long long)t.n_row_tiles, m, double(P[0]->step_bytes) / (m * 1e-6) / 6538e9);
+        std::fflush(stdout);
+        CK(cudaGraphExecDestroy(ge));
+        CK(cudaGraphDestroy(g));
+    }
+}
+
 int main(int argc, char** argv) {
     std::string which = argc > 1 ? argv[1] : "all";
     if (which.size() > 2 && which.compare(which.size() - 2, 2, ":r") == 0) {
@@ -625,6 +671,12 @@ int main(int argc, char** argv) {
         k2_sweep<KHmlstmBias, float, SigHmlstmBias>("k2r_16384x1024", true, 16384, 1024, {});
         k2_sweep<KHmlstm, float, SigHmlstmCanonical>("k2r_canon_65536x4096", false, 65536, 4096, {});
         g_recompute = false;
+    }
+    if (which == "stepss") {  // steady-state config-3 / config-2 steps under pullback tilings
+        step_steady<KHmlstmBias, float, SigHmlstmBias>("ss_cfg3", true, 1024, 1024,
+            {{0, 0, -1}, {0, 0, 0}, {16, 2, 0}, {16, 2, 1}, {16, 3, 0}, {16, 4, 0}, {32, 2, 0}, {32, 4, 1}, {8, 4, 1}});
+        step_steady<KHmlstm, float, SigHmlstmCanonical>("ss_cfg2", false, 1024, 1024,
+            {{0, 0, -1}, {0, 0, 1}, {256, 1, 0}, {256, 4, 0}, {256, 4, 1}, {128, 2, 0}, {128, 4, 1}});
     }
     if (which == "stepr") {  // RecomputeReverse steps (K1p + K2r) at the small configs
         g_recompute = true;
