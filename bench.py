@@ -566,15 +566,15 @@ def run_native(args, w: Workload, rank: int, world: int):
             if not key or key == w.key:
                 continue
             if key == "tape":
-                extra[key] = measure_tape(device, stream, max(5, K // 2))
+                extra[key] = measure_tape(device, stream, max(20, K))
             elif key == "shards":
-                extra[key] = measure_shards(device, stream, max(5, K // 2))
+                extra[key] = measure_shards(device, stream, max(20, K))
             elif key == "arity":
-                extra[key] = measure_arity(device, stream, max(5, K // 2))
+                extra[key] = measure_arity(device, stream, max(20, K))
             elif key.endswith(":r"):  # RecomputeReverse: K1p primal + fused K2r
-                extra[key] = measure_secondary(WORKLOADS[key[:-2]], device, stream, max(5, K // 2), 1, bool(args.graph))
+                extra[key] = measure_secondary(WORKLOADS[key[:-2]], device, stream, max(20, K), 1, bool(args.graph))
             else:
-                extra[key] = measure_secondary(WORKLOADS[key], device, stream, max(5, K // 2), args.policy, bool(args.graph))
+                extra[key] = measure_secondary(WORKLOADS[key], device, stream, max(20, K), args.policy, bool(args.graph))
 
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
