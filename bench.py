@@ -464,11 +464,15 @@ def run_native(args, w: Workload, rank: int, world: int):
         with torch.cuda.graph(graph, stream=stream):
             for k in range(K):
                 one_step(cases[k % R])
-        graph.replay()
-    torch.cuda.synchronize(device)
     ev_start, ev_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    # the clock sampler starts first (its start-up sleep would otherwise leave
+    # the GPU idle right before the timed replay); warm replays then bring the
+    # GPU to its loaded clocks, and the timed replay follows at once
     clocks = ClockSampler(local)
     clocks.start()
+    with torch.cuda.stream(stream):
+        for _ in range(3):
+            graph.replay()
     torch.cuda.synchronize(device)
     if world > 1:
         dist.barrier()
@@ -481,6 +485,16 @@ def run_native(args, w: Workload, rank: int, world: int):
         dist.barrier()
     clock_info = clocks.stop()
     total_ms = ev_start.elapsed_time(ev_end)
+    # informational (SURVEY §8(d) min / median over >= 20 repetitions): 20
+    # more replays of the same K-step graph, each between its own events
+    reps = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(20)]
+    with torch.cuda.stream(stream):
+        for a, b in reps:
+            a.record(stream)
+            graph.replay()
+            b.record(stream)
+    torch.cuda.synchronize(device)
+    rep_ms = sorted(a.elapsed_time(b) / K for a, b in reps)
     del graph
 
     # Breakdown (not the reported number): each piece of the step alone, K
@@ -493,7 +507,8 @@ def run_native(args, w: Workload, rank: int, world: int):
             with torch.cuda.graph(g, stream=stream):
                 for k in range(K):
                     piece(cases[k % R])
-            g.replay()
+            for _ in range(3):
+                g.replay()
             a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             a.record(stream)
             g.replay()
@@ -591,6 +606,9 @@ def run_native(args, w: Workload, rank: int, world: int):
                          "timing": "each kernel alone: K launches over the rotating sets as one CUDA graph between "
                                    "events, divided by K (K2 alone reads its partials from HBM)",
                          "allreduce": statistics.mean(ar_ms) if ar_ms else None},
+        "replays_ms_per_step": {"min": rep_ms[0], "median": rep_ms[len(rep_ms) // 2], "max": rep_ms[-1],
+                                "n": len(rep_ms), "note": "20 further replays of the timed K-step graph (informational; "
+                                                          "the reported value is the single bracketed replay)"},
         "isolated_step": {"ms_per_step": iso_ms, "value": cells_per_step / (iso_ms * 1e-3),
                           "method": "round-1 method, for comparison: L2 flushed before every step, each step timed "
                                     "alone (one 1-step graph replay between events) — adds the launch latency of "
@@ -719,7 +737,8 @@ def measure_secondary(w: Workload, device, stream, steps: int, policy: int, grap
             with torch.cuda.graph(g, stream=stream):
                 for k in range(K):
                     piece(cases[k % R])
-            g.replay()
+            for _ in range(3):
+                g.replay()
             a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             a.record(stream)
             g.replay()
@@ -888,7 +907,8 @@ def main():
                          "memory (bcad_cu_pullback_allreduce; default, falls back to NCCL if a rank cannot join), "
                          "or the NCCL allreduce after the pullback")
     ap.add_argument("--e2e-steps", type=int, default=10)
-    ap.add_argument("--graph", type=int, default=1, help="1: replay the step as a captured CUDA graph")
+    ap.add_argument("--graph", type=int, default=1,
+                    help="kept for compatibility: the timed steps always run as one captured CUDA graph")
     ap.add_argument("--extra", default="cfg3,cfg4,cfg4div,cfg5,cfg2:r,cfg5:r,tape,arity,shards",
                     help="secondary measurements at N=1 ('none' for none): configs, <cfg>:r = RecomputeReverse, "
                          "tape = cell_gradients mixed vs reverse-unfused, arity = tanh_product study, "
