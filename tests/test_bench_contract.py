@@ -76,3 +76,25 @@ def test_reference_arm_config_equals_gpu_arm_config():
     ref = _one_json(run("--impl", "reference", "--steps", "1", "--warmup", "3", env=env))
     assert gpu["config"] == ref["config"]
     assert ref["scaling"] == gpu["scaling"] == "weak"
+
+
+def test_rotation_sets_keep_every_step_out_of_l2():
+    """Steps rotate over R buffer sets so that a set is revisited only after
+    >= 2 x L2 of other steps' traffic; one set when a step alone moves more
+    than 4 x L2 (bench.rotation_sets)."""
+    sys.path.insert(0, ROOT)
+    import bench
+    from paper_1810_08297_b200.workloads import WORKLOADS
+    L2 = bench.L2_BYTES
+    for key in ("cfg2", "cfg3", "cfg4", "cfg4div", "cfg5"):
+        w = WORKLOADS[key]
+        for policy in (0, 1):
+            b = w.step_bytes(policy=policy)
+            R = bench.rotation_sets(b)
+            if b >= 4 * L2:
+                assert R == 1
+            else:
+                assert R >= 3 and (R - 1) * b >= 2 * L2, (key, policy, R, b)
+    assert bench.rotation_sets(WORKLOADS["cfg2"].step_bytes()) == 4
+    d = bench.bench_config(WORKLOADS["cfg2"], 1, 0)["l2"]
+    assert "4 independent batch buffer sets" in d and "no flush" in d
