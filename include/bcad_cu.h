@@ -5,7 +5,7 @@
  * NULL = the legacy default stream).
  *
  * This is the boundary the reference's hot path crosses when its host C++
- * API (include/bcad/*.hpp in this repo, mirroring /root/reference/proj/
+ * API (the include/bcad headers of this repo, mirroring /root/reference/proj/
  * include/bcad) is backed by the GPU. Every entry point names the reference
  * interface it replaces:
  *

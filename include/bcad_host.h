@@ -30,6 +30,21 @@ int bcad_host_mixed_step(const char* kernel, int dtype, int n_in, const void* co
                          void* const* host_primal, void* const* host_grads, int64_t* peak_cached_bytes,
                          void* stream);
 
+/* The same step, enqueued without waiting for it (a serving / training loop
+ * overlapping consecutive steps: the next step's uploads run during this
+ * one's downloads). Requires the pipelined, prepared path: pinned host
+ * buffers, a non-default stream, a problem large enough to chunk. Steps on
+ * the SAME host buffers are ordered among themselves (a buffer is
+ * overwritten only after the previous step has finished with it); give
+ * consecutive steps different host gradient / primal buffers to let them
+ * overlap. Results are on the host after bcad_host_synchronize(stream). */
+int bcad_host_mixed_step_async(const char* kernel, int dtype, int n_in, const void* const* host_in,
+                               const bcad_cu_shape* in_shapes, int m_out, int policy, const void* const* host_seeds,
+                               void* const* host_primal, void* const* host_grads, void* stream);
+/* Waits for every step this thread enqueued with bcad_host_mixed_step_async
+ * (and for `stream`). */
+int bcad_host_synchronize(void* stream);
+
 /* cell_gradients (proj/include/bcad/hmlstm.hpp:123-142) on an n x n cell:
  * impl 0 mixed-cache, 1 mixed-recompute, 2 reverse-unfused (the 8-primitive
  * vectorised-select baseline, hmlstm.hpp:82-99). Inputs c, f, i, g (n*n),

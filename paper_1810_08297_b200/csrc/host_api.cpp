@@ -103,7 +103,8 @@ struct Pipe {
     void* h2d = nullptr;
     void* d2h = nullptr;
     void* fork = nullptr;
-    void* join = nullptr;
+    void* join = nullptr;    // the step's last download (recorded on d2h)
+    void* x_free = nullptr;  // the step's last kernel (recorded on the compute stream): inputs consumed
     void* in_ready[kMaxChunks] = {};
     void* out_ready[kMaxChunks] = {};
     Pipe() {
@@ -111,6 +112,7 @@ struct Pipe {
         bcad::check(bcad_cu_stream_create(&d2h));
         bcad::check(bcad_cu_event_create(&fork));
         bcad::check(bcad_cu_event_create(&join));
+        bcad::check(bcad_cu_event_create(&x_free));
         for (int c = 0; c < kMaxChunks; ++c) {
             bcad::check(bcad_cu_event_create(&in_ready[c]));
             bcad::check(bcad_cu_event_create(&out_ready[c]));
@@ -123,6 +125,7 @@ struct Pipe {
         }
         bcad_cu_event_destroy(fork);
         bcad_cu_event_destroy(join);
+        bcad_cu_event_destroy(x_free);
         bcad_cu_stream_destroy(h2d);
         bcad_cu_stream_destroy(d2h);
     }
@@ -140,9 +143,15 @@ int64_t volume(const bcad_cu_shape& s) {
 }
 
 // Number of row chunks for this call (1 = one-shot tape).
+// Asynchronous steps overlap each other's head and tail, so they take fewer,
+// larger chunks: measured at config 2 (scripts/e2e_async_probe.py) a stream
+// of async steps runs 0.44 ms per step at 2 chunks, 0.49 at 4, 0.56 at 8 —
+// 2 chunks reach the H2D floor (21 MB at ~48 GB/s).
+constexpr int kAsyncChunks = 2;
+
 int plan_chunks(bcad_cu_kernel k, int n_in, const bcad_cu_shape* shapes, const bcad_cu_shape& out, int m_out,
                 std::size_t elem, const void* const* host_seeds, void* const* host_primal, void* const* host_grads,
-                const std::vector<bool>& split) {
+                const std::vector<bool>& split, bool async = false) {
     const int cfg = g_pipeline.load(std::memory_order_relaxed);
     if (cfg == 1 || out.rank < 1 || out.dims[0] < 2) return 1;
     if (bcad_cu_kernel_may_raise(k)) return 1;  // keep the reference's whole-tensor error index
@@ -155,6 +164,7 @@ int plan_chunks(bcad_cu_kernel k, int n_in, const bcad_cu_shape* shapes, const b
     for (int i = 0; i < m_out; ++i)
         bytes += std::size_t(vol) * elem * (((host_seeds && host_seeds[i]) ? 1 : 0) + ((host_primal && host_primal[i]) ? 1 : 0));
     int chunks = cfg > 1 ? cfg : int(std::min<std::size_t>(kMaxChunks, bytes / kChunkBytes));
+    if (async && cfg == 0 && chunks > kAsyncChunks) chunks = kAsyncChunks;
     chunks = std::min(chunks, kMaxChunks);
     if (chunks > out.dims[0]) chunks = int(out.dims[0]);
     return chunks < 2 ? 1 : chunks;
@@ -168,6 +178,10 @@ struct StepBuffers {
     std::vector<std::pair<int64_t, std::unique_ptr<bcad::detail::DeviceBuffer>>> ws;  // per chunk height
     std::vector<std::size_t> ws_bytes;
     std::size_t device_bytes = 0;
+    // streams and events of this entry (prepared steps own theirs, so
+    // consecutive asynchronous steps on different entries overlap)
+    std::unique_ptr<Pipe> own_pipe;
+    mutable bool used = false;  // a previous step enqueued on these buffers
     std::size_t ws_index(int64_t r) const {
         for (std::size_t q = 0; q < ws.size(); ++q)
             if (ws[q].first == r) return q;
@@ -235,7 +249,7 @@ int64_t enqueue_step(const StepBuffers<Real>& S, bcad_cu_kernel k, int n_in, con
     using namespace bcad;
     constexpr int dt = dtype_of<Real>::value;
     void* const comp = current_stream();
-    Pipe& P = pipe();
+    Pipe& P = S.own_pipe ? *S.own_pipe : pipe();
     const int chunks = int(S.bound.size()) - 1;
     const int64_t B = out.dims[0], E = volume(out), out_row = E / B;
     const std::size_t n = static_cast<std::size_t>(n_in), m = static_cast<std::size_t>(m_out);
@@ -249,15 +263,25 @@ int64_t enqueue_step(const StepBuffers<Real>& S, bcad_cu_kernel k, int n_in, con
     for (int i = 0; i < m_out; ++i) has_w[i] = host_seeds && host_seeds[i];
     for (int j = 0; j < n_in; ++j) has_g[j] = host_grads && host_grads[j];
     auto dev = [](const Tensor<Real>& t) { return const_cast<Real*>(t.device_data()); };
+    // Buffer reuse across steps on these buffers: the kernels may overwrite
+    // y / D / g only after the previous step's downloads have read them, the
+    // uploads may overwrite x / w only after its last kernel has read them.
+    // The first step instead orders the copy streams after the compute
+    // stream, where the buffers were allocated (stream-ordered).
+    if (S.used) check(bcad_cu_stream_wait_event(comp, P.join));
     {
         CopyBatch rep(0);  // batch-broadcast inputs: whole, on the compute stream
         for (int j = 0; j < n_in; ++j)
             if (!split[j]) rep.add(dev(S.x[j]), host_in[j], S.x[j].bytes());
         rep.submit(comp);
     }
-    check(bcad_cu_event_record(P.fork, comp));
-    check(bcad_cu_stream_wait_event(P.h2d, P.fork));
-    check(bcad_cu_stream_wait_event(P.d2h, P.fork));
+    if (!S.used || !S.own_pipe) {
+        check(bcad_cu_event_record(P.fork, comp));
+        check(bcad_cu_stream_wait_event(P.h2d, P.fork));
+        check(bcad_cu_stream_wait_event(P.d2h, P.fork));
+    } else {
+        check(bcad_cu_stream_wait_event(P.h2d, P.x_free));
+    }
 
     std::vector<bcad_cu_shape> cs(shapes, shapes + n_in);
     std::vector<const void*> xin(n), wp(m), Dp(m * n);
@@ -314,12 +338,18 @@ int64_t enqueue_step(const StepBuffers<Real>& S, bcad_cu_kernel k, int n_in, con
         }
         down.submit(P.d2h);
     }
+    check(bcad_cu_event_record(P.x_free, comp));
+    bool whole_grads = false;  // reduced gradients of batch-broadcast inputs: complete after the last chunk
+    for (int j = 0; j < n_in; ++j) whole_grads = whole_grads || (!split[j] && has_g[j]);
+    if (whole_grads) {
+        check(bcad_cu_stream_wait_event(P.d2h, P.x_free));
+        CopyBatch rep(1);
+        for (int j = 0; j < n_in; ++j)
+            if (!split[j] && has_g[j]) rep.add(host_grads[j], dev(S.g[j]), S.g[j].bytes());
+        rep.submit(P.d2h);
+    }
     check(bcad_cu_event_record(P.join, P.d2h));
-    check(bcad_cu_stream_wait_event(comp, P.join));
-    CopyBatch rep(1);
-    for (int j = 0; j < n_in; ++j)
-        if (!split[j] && has_g[j]) rep.add(host_grads[j], dev(S.g[j]), S.g[j].bytes());
-    rep.submit(comp);
+    S.used = true;
     // what the one-shot tape reports (tape.hpp:236-243): inputs + values + cache
     return (in_elems + int64_t(m) * E + (policy == 0 ? int64_t(m * n) * E : 0)) * int64_t(sizeof(Real));
 }
@@ -386,7 +416,7 @@ template <class Real>
 int64_t pipelined_step(bcad_cu_kernel k, const char* name, int n_in, const void* const* host_in,
                        const bcad_cu_shape* shapes, int m_out, int policy, const void* const* host_seeds,
                        void* const* host_primal, void* const* host_grads, const bcad_cu_shape& out,
-                       const std::vector<bool>& split, int chunks) {
+                       const std::vector<bool>& split, int chunks, bool async = false) {
     using namespace bcad;
     void* const comp = current_stream();
     int64_t in_bytes = 0;
@@ -397,11 +427,15 @@ int64_t pipelined_step(bcad_cu_kernel k, const char* name, int n_in, const void*
                            estimate <= kMaxPreparedBytes &&
                            all_pinned(n_in, host_in, m_out, host_seeds, host_primal, host_grads);
     if (!cacheable) {
+        if (async)
+            throw ConfigError("bcad_host_mixed_step_async needs pinned host buffers and prepared steps "
+                              "(bcad_host_set_prepared(1)) on a non-default stream");
         StepBuffers<Real> S;
         prepare_step<Real>(S, k, n_in, shapes, m_out, policy, host_seeds, host_grads, out, split, chunks);
         const int64_t p = enqueue_step<Real>(S, k, n_in, host_in, shapes, m_out, policy, host_seeds, host_primal,
                                              host_grads, out, split);
         check(bcad_cu_stream_synchronize(comp));
+        check(bcad_cu_stream_synchronize(pipe().d2h));
         return p;
     }
     auto& cache = prepared_cache<Real>();
@@ -417,6 +451,7 @@ int64_t pipelined_step(bcad_cu_kernel k, const char* name, int n_in, const void*
             cache.erase(lru);
         }
         auto entry = std::make_unique<Prepared<Real>>();
+        entry->bufs.own_pipe = std::make_unique<Pipe>();
         prepare_step<Real>(entry->bufs, k, n_in, shapes, m_out, policy, host_seeds, host_grads, out, split, chunks);
         it = cache.emplace(key, std::move(entry)).first;
     }
@@ -424,14 +459,27 @@ int64_t pipelined_step(bcad_cu_kernel k, const char* name, int n_in, const void*
     E.last_use = ++clock;
     const int64_t p = enqueue_step<Real>(E.bufs, k, n_in, host_in, shapes, m_out, policy, host_seeds, host_primal,
                                          host_grads, out, split);
-    check(bcad_cu_stream_synchronize(comp));
+    if (!async) {
+        check(bcad_cu_stream_synchronize(comp));
+        check(bcad_cu_stream_synchronize(E.bufs.own_pipe->d2h));
+    }
     return p;
+}
+
+// Waits for every step enqueued by bcad_host_mixed_step_async on this thread.
+template <class Real>
+void sync_prepared() {
+    for (auto& [key, e] : prepared_cache<Real>())
+        if (e->bufs.own_pipe) {
+            bcad::check(bcad_cu_stream_synchronize(e->bufs.own_pipe->h2d));
+            bcad::check(bcad_cu_stream_synchronize(e->bufs.own_pipe->d2h));
+        }
 }
 
 template <class Real>
 void step(const char* name, int n_in, const void* const* host_in, const bcad_cu_shape* shapes, int m_out,
           int policy, const void* const* host_seeds, void* const* host_primal, void* const* host_grads,
-          int64_t* peak) {
+          int64_t* peak, bool async = false) {
     using namespace bcad;
     bcad_cu_kernel k = nullptr;
     check(bcad_cu_kernel_lookup(name, n_in, m_out, &k));
@@ -439,14 +487,16 @@ void step(const char* name, int n_in, const void* const* host_in, const bcad_cu_
     check(bcad_cu_broadcast_shape(n_in, shapes, &out));
     std::vector<bool> split(static_cast<std::size_t>(n_in), false);
     for (int j = 0; j < n_in; ++j) split[j] = shapes[j].rank > 0 && out.rank > 0 && shapes[j].dims[0] == out.dims[0];
-    const int chunks = plan_chunks(k, n_in, shapes, out, m_out, sizeof(Real), host_seeds, host_primal, host_grads, split);
+    const int chunks =
+        plan_chunks(k, n_in, shapes, out, m_out, sizeof(Real), host_seeds, host_primal, host_grads, split, async);
     int64_t p = 0;
     if (chunks == 1) {
+        if (async) throw ConfigError("bcad_host_mixed_step_async needs a pipelined (row-chunked) step");
         p = tape_step<Real>(name, n_in, host_in, shapes, m_out, policy, host_seeds, host_primal, host_grads);
         check(bcad_cu_stream_synchronize(current_stream()));
     } else {
         p = pipelined_step<Real>(k, name, n_in, host_in, shapes, m_out, policy, host_seeds, host_primal, host_grads,
-                                 out, split, chunks);
+                                 out, split, chunks, async);
     }
     if (peak) *peak = p;
 }
@@ -579,6 +629,38 @@ int bcad_host_mixed_step(const char* kernel, int dtype, int n_in, const void* co
             step<double>(kernel, n_in, host_in, in_shapes, m_out, policy, host_seeds, host_primal, host_grads, peak_cached_bytes);
         else
             throw bcad::ConfigError("dtype must be F32 or F64");
+        return BCAD_CU_OK;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return code_of(e);
+    }
+}
+
+int bcad_host_mixed_step_async(const char* kernel, int dtype, int n_in, const void* const* host_in,
+                               const bcad_cu_shape* in_shapes, int m_out, int policy, const void* const* host_seeds,
+                               void* const* host_primal, void* const* host_grads, void* stream) {
+    try {
+        bcad::StreamGuard guard(stream);
+        if (dtype == BCAD_CU_F32)
+            step<float>(kernel, n_in, host_in, in_shapes, m_out, policy, host_seeds, host_primal, host_grads, nullptr,
+                        true);
+        else if (dtype == BCAD_CU_F64)
+            step<double>(kernel, n_in, host_in, in_shapes, m_out, policy, host_seeds, host_primal, host_grads, nullptr,
+                         true);
+        else
+            throw bcad::ConfigError("dtype must be F32 or F64");
+        return BCAD_CU_OK;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return code_of(e);
+    }
+}
+
+int bcad_host_synchronize(void* stream) {
+    try {
+        bcad::check(bcad_cu_stream_synchronize(stream));
+        sync_prepared<float>();
+        sync_prepared<double>();
         return BCAD_CU_OK;
     } catch (const std::exception& e) {
         g_err = e.what();

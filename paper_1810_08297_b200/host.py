@@ -25,6 +25,11 @@ def _load():
     lib.bcad_host_set_pipeline.argtypes = [C.c_int]
     lib.bcad_host_set_prepared.restype = C.c_int
     lib.bcad_host_set_prepared.argtypes = [C.c_int]
+    lib.bcad_host_mixed_step_async.restype = C.c_int
+    lib.bcad_host_mixed_step_async.argtypes = [C.c_char_p, C.c_int, C.c_int, C.c_void_p, C.c_void_p, C.c_int, C.c_int,
+                                               C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
+    lib.bcad_host_synchronize.restype = C.c_int
+    lib.bcad_host_synchronize.argtypes = [C.c_void_p]
     return lib
 
 
@@ -72,6 +77,21 @@ class HostStep:
         if rc:
             raise native._BY_CODE.get(rc, native.Error)(LIB.bcad_host_last_error().decode())
         return int(self.peak.value)
+
+    def enqueue(self) -> None:
+        """bcad_host_mixed_step_async: the same step without waiting for it
+        (see synchronize)."""
+        rc = LIB.bcad_host_mixed_step_async(self.kernel, self.dt, self.n, self.ins, self.shapes, self.m, self.policy,
+                                            self.seeds, self.prim, self.grads, self.stream)
+        if rc:
+            raise native._BY_CODE.get(rc, native.Error)(LIB.bcad_host_last_error().decode())
+
+
+def synchronize(stream=None) -> None:
+    """bcad_host_synchronize: wait for every enqueued host step."""
+    rc = LIB.bcad_host_synchronize(stream)
+    if rc:
+        raise native._BY_CODE.get(rc, native.Error)(LIB.bcad_host_last_error().decode())
 
 
 LIB.bcad_host_cell_gradients.restype = C.c_int

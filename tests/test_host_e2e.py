@@ -206,3 +206,38 @@ def test_prepared_step_replay_rereads_buffers(oracle_lib):
     finally:
         H.set_prepared(True)
         H.set_pipeline(0)
+
+
+@pytest.mark.parametrize("variant", ["canonical", "bias"])
+def test_async_host_steps_overlap_and_match(oracle_lib, variant):
+    """bcad_host_mixed_step_async: a stream of steps alternating between two
+    host gradient buffer sets (the overlap the e2e bench times) gives every
+    step the same bits as the synchronous call — including the bias
+    variant's (1,H) gradients, accumulated over chunks and downloaded after
+    the last one — and steps on the same buffers stay ordered."""
+    import torch
+    from paper_1810_08297_b200 import host as H
+    B, Hd = 2048, 1024
+    ins = O.hmlstm_inputs(oracle_lib, B, Hd, np.float32, variant)
+    pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory().numpy()  # noqa: E731
+    hin = [pin(a) for a in ins]
+    seed = pin(np.random.default_rng(3).uniform(-1, 1, (B, Hd)).astype(np.float32))
+    name = O.hmlstm_kernel(variant)
+    stream = torch.cuda.Stream()
+    sp = int(stream.cuda_stream)
+    ref = [pin(np.zeros(a.shape, np.float32)) for a in ins]
+    # the synchronous reference at the async path's chunk count (2): the
+    # (1,H) gradients are summed per chunk, so their last bits follow the count
+    H.set_pipeline(2)
+    try:
+        H.HostStep(name, hin, [seed], grads_out=ref, stream=sp)()
+    finally:
+        H.set_pipeline(0)
+    sets = [[pin(np.full(a.shape, np.nan, np.float32)) for a in ins] for _ in range(2)]
+    calls = [H.HostStep(name, hin, [seed], grads_out=g, stream=sp) for g in sets]
+    for k in range(7):
+        calls[k % 2].enqueue()
+    H.synchronize(sp)
+    for g in sets:
+        for j, (x, y) in enumerate(zip(g, ref)):
+            assert np.array_equal(x, y), f"grad[{j}] differs from the synchronous step"
