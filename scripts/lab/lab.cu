@@ -575,20 +575,24 @@ void step_ab(const char* tag, bool bias, int64_t B, int64_t H, const std::vector
 // Steady-state step time (the bench's method): R rotating problems, K steps
 // back to back captured as one CUDA graph, one timed replay (mean over reps).
 template <class Body, class T, class Sig>
-void step_steady(const char* tag, bool bias, int64_t B, int64_t H, const std::vector<std::array<int, 3>>& variants) {
+void step_steady(const char* tag, bool bias, int64_t B, int64_t H, const std::vector<std::array<int, 3>>& variants,
+                 const std::vector<std::array<int, 2>>& fwd_variants = {{0, 0}}) {
     constexpr int R = 4, K = 40;
     std::vector<Problem<T>*> P;
     for (int r = 0; r < R; ++r) P.push_back(new Problem<T>(bias, B, H));
     constexpr int V = vec_width<T>();
+    for (auto [ftxv, frpt] : fwd_variants)
     for (auto [txv, rpt, pipe] : variants) {
         Tiling t = txv == 0 ? choose_tiling(P[0]->plan, V, class_mix(P[0]->plan)) : make_tiling(P[0]->plan, V, txv, rpt, 1);
         if (pipe >= 0) t.pipe = pipe;
+        const Tiling ft = make_tiling(P[0]->plan, V, ftxv ? ftxv : 1, frpt ? frpt : 1, 1);
+        const Tiling* ftp = ftxv ? &ft : nullptr;
         for (auto* p : P) CK(cudaMemset(p->ws, 0, p->ws_bytes));
         cudaGraph_t g;
         cudaGraphExec_t ge;
         CK(cudaStreamBeginCapture(g_s, cudaStreamCaptureModeGlobal));
         for (int k = 0; k < K; ++k) {
-            fwd<Body, T, Sig>(*P[k % R], nullptr);
+            fwd<Body, T, Sig>(*P[k % R], ftp);
             pull<Body, T, Sig>(*P[k % R], &t);
         }
         CK(cudaStreamEndCapture(g_s, &g));
@@ -609,9 +613,9 @@ void step_steady(const char* tag, bool bias, int64_t B, int64_t H, const std::ve
         double m = 0;
         for (double u : us) m += u;
         m /= us.size();
-        std::printf("{\"exp\": \"%s\", \"txv\": %d, \"rpt\": %d, \"pipe\": %d, \"grid\": [%lld, %lld], \"step_us\": %.3f, "
-                    "\"step_frac\": %.3f}\n", tag, t.txv, t.rpt, int(pull_pipe(t, g_recompute)), (long long)t.n_col_tiles,
-                    (long long)t.n_row_tiles, m, double(P[0]->step_bytes) / (m * 1e-6) / 6538e9);
+        std::printf("{\"exp\": \"%s\", \"k1\": [%d, %d], \"txv\": %d, \"rpt\": %d, \"pipe\": %d, \"grid\": [%lld, %lld], "
+                    "\"step_us\": %.3f, \"step_frac\": %.3f}\n", tag, ftxv, frpt, t.txv, t.rpt, int(pull_pipe(t, g_recompute)),
+                    (long long)t.n_col_tiles, (long long)t.n_row_tiles, m, double(P[0]->step_bytes) / (m * 1e-6) / 6538e9);
         std::fflush(stdout);
         CK(cudaGraphExecDestroy(ge));
         CK(cudaGraphDestroy(g));
@@ -677,6 +681,10 @@ int main(int argc, char** argv) {
             {{0, 0, -1}, {0, 0, 0}, {16, 2, 0}, {16, 2, 1}, {16, 3, 0}, {16, 4, 0}, {32, 2, 0}, {32, 4, 1}, {8, 4, 1}});
         step_steady<KHmlstm, float, SigHmlstmCanonical>("ss_cfg2", false, 1024, 1024,
             {{0, 0, -1}, {0, 0, 1}, {256, 1, 0}, {256, 4, 0}, {256, 4, 1}, {128, 2, 0}, {128, 4, 1}});
+    }
+    if (which == "stepss3") {  // config 3 steady state: K1 tilings x a few K2 tilings
+        step_steady<KHmlstmBias, float, SigHmlstmBias>("ss3", true, 1024, 1024, {{0, 0, -1}, {16, 2, 0}, {32, 4, 1}},
+                                                       {{0, 0}, {128, 3}, {256, 2}, {256, 3}, {128, 2}, {64, 3}, {128, 4}});
     }
     if (which == "stepr") {  // RecomputeReverse steps (K1p + K2r) at the small configs
         g_recompute = true;
