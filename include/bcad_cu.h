@@ -138,8 +138,9 @@ int bcad_cu_pullback_workspace(bcad_cu_kernel k, int dtype, int n_in, const bcad
 int bcad_cu_pullback_workspace_init(void* workspace, size_t bytes, void* stream);
 
 /* Device kernel launches one bcad_cu_pullback of this problem issues with
- * aligned pointers (1: K2, including any cross-CTA combination; 0: the
- * generic rank-N path). */
+ * aligned pointers, every input taking an adjoint and the workspace
+ * bcad_cu_pullback_workspace sizes (tiled 2-D path: 1 = K2 alone, 2 = K2 +
+ * K2f; generic rank-N path: 1-5). */
 int bcad_cu_pullback_launches(bcad_cu_kernel k, int dtype, int n_in, const bcad_cu_shape* in_shapes, int m_out,
                               int* launches);
 

@@ -992,6 +992,16 @@ struct GenParams {
     T* adj[N];
     uint32_t acc_mask;
     int64_t adj_offset[N + 1];  // prefix sums of arg volumes over active adj
+    // segmented reductions (pull_generic_seg_kernel): segments per element of
+    // argument j (0 = not segmented), prefix sums of arg_vol[j] * segs[j],
+    // and the fp64 partials [item][segment]
+    int segs[N];
+    int64_t seg_offset[N + 1];
+    double* seg_ws;
+    // column-mode segmented arguments (full along the last axis): a CTA per
+    // (kThreads consecutive elements, segment); first CTA of each argument
+    uint32_t seg_col_mask;
+    int64_t seg_block[N + 1];
     unsigned long long* err;
 };
 
@@ -999,6 +1009,17 @@ template <int N, int M, class T>
 __device__ __forceinline__ void decode_offsets(const GenParams<N, M, T>& p, int64_t flat, int64_t* off) {
 #pragma unroll
     for (int j = 0; j < N; ++j) off[j] = 0;
+    if (p.vol <= 0xffffffffll) {  // 32-bit index arithmetic (64-bit division costs ~4x the instructions)
+        uint32_t f = uint32_t(flat);
+        for (int k = p.out_rank - 1; k >= 0; --k) {
+            const uint32_t len = uint32_t(p.out_dims[k]);
+            const uint32_t c = f % len;
+            f /= len;
+#pragma unroll
+            for (int j = 0; j < N; ++j) off[j] += int64_t(c) * p.strides[j][k];
+        }
+        return;
+    }
     for (int k = p.out_rank - 1; k >= 0; --k) {
         const int64_t len = p.out_dims[k];
         const int64_t c = flat % len;
@@ -1039,6 +1060,120 @@ __global__ void __launch_bounds__(kThreads) fwd_generic_kernel(const __grid_cons
                 for (int j = 0; j < N; ++j)
                     if (p.partials[i * N + j]) p.partials[i * N + j][cell] = yo[i].d[j];
             }
+        }
+    }
+}
+
+// Generic forward, V cells per thread along the output's last axis (when
+// its length is a multiple of V and every argument is contiguous or
+// broadcast along it): one offset decode per V cells, 128-bit loads of the
+// arguments full along the last axis (read-only loads for those re-read
+// through broadcasting), 128-bit stores of the primal and the partials.
+template <class Body, class T, int V, bool kReal>
+__global__ void __launch_bounds__(kThreads) fwd_generic_vec_kernel(const __grid_constant__ GenParams<Body::kIn, Body::kOut, T> p) {
+    constexpr int N = Body::kIn, M = Body::kOut;
+    if constexpr (Body::kMayRaise && !kReal) s_err_flag[threadIdx.x] = 0;
+    const int last = p.out_rank - 1;
+    const int64_t nv = p.vol / V;
+    for (int64_t v = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; v < nv; v += int64_t(gridDim.x) * blockDim.x) {
+        const int64_t cell = v * V;
+        int64_t off[N];
+        decode_offsets<N, M, T>(p, cell, off);
+        Pack<T, V> x[N];
+#pragma unroll
+        for (int j = 0; j < N; ++j) {
+            if (p.strides[j][last] == 0) {
+                const T s = __ldg(p.in[j] + off[j]);
+#pragma unroll
+                for (int u = 0; u < V; ++u) x[j].x[u] = s;
+            } else if (p.arg_vol[j] == p.vol) {
+                x[j] = ld_stream<T, V>(p.in[j] + off[j]);
+            } else {
+                x[j] = ld_ro<T, V>(p.in[j] + off[j]);
+            }
+        }
+        if constexpr (kReal) {
+            Pack<T, V> y[M];
+#pragma unroll
+            for (int u = 0; u < V; ++u) {
+                T xi[N], yo[M];
+#pragma unroll
+                for (int j = 0; j < N; ++j) xi[j] = x[j].x[u];
+                Body::template body<T>(xi, yo);
+#pragma unroll
+                for (int i = 0; i < M; ++i) y[i].x[u] = yo[i];
+            }
+#pragma unroll
+            for (int i = 0; i < M; ++i)
+                if (p.primal[i]) st_vec<T, V>(p.primal[i] + cell, y[i]);
+        } else {
+            Pack<T, V> y[M], d[M * N];
+            eval_cells<Body, T, V, DynSig>(x, y, d, p.err, cell);
+#pragma unroll
+            for (int i = 0; i < M; ++i) {
+                if (p.primal[i]) st_vec<T, V>(p.primal[i] + cell, y[i]);
+#pragma unroll
+                for (int j = 0; j < N; ++j)
+                    if (p.partials[i * N + j]) st_vec<T, V>(p.partials[i * N + j] + cell, d[i * N + j]);
+            }
+        }
+    }
+}
+
+// Generic pullback of the arguments of the output's full shape (p.adj set
+// for exactly those): their adjoint is elementwise, sum_i w_i (.) D_ij in
+// the element type in output order, as the thread-per-element kernel forms
+// it (cnt = 1), V cells per thread, each output's seed read once for all of
+// them. RecomputeReverse re-evaluates D as fwd_generic_vec_kernel does.
+template <class Body, class T, int V, bool kRecompute>
+__global__ void __launch_bounds__(kThreads) pull_generic_full_kernel(const __grid_constant__ GenParams<Body::kIn, Body::kOut, T> p) {
+    constexpr int N = Body::kIn, M = Body::kOut;
+    if constexpr (Body::kMayRaise && kRecompute) s_err_flag[threadIdx.x] = 0;
+    const int last = p.out_rank - 1;
+    const int64_t nv = p.vol / V;
+    for (int64_t v = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; v < nv; v += int64_t(gridDim.x) * blockDim.x) {
+        const int64_t cell = v * V;
+        Pack<T, V> w[M];
+#pragma unroll
+        for (int i = 0; i < M; ++i)
+            if (p.w[i]) w[i] = ld_stream<T, V>(p.w[i] + cell);
+        Pack<T, V> d[M * N];
+        if constexpr (kRecompute) {
+            int64_t off[N];
+            decode_offsets<N, M, T>(p, cell, off);
+            Pack<T, V> x[N];
+#pragma unroll
+            for (int j = 0; j < N; ++j) {
+                if (p.strides[j][last] == 0) {
+                    const T s = __ldg(p.in[j] + off[j]);
+#pragma unroll
+                    for (int u = 0; u < V; ++u) x[j].x[u] = s;
+                } else if (p.arg_vol[j] == p.vol) {
+                    x[j] = ld_stream<T, V>(p.in[j] + off[j]);
+                } else {
+                    x[j] = ld_ro<T, V>(p.in[j] + off[j]);
+                }
+            }
+            eval_cells<Body, T, V, DynSig>(x, static_cast<Pack<T, V>*>(nullptr), d, p.err, cell);
+        }
+#pragma unroll
+        for (int j = 0; j < N; ++j) {
+            if (!p.adj[j]) continue;
+            Pack<T, V> out;
+            if ((p.acc_mask >> j) & 1u) out = ld_stream<T, V>(p.adj[j] + cell);
+            else
+#pragma unroll
+                for (int u = 0; u < V; ++u) out.x[u] = T(0);
+#pragma unroll
+            for (int i = 0; i < M; ++i) {
+                if (!p.w[i]) continue;
+                Pack<T, V> dj;
+                if constexpr (kRecompute) dj = d[i * N + j];
+                else dj = ld_stream<T, V>(p.D[i * N + j] + cell);
+#pragma unroll
+                for (int u = 0; u < V; ++u) out.x[u] = out.x[u] + T(w[i].x[u] * dj.x[u]);
+            }
+            st_vec<T, V>(p.adj[j] + cell, out);
         }
     }
 }
@@ -1152,6 +1287,218 @@ __global__ void __launch_bounds__(kThreads) pull_generic_kernel(const __grid_con
             else p.adj[j][e] = acc ? T(double(p.adj[j][e]) + sum) : T(sum);
         }
     }
+}
+
+// Generic pullback, arguments reduced over many output cells, cut into
+// `segs` contiguous segments of each element's broadcast cells (row-major,
+// last broadcast axis fastest) whose fp64 partials pull_generic_seg_finish
+// adds in segment order. Two CTA shapes, chosen per argument:
+//  - row mode (reduced along the last axis, >= kSegMinCells cells): one CTA
+//    per (element, segment); threads stride the segment, so warps read
+//    consecutive cells; then a fixed-shape shared-memory tree;
+//  - column mode (full along the last axis): one CTA per (kThreads
+//    consecutive elements, segment); each thread walks its element's segment
+//    in order, so warps read consecutive elements of the same broadcast cell.
+// Either way a fixed association of the same rounded terms; bitwise
+// run-to-run deterministic.
+template <class Body, class T, bool kRecompute>
+__device__ __forceinline__ double generic_cell_term(const GenParams<Body::kIn, Body::kOut, T>& p, int j, int64_t flat) {
+    constexpr int N = Body::kIn, M = Body::kOut;
+    T dj[M];
+    if constexpr (kRecompute) {
+        int64_t off[N];
+        decode_offsets<N, M, T>(p, flat, off);
+        Dual<T, N> xi[N], yo[M];
+#pragma unroll
+        for (int jj = 0; jj < N; ++jj) xi[jj] = Dual<T, N>::seeded(p.in[jj][off[jj]], jj);
+        Body::template body<Dual<T, N>>(xi, yo);
+        if constexpr (Body::kMayRaise) report_error(p.err, flat);
+#pragma unroll
+        for (int i = 0; i < M; ++i) {
+            T v = T(0);
+#pragma unroll
+            for (int jj = 0; jj < N; ++jj)
+                if (jj == j) v = yo[i].d[jj];
+            dj[i] = v;
+        }
+    } else {
+#pragma unroll
+        for (int i = 0; i < M; ++i) dj[i] = p.w[i] ? p.D[i * N + j][flat] : T(0);
+    }
+    double sum = 0.0;
+#pragma unroll
+    for (int i = 0; i < M; ++i)
+        if (p.w[i]) sum += double(T(p.w[i][flat] * dj[i]));
+    return sum;
+}
+
+template <class Body, class T, bool kRecompute>
+__global__ void __launch_bounds__(kThreads) pull_generic_seg_kernel(const __grid_constant__ GenParams<Body::kIn, Body::kOut, T> p) {
+    constexpr int N = Body::kIn;
+    if constexpr (Body::kMayRaise && kRecompute) s_err_flag[threadIdx.x] = 0;
+    __shared__ double part[kThreads];
+    const int64_t b = blockIdx.x;
+    int j = 0;
+    while (j + 1 < N && b >= p.seg_block[j + 1]) ++j;
+    const int S = p.segs[j];
+    const bool column = (p.seg_col_mask >> j) & 1u;
+    const int64_t local = b - p.seg_block[j];
+    int64_t e;
+    int seg;
+    if (column) {
+        seg = int(local % S);
+        e = (local / S) * kThreads + threadIdx.x;
+        if (e >= p.arg_vol[j]) return;  // no CTA-wide sync below in column mode
+    } else {
+        e = local / S;
+        seg = int(local % S);
+    }
+    // the element's coordinates on the axes where argument j is full, and the
+    // broadcast axes it is summed over
+    int64_t coord[kMaxRank], ostride[kMaxRank];
+    int bax[kMaxRank];
+    int nb = 0;
+    int64_t cnt = 1, flat0 = 0;
+    {
+        int64_t rem = e, os = 1;
+        for (int k = p.out_rank - 1; k >= 0; --k) {
+            ostride[k] = os;
+            os *= p.out_dims[k];
+            if (p.strides[j][k] != 0) {
+                coord[k] = rem % p.out_dims[k];
+                rem /= p.out_dims[k];
+            } else {
+                coord[k] = 0;
+            }
+            flat0 += coord[k] * ostride[k];
+        }
+        for (int k = 0; k < p.out_rank; ++k)
+            if (p.strides[j][k] == 0 && p.out_dims[k] > 1) {
+                bax[nb++] = k;
+                cnt *= p.out_dims[k];
+            }
+    }
+    const int64_t q0 = cnt * seg / S, q1 = cnt * (seg + 1) / S;
+    double sum = 0.0;
+    if (column) {
+        // odometer over the broadcast axes from cell q0, the flat index kept
+        // incrementally; four cells' loads in flight before they are summed
+        int64_t c[kMaxRank];
+        int64_t flat = flat0;
+        {
+            int64_t rem = q0;
+            for (int b2 = nb - 1; b2 >= 0; --b2) {
+                const int k = bax[b2];
+                c[k] = rem % p.out_dims[k];
+                rem /= p.out_dims[k];
+                flat += c[k] * ostride[k];
+            }
+        }
+        auto advance = [&]() {
+            for (int b2 = nb - 1; b2 >= 0; --b2) {
+                const int k = bax[b2];
+                flat += ostride[k];
+                if (++c[k] < p.out_dims[k]) return;
+                flat -= c[k] * ostride[k];
+                c[k] = 0;
+            }
+        };
+        int64_t q = q0;
+        for (; q + 4 <= q1; q += 4) {
+            int64_t f[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                f[u] = flat;
+                advance();
+            }
+            double t[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) t[u] = generic_cell_term<Body, T, kRecompute>(p, j, f[u]);
+#pragma unroll
+            for (int u = 0; u < 4; ++u) sum += t[u];
+        }
+        for (; q < q1; ++q) {
+            sum += generic_cell_term<Body, T, kRecompute>(p, j, flat);
+            advance();
+        }
+        p.seg_ws[p.seg_offset[j] + e * S + seg] = sum;
+        return;
+    }
+    {
+        // threads stride the segment by kThreads cells: the odometer advances
+        // by kThreads with a division only when an axis wraps; four cells'
+        // loads in flight before they are summed (in q order)
+        int64_t c[kMaxRank];
+        int64_t flat = flat0;
+        {
+            int64_t rem = q0 + threadIdx.x;
+            for (int b2 = nb - 1; b2 >= 0; --b2) {
+                const int k = bax[b2];
+                c[k] = rem % p.out_dims[k];
+                rem /= p.out_dims[k];
+                flat += c[k] * ostride[k];
+            }
+        }
+        auto advance = [&]() {
+            int64_t step = kThreads;
+            for (int b2 = nb - 1; b2 >= 0 && step; --b2) {
+                const int k = bax[b2];
+                const int64_t len = p.out_dims[k];
+                int64_t cn = c[k] + step;
+                step = 0;
+                if (cn >= len) {
+                    step = cn / len;
+                    cn -= step * len;
+                }
+                flat += (cn - c[k]) * ostride[k];
+                c[k] = cn;
+            }
+        };
+        int64_t q = q0 + threadIdx.x;
+        for (; q + 3 * kThreads < q1; q += 4 * kThreads) {
+            int64_t f[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                f[u] = flat;
+                advance();
+            }
+            double t[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) t[u] = generic_cell_term<Body, T, kRecompute>(p, j, f[u]);
+#pragma unroll
+            for (int u = 0; u < 4; ++u) sum += t[u];
+        }
+        for (; q < q1; q += kThreads) {
+            sum += generic_cell_term<Body, T, kRecompute>(p, j, flat);
+            advance();
+        }
+    }
+    part[threadIdx.x] = sum;
+    __syncthreads();
+    for (int stride = kThreads / 2; stride > 0; stride >>= 1) {
+        if (threadIdx.x < stride) part[threadIdx.x] += part[threadIdx.x + stride];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) p.seg_ws[p.seg_offset[j] + e * S + seg] = part[0];
+}
+
+template <int N, int M, class T>
+__global__ void __launch_bounds__(kThreads) pull_generic_seg_finish(const __grid_constant__ GenParams<N, M, T> p) {
+    const int64_t g = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;  // over segmented elements
+    int j = 0;
+    int64_t base = 0;  // first element index of argument j among segmented elements
+    for (; j < N; ++j) {
+        const int64_t n = p.segs[j] > 0 ? p.arg_vol[j] : 0;
+        if (g < base + n) break;
+        base += n;
+    }
+    if (j >= N) return;
+    const int64_t e = g - base;
+    const int S = p.segs[j];
+    double sum = 0.0;
+    for (int k = 0; k < S; ++k) sum += p.seg_ws[p.seg_offset[j] + e * S + k];
+    const bool acc = (p.acc_mask >> j) & 1u;
+    p.adj[j][e] = acc ? T(double(p.adj[j][e]) + sum) : T(sum);
 }
 
 }  // namespace bcad_dev

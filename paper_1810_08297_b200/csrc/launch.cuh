@@ -120,6 +120,22 @@ constexpr int fwd_vec_width() {
     else return v;
 }
 
+// Generic kernels' cells per thread along the output's last axis: one
+// 128-bit vector for bodies whose per-cell dual state is small (N*M <= 18),
+// when the last axis is a multiple of it and every argument is contiguous
+// (stride 1) or broadcast (stride 0) along it.
+template <class Body, class T>
+constexpr int generic_vec_width() {
+    return Body::kIn * Body::kOut <= 18 ? fwd_vec_width<Body, T>() : 1;
+}
+inline bool generic_vec_ok(const Plan& plan, int V) {
+    const int last = plan.out_rank - 1;
+    if (last < 0 || plan.out_dims[last] % V != 0) return false;
+    for (int j = 0; j < plan.n; ++j)
+        if (plan.strides[j][last] != 0 && plan.strides[j][last] != 1) return false;
+    return true;
+}
+
 // K1's rows per thread on large problems (more than two waves of CTAs):
 // short CTAs, unless the body asks for more (Body::kFwdRows). The
 // primal-only K1p moves 5 tensors per cell instead of 1 + N + M*N and wants
@@ -208,6 +224,23 @@ int launch_fwd_t(const FwdArgs& a, std::string* err) {
         for (int j = 0; j < N; ++j) g.partials[i * N + j] = a.partials ? static_cast<T*>(a.partials[i * N + j]) : nullptr;
     }
     g.err = a.err;
+    if constexpr (generic_vec_width<Body, T>() > 1) {
+        constexpr int GV = generic_vec_width<Body, T>();
+        bool gvec = generic_vec_ok(plan, GV);
+        for (int j = 0; j < N && gvec; ++j)
+            if (plan.strides[j][plan.out_rank - 1] != 0 && !aligned16(a.in[j])) gvec = false;
+        for (int i = 0; i < M && gvec; ++i) {
+            if (a.primal && a.primal[i] && !aligned16(a.primal[i])) gvec = false;
+            for (int j = 0; j < N && a.partials && gvec; ++j)
+                if (a.partials[i * N + j] && !aligned16(a.partials[i * N + j])) gvec = false;
+        }
+        if (gvec) {
+            const int grid = generic_grid(plan.vol / GV);
+            if (real) bcad_dev::fwd_generic_vec_kernel<Body, T, GV, true><<<grid, kThreads, 0, a.stream>>>(g);
+            else bcad_dev::fwd_generic_vec_kernel<Body, T, GV, false><<<grid, kThreads, 0, a.stream>>>(g);
+            return cuda_status(cudaGetLastError(), err);
+        }
+    }
     const int grid = generic_grid(plan.vol);
     if (real) bcad_dev::fwd_generic_kernel<Body, T, true><<<grid, kThreads, 0, a.stream>>>(g);
     else bcad_dev::fwd_generic_kernel<Body, T, false><<<grid, kThreads, 0, a.stream>>>(g);
@@ -382,8 +415,11 @@ int launch_pull_t(const PullArgs& a, std::string* err) {
     if (pull_scalar2d_ok<T>(plan) &&
         a.ws_bytes >= pull_layout(plan, choose_tiling(plan, 1, class_mix(plan))).total)
         return launch_pull2d<Body, T, 1>(a, err);
-    // generic rank-N pullback: thread per element, or warp per element for
-    // arguments reduced over >= 32 output cells
+    // generic rank-N pullback: a thread per element (coalesced when the
+    // argument is full along the last axis; its reduction cut into segments
+    // when that leaves too few threads), a warp per element for arguments
+    // reduced over >= 32 cells including the last axis, segments over CTAs
+    // when those are >= 4096 cells
     bcad_dev::GenParams<N, M, T> g{};
     fill_generic(g, plan);
     for (int j = 0; j < N; ++j) g.in[j] = a.in ? static_cast<const T*>(a.in[j]) : nullptr;
@@ -394,12 +430,31 @@ int launch_pull_t(const PullArgs& a, std::string* err) {
         for (int j = 0; j < N; ++j) g.D[i * N + j] = recompute ? nullptr : static_cast<const T*>(a.partials[i * N + j]);
     }
     g.err = a.err;
-    bcad_dev::GenParams<N, M, T> gw = g;
-    int64_t off = 0, offw = 0;
+    bcad_dev::GenParams<N, M, T> gw = g, gs = g, gf = g;
+    bool any_full = false;
+    // arguments reduced over many cells per element: segmented (needs the
+    // workspace bcad_cu_pullback_workspace sizes for the generic path)
+    const size_t seg_bytes = generic_seg_ws(plan);
+    const bool can_seg = seg_bytes > 0 && a.workspace && a.ws_bytes >= seg_bytes;
+    int64_t off = 0, offw = 0, segoff = 0, seg_items = 0, segblk = 0;
     for (int j = 0; j < N; ++j) {
-        const bool wide = a.in_adj[j] && plan.vol / (plan.arg_vol[j] > 0 ? plan.arg_vol[j] : 1) >= 32;
-        g.adj[j] = wide ? nullptr : static_cast<T*>(a.in_adj[j]);
+        const int S = can_seg && a.in_adj[j] ? generic_segments(plan, j) : 0;
+        const bool col = S && generic_column_mode(plan, j);
+        if (col) gs.seg_col_mask |= 1u << j;
+        gs.seg_block[j] = segblk;
+        segblk += col ? ceil_div(plan.arg_vol[j], kThreads) * S : plan.arg_vol[j] * S;
+        const bool wide = a.in_adj[j] && S == 0 && reduced_along_last_axis(plan, j) &&
+                          plan.vol / (plan.arg_vol[j] > 0 ? plan.arg_vol[j] : 1) >= 32;
+        const bool full = a.in_adj[j] && plan.arg_vol[j] == plan.vol;
+        any_full |= full;
+        gf.adj[j] = full ? static_cast<T*>(a.in_adj[j]) : nullptr;
+        g.adj[j] = wide || S || full ? nullptr : static_cast<T*>(a.in_adj[j]);
         gw.adj[j] = wide ? static_cast<T*>(a.in_adj[j]) : nullptr;
+        gs.adj[j] = S ? static_cast<T*>(a.in_adj[j]) : nullptr;
+        gs.segs[j] = S;
+        gs.seg_offset[j] = segoff;
+        segoff += plan.arg_vol[j] * S;
+        if (S) seg_items += plan.arg_vol[j];
         g.adj_offset[j] = off;
         gw.adj_offset[j] = offw;
         if (g.adj[j]) off += plan.arg_vol[j];
@@ -407,6 +462,39 @@ int launch_pull_t(const PullArgs& a, std::string* err) {
     }
     g.adj_offset[N] = off;
     gw.adj_offset[N] = offw;
+    gs.seg_offset[N] = segoff;
+    gs.seg_block[N] = segblk;
+    gs.seg_ws = static_cast<double*>(a.workspace);
+    if (segoff > 0) {
+        if (recompute) bcad_dev::pull_generic_seg_kernel<Body, T, true><<<unsigned(segblk), kThreads, 0, a.stream>>>(gs);
+        else bcad_dev::pull_generic_seg_kernel<Body, T, false><<<unsigned(segblk), kThreads, 0, a.stream>>>(gs);
+        if (const int rc = cuda_status(cudaGetLastError(), err)) return rc;
+        bcad_dev::pull_generic_seg_finish<N, M, T><<<unsigned(ceil_div(seg_items, kThreads)), kThreads, 0, a.stream>>>(gs);
+        if (const int rc = cuda_status(cudaGetLastError(), err)) return rc;
+    }
+    if (any_full) {  // arguments of the output's shape: elementwise
+        constexpr int GV = generic_vec_width<Body, T>();
+        bool gvec = GV > 1 && generic_vec_ok(plan, GV);
+        for (int i = 0; i < M && gvec; ++i) {
+            if (gf.w[i] && !aligned16(gf.w[i])) gvec = false;
+            for (int j = 0; j < N && gvec; ++j)
+                if (gf.w[i] && gf.adj[j] && !recompute && !aligned16(gf.D[i * N + j])) gvec = false;
+        }
+        for (int j = 0; j < N && gvec; ++j) {
+            if (gf.adj[j] && !aligned16(gf.adj[j])) gvec = false;
+            if (recompute && plan.strides[j][plan.out_rank - 1] != 0 && !aligned16(gf.in[j])) gvec = false;
+        }
+        if (gvec) {
+            const int grid = generic_grid(plan.vol / GV);
+            if (recompute) bcad_dev::pull_generic_full_kernel<Body, T, GV, true><<<grid, kThreads, 0, a.stream>>>(gf);
+            else bcad_dev::pull_generic_full_kernel<Body, T, GV, false><<<grid, kThreads, 0, a.stream>>>(gf);
+        } else {
+            const int grid = generic_grid(plan.vol);
+            if (recompute) bcad_dev::pull_generic_full_kernel<Body, T, 1, true><<<grid, kThreads, 0, a.stream>>>(gf);
+            else bcad_dev::pull_generic_full_kernel<Body, T, 1, false><<<grid, kThreads, 0, a.stream>>>(gf);
+        }
+        if (const int rc = cuda_status(cudaGetLastError(), err)) return rc;
+    }
     if (off > 0) {
         const int grid = generic_grid(off);
         if (recompute) bcad_dev::pull_generic_kernel<Body, T, true, false><<<grid, kThreads, 0, a.stream>>>(g);

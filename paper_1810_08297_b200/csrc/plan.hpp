@@ -346,6 +346,44 @@ bool pull_scalar2d_ok(const Plan& plan) {
     return plan.is2d && pull_layout(plan, choose_tiling(plan, 1, class_mix(plan))).smem <= kMaxPullSmem;
 }
 
+// Generic (rank-N) pullback: an argument reduced over at least kSegMinCells
+// output cells per element is summed in segments of about kSegCells cells,
+// one CTA each, into fp64 partials the finisher adds in segment order.
+constexpr int64_t kSegMinCells = 4096, kSegCells = 4096;
+constexpr int kMaxSegs = 256;
+// True when argument j is broadcast along the output's last (fastest) axis:
+// its reduced cells then include consecutive addresses, so lanes striding
+// the reduction read coalesced; otherwise neighbouring ELEMENTS are
+// neighbouring addresses and a thread per element reads coalesced.
+inline bool reduced_along_last_axis(const Plan& plan, int j) {
+    const int last = plan.out_rank - 1;
+    return last >= 0 && plan.out_dims[last] > 1 && plan.strides[j][last] == 0;
+}
+// Arguments full along the last axis but reduced over kColMinCells or more
+// cells per element (e.g. (B,1,H) under a (B,T,H) output): a thread per
+// element, as above, but the reduction is also cut into segments over the
+// grid's y dimension until about kColThreads threads are in flight (a thread
+// walking all its cells alone leaves the SMs latency-bound when the argument
+// is small), at least kColSegCells cells per segment.
+constexpr int64_t kColMinCells = 64, kColSegCells = 16, kColThreads = int64_t(1) << 18;
+inline bool generic_column_mode(const Plan& plan, int j) { return !reduced_along_last_axis(plan, j); }
+inline int generic_segments(const Plan& plan, int j) {
+    const int64_t av = plan.arg_vol[j] > 0 ? plan.arg_vol[j] : 1;
+    const int64_t cnt = plan.vol / av;
+    if (generic_column_mode(plan, j)) {
+        if (cnt < kColMinCells) return 0;
+        const int64_t s = std::min<int64_t>({kMaxSegs, cnt / kColSegCells, ceil_div(kColThreads, av)});
+        return s > 1 ? int(s) : 0;
+    }
+    if (cnt < kSegMinCells) return 0;
+    return int(std::min<int64_t>(kMaxSegs, ceil_div(cnt, kSegCells)));
+}
+inline size_t generic_seg_ws(const Plan& plan) {
+    size_t b = 0;
+    for (int j = 0; j < plan.n; ++j) b += size_t(plan.arg_vol[j]) * size_t(generic_segments(plan, j)) * 8;
+    return b;
+}
+
 // Workspace of the tiled variant the width selects: vectors when the width
 // allows them, else one cell per thread. (A vector-width problem handed
 // unaligned views at launch uses the one-cell variant only if this
@@ -356,6 +394,7 @@ size_t pull_ws_t(const Plan& plan) {
     size_t ws = 256;
     if (pull_vec_shape_ok<T>(plan)) ws = std::max(ws, pull_layout(plan, choose_tiling(plan, V, class_mix(plan))).total);
     else if (pull_scalar2d_ok<T>(plan)) ws = std::max(ws, pull_layout(plan, choose_tiling(plan, 1, class_mix(plan))).total);
+    else ws = std::max(ws, align256(generic_seg_ws(plan)));  // generic: segmented reductions
     return ws;
 }
 
@@ -381,7 +420,20 @@ template <class T>
 int pull_launches_t(const Plan& plan) {
     int V = vec_width<T>();
     if (!pull_vec_shape_ok<T>(plan)) {
-        if (!pull_scalar2d_ok<T>(plan)) return 0;
+        if (!pull_scalar2d_ok<T>(plan)) {
+            // generic rank-N: elementwise (full-shape arguments), segmented
+            // reductions (+ finisher), thread- and warp-per-element kernels,
+            // each launched when some input uses it
+            bool full = false, seg = false, thread = false, warp = false;
+            for (int j = 0; j < plan.n; ++j) {
+                const int64_t cnt = plan.vol / (plan.arg_vol[j] > 0 ? plan.arg_vol[j] : 1);
+                if (plan.arg_vol[j] == plan.vol) full = true;
+                else if (generic_segments(plan, j)) seg = true;
+                else if (reduced_along_last_axis(plan, j) && cnt >= 32) warp = true;
+                else thread = true;
+            }
+            return full + 2 * seg + thread + warp;
+        }
         V = 1;
     }
     const Tiling t = choose_tiling(plan, V, class_mix(plan));

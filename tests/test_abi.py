@@ -121,3 +121,10 @@ def test_pullback_launch_count():
     assert native.pullback_launches(k, [(1024, 1024)] * 4 + [(1024,)] * 2, native.F32) == 1
     # (1,H) reductions over 1024 rows span CTAs: K2 + the finisher K2f
     assert native.pullback_launches(kb, [(1024, 1024)] * 4 + [(1, 1024)] * 3 + [(1024,)] * 2, native.F32) == 2
+    # generic rank-N (three irreducible axis groups): the full-shape argument's
+    # elementwise kernel + a segmented reduction (segments + finisher)
+    g = native.Kernel("mul")
+    assert native.pullback_launches(g, [(64, 256, 1024), (64, 1, 1024)], native.F32) == 3
+    assert native.pullback_launches(g, [(64, 256, 1024), (1, 256, 1)], native.F32) == 3
+    # ... a small reduction (< 64 cells per element): thread per element
+    assert native.pullback_launches(g, [(64, 8, 1024), (64, 1, 1024)], native.F32) == 2

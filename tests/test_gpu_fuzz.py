@@ -105,3 +105,39 @@ def test_fuzz_generic_rank3(gpu, oracle_lib, dtype):
         want_a64 = [w if e is None else e.astype(np.float64) + w for w, e in zip(want_a64, existing)]
         assert_grads(got_g, want_g, want_a64, shapes, out_shape, dtype, tag,
                      terms=step_terms(oracle_lib, gpu, name, ins, seeds))
+
+
+@pytest.mark.parametrize("dtype", [np.float32, np.float64])
+def test_fuzz_generic_segmented_reductions(gpu, oracle_lib, dtype):
+    """Generic rank-N problems whose reduced arguments sum >= 4096 output
+    cells per element (e.g. a (1, T, 1) argument of a (B, T, C) broadcast)
+    take the segmented pullback: one CTA per (element, segment), fp64
+    partials, a finisher in segment order; arguments full along the last axis
+    and reduced over >= 64 cells ((1, 1, C), and (B, 1, C) when T >= 64) take
+    its column form (a thread per element, the reduction cut into segments
+    over the grid). Both policies, accumulate flags, against the oracle's fp64
+    sums; and run to run bit-identical."""
+    rng = np.random.default_rng(91 if dtype == np.float32 else 92)
+    for case in range(8):
+        name = ["mul", "gate", "two", "blend"][case % 4]
+        n, m = oracle_lib.arity(name)
+        B, T, C = int(rng.integers(64, 160)), int(rng.integers(3, 12) if case % 2 == 0 else rng.integers(64, 90)), int(rng.integers(64, 300))
+        kinds = [(B, T, C), (1, T, 1), (B, 1, C), (1, 1, C)]
+        shapes = [kinds[0]] + [kinds[int(rng.integers(1, len(kinds)))] for _ in range(n - 1)]
+        if all(s != (1, T, 1) for s in shapes):
+            shapes[-1] = (1, T, 1)
+        ins = [rng.uniform(-1, 1, s).astype(dtype) for s in shapes]
+        out_shape = O.broadcast_shape_py(shapes)
+        seeds = [rng.uniform(-1, 1, out_shape).astype(dtype) for _ in range(m)]
+        existing = [rng.uniform(-1, 1, s).astype(dtype) if rng.integers(0, 3) == 0 else None for s in shapes]
+        policy = int(rng.integers(0, 2))
+        tag = f"segmented case {case} {name} {shapes} p{policy}"
+        got_p, _, got_g = gpu.step(name, ins, seeds=seeds, policy=policy, existing=existing)
+        _, _, got_g2 = gpu.step(name, ins, seeds=seeds, policy=policy, existing=existing)
+        for a, b in zip(got_g, got_g2):
+            assert np.array_equal(a, b), tag + ": not run-to-run bit-identical"
+        _, want_g, want_a64 = oracle_lib.mixed_step(name, ins, O.CACHE_FORWARD, seeds)
+        want_g = [w if e is None else (e.astype(np.float64) + w).astype(dtype) for w, e in zip(want_g, existing)]
+        want_a64 = [w if e is None else e.astype(np.float64) + w for w, e in zip(want_a64, existing)]
+        assert_grads(got_g, want_g, want_a64, shapes, out_shape, dtype, tag,
+                     terms=step_terms(oracle_lib, gpu, name, ins, seeds))
