@@ -719,15 +719,26 @@ __global__ void __launch_bounds__(kThreads, kPipe ? 2 : (kRecompute ? kRecompute
                         row_acc[(arg_slot<S, kDense>(p.slot, j) * trows + k * p.ty) * wpr + row_base] = 0.0;
                 continue;
             }
-            // reduced classes: fp64 sum of the rounded terms
+            // reduced classes: fp64 sum of the rounded terms. A dead row adds
+            // nothing to column / scalar partials (skipped: adding +0.0 to a
+            // sum that starts at +0.0 changes no bit); row sums need the zero
+            // for the lane shuffle. Each cell's sum starts from its first term
+            // rather than 0.0 + term: every sum these feed starts from +0.0,
+            // so the results are bit-identical and the adds are saved.
+            if (cls != kRow && !live) continue;
             double s[V];
 #pragma unroll
             for (int v = 0; v < V; ++v) {
                 s[v] = 0.0;
-                if (live)
+                bool first = true;
 #pragma unroll
-                    for (int i = 0; i < M; ++i)
-                        if (kDense || p.w[i]) s[v] += double(T(w[i].x[v] * D[i * N + j].x[v]));
+                for (int i = 0; i < M; ++i)
+                    if (kDense || p.w[i]) {
+                        const double t = double(T(w[i].x[v] * D[i * N + j].x[v]));
+                        s[v] = first ? t : s[v] + t;
+                        first = false;
+                    }
+                if (cls == kRow && !live) s[v] = 0.0;
             }
             if (cls == kCol) {
                 if constexpr (kAnyCol) {
