@@ -141,3 +141,57 @@ def test_fuzz_generic_segmented_reductions(gpu, oracle_lib, dtype):
         want_a64 = [w if e is None else e.astype(np.float64) + w for w, e in zip(want_a64, existing)]
         assert_grads(got_g, want_g, want_a64, shapes, out_shape, dtype, tag,
                      terms=step_terms(oracle_lib, gpu, name, ins, seeds))
+
+
+@pytest.mark.parametrize("dtype", [np.float32, np.float64])
+def test_generic_vector_and_scalar_paths_agree(gpu, oracle_lib, dtype):
+    """The generic rank-N kernels run 128-bit vectors of cells along the last
+    axis when it is a multiple of the vector width and every buffer is 16-byte
+    aligned (fwd_generic_vec_kernel, pull_generic_full_kernel), else one cell
+    per thread. The same problem on aligned buffers and on buffers offset by
+    one element (element-aligned only) must give bit-identical primals,
+    partials and adjoints under both policies, equal to the oracle."""
+    import torch
+    from paper_1810_08297_b200 import native
+    rng = np.random.default_rng(131)
+    B, T, C = 24, 70, 16  # three irreducible axis groups; C a multiple of 4 and 2
+    name = "gate"
+    shapes = [(B, T, C), (B, 1, C)]
+    ins = [rng.uniform(-1, 1, s).astype(dtype) for s in shapes]
+    seed = rng.uniform(-1, 1, (B, T, C)).astype(dtype)
+    k = native.Kernel(name)
+    tdt = torch.float32 if dtype == np.float32 else torch.float64
+
+    def buf(shape, offset, data=None):
+        n = int(np.prod(shape))
+        b = torch.empty(n + 4, dtype=tdt, device="cuda")[offset:offset + n].view(shape)
+        if data is not None:
+            b.copy_(torch.from_numpy(np.ascontiguousarray(data)).cuda())
+        return b
+
+    results = {}
+    for offset in (0, 1):
+        dins = [buf(s, offset, a) for s, a in zip(shapes, ins)]
+        prim = [buf((B, T, C), offset)]
+        parts = [buf((B, T, C), offset) for _ in range(k.n_in)]
+        native.forward(k, dins, prim, parts)
+        dseed = [buf((B, T, C), offset, seed)]
+        for policy_parts in ("cache", "recompute"):
+            adj = [buf(s, offset) for s in shapes]
+            native.pullback(k, shapes, dseed, parts if policy_parts == "cache" else None, dins, adj,
+                            workspace=native.new_workspace(k, shapes, tdt))
+            torch.cuda.synchronize()
+            results[(offset, policy_parts)] = [a.cpu().numpy() for a in adj]
+        results[(offset, "fwd")] = [prim[0].cpu().numpy()] + [p.cpu().numpy() for p in parts]
+    for key in ("fwd", "cache", "recompute"):
+        for a, b in zip(results[(0, key)], results[(1, key)]):
+            assert np.array_equal(a, b), f"{key}: vector and scalar paths differ"
+    want_p, want_d = oracle_lib.forward(name, ins)
+    rtol, atol = tol_for(dtype)
+    assert_close(results[(0, "fwd")][0], want_p[0], rtol, atol, "generic primal")
+    for j in range(k.n_in):
+        assert_close(results[(0, "fwd")][1 + j], want_d[j], rtol, atol, f"generic D{j}")
+    _, want_g, want_a64 = oracle_lib.mixed_step(name, ins, O.CACHE_FORWARD, [seed])
+    for key in ("cache", "recompute"):
+        assert_grads(results[(0, key)], want_g, want_a64, shapes, (B, T, C), dtype, f"generic {key}",
+                     terms=step_terms(oracle_lib, gpu, name, ins, [seed]))
