@@ -2,6 +2,7 @@
 #pragma once
 
 #include "bcad/arity_workload.hpp"
+#include "bcad/broadcast.hpp"
 #include "bcad/counters.hpp"
 #include "bcad/dual.hpp"
 #include "bcad/errors.hpp"

@@ -1,11 +1,15 @@
 // Evaluation counters of the drop-in API (reference proj/include/bcad/
 // counters.hpp:10-33, src/counters.cpp).
 //
-// These count HOST scalar evaluations only: BroadcastKernel::eval on reals or
-// duals (the finite-difference / Jacobian oracles and the body check at kernel
-// construction) calls the counting wrappers of bcad/dual.hpp exactly as the
-// reference's bodies do. Broadcasts run on the device and are not counted per
-// element (a per-cell counter would serialise the kernels): the device's
+// Element visits are counted like the reference counts them, once per
+// broadcast with the output volume (broadcast.hpp:123, forward.hpp:148): each
+// device forward, and each RecomputeReverse pullback (which re-derives every
+// cell's diagonals), visits every output cell exactly once.
+// Transcendental evaluations are counted for HOST scalar evaluations only:
+// BroadcastKernel::eval on reals or duals (the finite-difference / Jacobian
+// oracles and the body check at kernel construction) calls the counting
+// wrappers of bcad/dual.hpp exactly as the reference's bodies do. On the
+// device a per-evaluation counter would sit in the hot loop: the device's
 // transcendental census is measured with ncu instead
 // (smsp__inst_executed_pipe_xu, profiles/r02/census.md).
 #pragma once

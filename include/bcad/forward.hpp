@@ -2,13 +2,17 @@
 //   broadcast_apply         (reference proj/include/bcad/broadcast.hpp:102-125)
 //   broadcast_diag_jacobian (reference proj/include/bcad/forward.hpp:98-150)
 //   scatter_add             (reference proj/include/bcad/broadcast.hpp:210-217)
-// Each is one C-ABI call into the fused sm_100a kernels.
+// Each is one C-ABI call into the fused sm_100a kernels. Like the reference
+// (broadcast.hpp:123, forward.hpp:148), each broadcast adds its output volume
+// to the element-visit counter (bcad/counters.hpp): the launch visits every
+// output cell exactly once.
 #pragma once
 
 #include <array>
 #include <span>
 #include <vector>
 
+#include "bcad/counters.hpp"
 #include "bcad/kernel.hpp"
 #include "bcad/tensor.hpp"
 
@@ -91,12 +95,25 @@ void check_arity(const BroadcastKernel<Real>& kernel, std::size_t n, const char*
                             std::to_string(kernel.arity_in()) + " arguments, got " + std::to_string(n));
 }
 
+template <class Real>
+void require_single_stage(const BroadcastKernel<Real>& kernel, const char* who) {
+    if (kernel.is_composite())
+        throw ConfigError(std::string(who) + ": kernel " + kernel.name() + " is a composition (compose_kernels), "
+                          "which runs in broadcast_apply only; differentiate its stages as separate nodes");
+}
+
 }  // namespace detail
 
 template <class Real>
 std::vector<Tensor<Real>> broadcast_apply(const BroadcastKernel<Real>& kernel,
                                           std::span<const Tensor<Real>* const> args) {
     detail::check_arity(kernel, args.size(), "broadcast_apply");
+    if (kernel.is_composite()) {  // compose_kernels: one launch per stage
+        const std::vector<Tensor<Real>> mid = broadcast_apply<Real>(kernel.stages().f, args);
+        std::vector<const Tensor<Real>*> mp;
+        for (const Tensor<Real>& t : mid) mp.push_back(&t);
+        return broadcast_apply<Real>(kernel.stages().g, std::span<const Tensor<Real>* const>(mp));
+    }
     const Shape out = detail::out_shape_of<Real>(args);
     const auto shapes = detail::c_shapes<Real>(args);
     std::vector<const void*> in;
@@ -109,6 +126,7 @@ std::vector<Tensor<Real>> broadcast_apply(const BroadcastKernel<Real>& kernel,
     }
     check(bcad_cu_forward(kernel.handle(), dtype_of<Real>::value, kernel.arity_in(), in.data(), shapes.data(),
                           kernel.arity_out(), po.data(), nullptr, current_stream()));
+    count_element_visits(static_cast<std::uint64_t>(out.volume()));
     return outs;
 }
 
@@ -123,6 +141,7 @@ template <class Real>
 ForwardBroadcastResult<Real> broadcast_diag_jacobian(const BroadcastKernel<Real>& kernel,
                                                      std::span<const Tensor<Real>* const> args, bool want_primal) {
     detail::check_arity(kernel, args.size(), "broadcast_diag_jacobian");
+    detail::require_single_stage(kernel, "broadcast_diag_jacobian");
     const Shape out = detail::out_shape_of<Real>(args);
     const auto shapes = detail::c_shapes<Real>(args);
     const int n = kernel.arity_in(), m = kernel.arity_out();
@@ -144,6 +163,7 @@ ForwardBroadcastResult<Real> broadcast_diag_jacobian(const BroadcastKernel<Real>
         }
     check(bcad_cu_forward(kernel.handle(), dtype_of<Real>::value, n, in.data(), shapes.data(), m,
                           want_primal ? po.data() : nullptr, pp.data(), current_stream()));
+    count_element_visits(static_cast<std::uint64_t>(out.volume()));
     return r;
 }
 
@@ -193,6 +213,7 @@ ForwardBroadcastResult<Real> broadcast_diag_jacobian_reference(const BroadcastKe
                 part[static_cast<std::size_t>(i * n + j)][static_cast<std::size_t>(c)] = jac[static_cast<std::size_t>(i * n + j)];
         }
     }
+    count_element_visits(static_cast<std::uint64_t>(vol));
     ForwardBroadcastResult<Real> r;
     r.jacobian.out_shape = out;
     r.jacobian.outputs = m;

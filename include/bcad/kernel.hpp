@@ -5,7 +5,7 @@
 // CPU. std::function cannot run on a GPU, so every broadcast here runs a
 // compiled device functor registered in libbcad_cu.so under the kernel's
 // name — the library's own bodies (csrc/bodies.cuh) or a user's, registered
-// from the user's nvcc translation unit with BCAD_REGISTER_DEVICE_KERNEL
+// from the user's nvcc translation unit with BCAD_DEVICE_KERNEL
 // (bcad/device_kernel.cuh). The arity rules are the reference's
 // (kernel.hpp:30-35); a name with no device body throws UnknownPrimitive —
 // there is no CPU fallback.
@@ -20,9 +20,11 @@
 #pragma once
 
 #include <algorithm>
+#include <array>
 #include <cmath>
 #include <cstdint>
 #include <functional>
+#include <memory>
 #include <mutex>
 #include <set>
 #include <span>
@@ -40,7 +42,13 @@ namespace bcad {
 inline constexpr int kMaxKernelInputs = BCAD_CU_MAX_INPUTS;
 inline constexpr int kMaxKernelOutputs = BCAD_CU_MAX_OUTPUTS;
 
+template <class Real>
+class BroadcastKernel;
+
 namespace detail {
+
+template <class Real>
+struct ComposedStages;  // compose_kernels(g, f): the stages, applied f then g
 
 // One forward launch over `cells` probe points given as per-argument host
 // columns; returns the M primals and (when `jac`) the M*N partial columns.
@@ -119,14 +127,19 @@ public:
     int arity_out() const { return arity_out_; }
     const std::string& name() const { return name_; }
     bcad_cu_kernel handle() const { return handle_; }
-    bool may_raise() const { return bcad_cu_kernel_may_raise(handle_) != 0; }
-    bool has_host_body() const { return static_cast<bool>(real_body_); }
+    bool may_raise() const;
+    bool has_host_body() const;
+    // A kernel made by compose_kernels: no device body of its own; its stages
+    // run as one launch each (broadcast_apply), see compose_kernels below.
+    bool is_composite() const { return static_cast<bool>(stages_); }
+    const detail::ComposedStages<Real>& stages() const { return *stages_; }
 
     // One scalar evaluation (kernel.hpp:45-46). With a host body: the body,
     // as the reference does. Device-only kernels: one cell on the device
     // (synchronous); on duals the outputs carry J * (input perturbations),
     // J the device's M x N partials at the primal point.
     void eval(std::span<const Real> in, std::span<Real> out) const {
+        if (stages_) return eval_composite<Real>(in, out);
         if (real_body_) return real_body_(in, out);
         std::vector<std::vector<Real>> cols, prim;
         for (int j = 0; j < arity_in_; ++j) cols.push_back({in[static_cast<std::size_t>(j)]});
@@ -134,6 +147,7 @@ public:
         for (int i = 0; i < arity_out_; ++i) out[static_cast<std::size_t>(i)] = prim[static_cast<std::size_t>(i)][0];
     }
     void eval(std::span<const DualT> in, std::span<DualT> out) const {
+        if (stages_) return eval_composite<DualT>(in, out);
         if (dual_body_) return dual_body_(in, out);
         Tag tag{};
         int width = 0;
@@ -161,6 +175,16 @@ public:
     }
 
 private:
+    template <class R>
+    friend BroadcastKernel<R> compose_kernels(const BroadcastKernel<R>& g, const BroadcastKernel<R>& f);
+
+    BroadcastKernel(int arity_in, int arity_out, std::string name,
+                    std::shared_ptr<const detail::ComposedStages<Real>> stages)
+        : arity_in_(arity_in), arity_out_(arity_out), name_(std::move(name)), stages_(std::move(stages)) {}
+
+    template <class S>
+    void eval_composite(std::span<const S> in, std::span<S> out) const;
+
     void bind() {
         if (arity_in_ < 1 || arity_in_ > kMaxKernelInputs)
             throw ArityMismatch("kernel input arity " + std::to_string(arity_in_) + " outside [1, " +
@@ -234,7 +258,7 @@ private:
                                       "device body registered under that name (output " + std::to_string(i) +
                                       (bad_j < 0 ? " primal" : ", partial d/dx" + std::to_string(bad_j)) + " at " +
                                       at + ")); register the new body under its own name with "
-                                      "BCAD_REGISTER_DEVICE_KERNEL (bcad/device_kernel.cuh)");
+                                      "BCAD_DEVICE_KERNEL (bcad/device_kernel.cuh)");
                 }
             }
     }
@@ -245,7 +269,52 @@ private:
     bcad_cu_kernel handle_ = nullptr;
     std::function<void(std::span<const Real>, std::span<Real>)> real_body_;
     std::function<void(std::span<const DualT>, std::span<DualT>)> dual_body_;
+    std::shared_ptr<const detail::ComposedStages<Real>> stages_;
 };
+
+namespace detail {
+template <class Real>
+struct ComposedStages {
+    BroadcastKernel<Real> g, f;  // out = g(f(in))
+};
+}  // namespace detail
+
+template <class Real>
+bool BroadcastKernel<Real>::may_raise() const {
+    if (stages_) return stages_->f.may_raise() || stages_->g.may_raise();
+    return bcad_cu_kernel_may_raise(handle_) != 0;
+}
+
+template <class Real>
+bool BroadcastKernel<Real>::has_host_body() const {
+    if (stages_) return stages_->f.has_host_body() && stages_->g.has_host_body();
+    return static_cast<bool>(real_body_);
+}
+
+template <class Real>
+template <class S>
+void BroadcastKernel<Real>::eval_composite(std::span<const S> in, std::span<S> out) const {
+    std::array<S, kMaxKernelOutputs> mid;
+    stages_->f.eval(in, std::span<S>(mid.data(), static_cast<std::size_t>(stages_->f.arity_out())));
+    stages_->g.eval(std::span<const S>(mid.data(), static_cast<std::size_t>(stages_->g.arity_in())), out);
+}
+
+// g after f as one kernel (reference kernel.hpp:54-70). The reference fuses
+// the two bodies into one lambda run in a single element visit. Device bodies
+// are compiled functors and cannot be fused at run time, so here the composed
+// kernel runs its stages as one launch each in broadcast_apply (f over the
+// broadcast, then g elementwise over f's outputs): bit-identical to applying
+// f and then g, which is the reference's fusion law (test_broadcast.cpp:168-193).
+// Differentiating a composed kernel (broadcast_diag_jacobian / mixed_broadcast)
+// throws ConfigError: record the stages as two mixed nodes instead.
+template <class Real>
+BroadcastKernel<Real> compose_kernels(const BroadcastKernel<Real>& g, const BroadcastKernel<Real>& f) {
+    if (g.arity_in() != f.arity_out())
+        throw ArityMismatch("cannot compose: inner kernel produces " + std::to_string(f.arity_out()) +
+                            " outputs, outer expects " + std::to_string(g.arity_in()));
+    return BroadcastKernel<Real>(f.arity_in(), g.arity_out(), g.name() + "." + f.name(),
+                                 std::make_shared<const detail::ComposedStages<Real>>(detail::ComposedStages<Real>{g, f}));
+}
 
 template <class Real>
 BroadcastKernel<Real> identity_kernel() {  // kernel.hpp:72-76

@@ -76,6 +76,9 @@ void backprop_diag_device(Tape<Real>& tape, int node, const BroadcastKernel<Real
     check(bcad_cu_pullback(kernel.handle(), dtype_of<Real>::value, n, shapes.data(), m, w.data(),
                            cached ? parts.data() : nullptr, in_ptrs.data(), adj.data(), acc.data(), ws,
                            tape.workspace_bytes(node), current_stream()));
+    // RecomputeReverse re-derives the diagonals in K2r, visiting every output
+    // cell again (the reference reruns broadcast_diag_jacobian, mixed.hpp:85)
+    if (!cached) count_element_visits(static_cast<std::uint64_t>(tape.value(Var<Real>{&tape, node, 0}).volume()));
     for (auto& [first, scratch] : dup) tape.accumulate_adjoint(ins[static_cast<std::size_t>(first)], scratch);
 }
 
@@ -88,6 +91,7 @@ std::vector<Var<Real>> mixed_broadcast(Tape<Real>& tape, const BroadcastKernel<R
     if (static_cast<int>(inputs.size()) != kernel.arity_in())
         throw ArityMismatch("mixed_broadcast: kernel " + kernel.name() + " expects " +
                             std::to_string(kernel.arity_in()) + " inputs, got " + std::to_string(inputs.size()));
+    detail::require_single_stage(kernel, "mixed_broadcast");
     std::vector<const Tensor<Real>*> args;
     for (const Var<Real>& v : inputs) args.push_back(&tape.value(v));
     auto k = std::make_shared<BroadcastKernel<Real>>(kernel);

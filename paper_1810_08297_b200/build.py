@@ -170,11 +170,14 @@ REF_SUITES_B200 = os.path.join(ROOT, "tests", "cpp", "bin", "ref_suites_b200")
 # The reference's own doctest suites that exercise the drop-in surface,
 # compiled UNCHANGED against this repo's include/ (not the reference's) with
 # oracle/doctest_shim for the absent doctest.h, linked to libbcad_cu.so: every
-# Tensor lives in HBM and every broadcast runs on the B200. test_broadcast.cpp
-# is not among them: it drives the reference's host-side iteration API
-# (BroadcastPlan / plan_for_each, tensor_zip / tensor_map over arbitrary host
-# lambdas, broadcast_apply_reference), which has no device counterpart here.
-REF_SUITES = ["test_mixed", "test_hmlstm", "test_forward", "test_tape", "test_dual", "test_oracle"]
+# Tensor lives in HBM and every broadcast runs on the B200. The suites'
+# test-local lambda bodies get their device twins from
+# tests/cpp/ref_suite_bodies/ref_suite_bodies.cu (the porting step a reference
+# user takes for their own bodies). Not compiled: test_bench.cpp and
+# acceptance.cpp (they link the reference's CLI, which needs CLI11).
+REF_SUITES = ["test_mixed", "test_hmlstm", "test_forward", "test_tape", "test_dual", "test_oracle",
+              "test_broadcast"]
+REF_BODIES = os.path.join(ROOT, "tests", "cpp", "ref_suite_bodies", "ref_suite_bodies.cu")
 
 
 def build_ref_suites_b200(verbose: bool = False) -> list[str]:
@@ -199,12 +202,21 @@ def build_ref_suites_b200(verbose: bool = False) -> list[str]:
         cmd = flags + ["-c", src, "-o", obj]
         if _stale(obj, [src] + hdrs, cmd):
             todo.append((obj, [src] + hdrs, cmd, _digest([src] + hdrs, cmd)))
+    # the device twins of the suites' local bodies (nvcc, relocatable so the
+    # registration objects' static constructors run in the host-linked binary)
+    bobj = os.path.join(odir, "ref_suite_bodies.o")
+    objs.append(bobj)
+    bdeps = [REF_BODIES] + glob.glob(os.path.join(INCLUDE, "bcad", "*")) + glob.glob(os.path.join(CSRC, "*.cuh")) + \
+        glob.glob(os.path.join(CSRC, "*.hpp")) + [os.path.join(INCLUDE, "bcad_cu.h")]
+    bcmd = [nvcc(), *NVCC_FLAGS, "-c", REF_BODIES, "-o", bobj]
+    if _stale(bobj, bdeps, bcmd):
+        todo.append((bobj, bdeps, bcmd, _digest(bdeps, bcmd)))
     with cf.ThreadPoolExecutor(max(1, min(len(todo), os.cpu_count() or 4))) as ex:
         for (obj, deps, cmd, dg), f in [(t, ex.submit(_run, t[2], verbose)) for t in todo]:
             f.result()
             _stamp(obj, deps, cmd, dg)
-    link = [cxx(), "-o", REF_SUITES_B200, *objs, "-L" + PKG, "-lbcad_cu",
-            "-Wl,-rpath,$ORIGIN/../../../paper_1810_08297_b200"]
+    link = [nvcc(), *ARCH, "-o", REF_SUITES_B200, *objs, "-L" + PKG, "-lbcad_cu",
+            "-Xlinker", "-rpath,$ORIGIN/../../../paper_1810_08297_b200"]
     if todo or _stale(REF_SUITES_B200, objs + [LIB], link):
         _run(link, verbose)
         _stamp(REF_SUITES_B200, objs + [LIB], link)

@@ -172,4 +172,52 @@ TEST_CASE("a may-raise user body reports the failing output index") {
     CHECK_THROWS_AS((void)broadcast_diag_jacobian(k, false, b, z), DivisionByZero);
 }
 
+TEST_CASE("compose_kernels applies its stages in turn; differentiating a composition is refused") {
+    const BroadcastKernel<double> t(1, 1, "tanh"), s(1, 1, "sigmoid");
+    const BroadcastKernel<double> c = compose_kernels(s, t);
+    CHECK(c.is_composite());
+    CHECK(c.name() == "sigmoid.tanh");
+    Rng rng(37);
+    const Tensor<double> x = random_pm1<double>(Shape{8, 8}, rng);
+    const auto before = counter_totals().kernel_element_visits;
+    const auto fused = broadcast_apply(c, x);
+    CHECK(counter_totals().kernel_element_visits - before == 128);  // two launches over 64 cells
+    const auto two_pass = broadcast_apply(s, broadcast_apply(t, x)[0]);
+    const auto a = fused[0].to_host(), b = two_pass[0].to_host();
+    for (std::size_t e = 0; e < a.size(); ++e) CHECK(a[e] == b[e]);
+    // one scalar evaluation runs the stages too
+    const double p[1] = {0.3};
+    double y = 0, mid = 0, want = 0;
+    c.eval(std::span<const double>(p, 1), std::span<double>(&y, 1));
+    t.eval(std::span<const double>(p, 1), std::span<double>(&mid, 1));
+    s.eval(std::span<const double>(&mid, 1), std::span<double>(&want, 1));
+    CHECK(y == want);
+    CHECK_THROWS_AS((void)broadcast_diag_jacobian(c, false, x), ConfigError);
+    Tape<double> tape;
+    const Var<double> v = tape.input(x);
+    CHECK_THROWS_AS((void)mixed_broadcast(tape, c, {v}, MixedPolicy::CacheForward), ConfigError);
+    CHECK_THROWS_AS((void)compose_kernels(BroadcastKernel<double>(2, 1, "mul"), t), ArityMismatch);
+}
+
+TEST_CASE("reduce_sum_keepdims and make_broadcast_plan (bcad/broadcast.hpp)") {
+    Rng rng(41);
+    const Tensor<double> a = random_pm1<double>(Shape{5, 6}, rng);
+    const int ax[1] = {1};
+    const Tensor<double> r = reduce_sum_keepdims(a, std::span<const int>(ax, 1));
+    CHECK(r.shape() == (Shape{5, 1}));
+    const auto ha = a.to_host(), hr = r.to_host();
+    for (int i = 0; i < 5; ++i) {
+        double want = 0;
+        for (int j = 0; j < 6; ++j) want += ha[static_cast<std::size_t>(i * 6 + j)];
+        CHECK(mini::close(hr[static_cast<std::size_t>(i)], want, 1e-15, 1e-15));
+    }
+    const Shape shapes[2] = {Shape{5, 6}, Shape{5}};
+    const BroadcastPlan plan = make_broadcast_plan(std::span<const Shape>(shapes, 2));
+    CHECK(plan.volume == 30);
+    CHECK(plan.arg_strides[0] == (std::vector<std::int64_t>{6, 1}));
+    CHECK(plan.arg_strides[1] == (std::vector<std::int64_t>{1, 0}));
+    const int bad[1] = {2};
+    CHECK_THROWS_AS((void)reduce_sum_keepdims(a, std::span<const int>(bad, 1)), ShapeMismatch);
+}
+
 int main() { return mini::run_all(); }
