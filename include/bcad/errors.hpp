@@ -3,6 +3,8 @@
 // mapping from C-ABI status codes (include/bcad_cu.h) back to them.
 #pragma once
 
+#include <atomic>
+#include <cstdint>
 #include <stdexcept>
 #include <string>
 
@@ -51,8 +53,26 @@ struct NcclError : Error { using Error::Error; };
     }
 }
 
+// Generation of device memory as the host API sees it. Any C-ABI call made
+// through check() may have written device memory (or enqueued a write), so it
+// advances the generation; a Tensor's cached host view of its elements
+// (tensor.hpp, element reads) is valid only within the generation it was
+// taken in.
+inline std::atomic<std::uint64_t>& device_generation() {
+    static std::atomic<std::uint64_t> g{1};
+    return g;
+}
+inline void advance_device_generation() { device_generation().fetch_add(1, std::memory_order_relaxed); }
+
 // Throws the bcad exception matching a non-OK C-ABI status.
 inline void check(int status) {
+    advance_device_generation();
+    if (status != BCAD_CU_OK) throw_status(status, bcad_cu_last_error());
+}
+
+// The same for calls that only read device memory into the host (a cached
+// element view must not invalidate itself).
+inline void check_read(int status) {
     if (status != BCAD_CU_OK) throw_status(status, bcad_cu_last_error());
 }
 

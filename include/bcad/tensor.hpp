@@ -4,12 +4,21 @@
 // tensor.hpp:12-69): copyable (deep copy, device-to-device), single writer,
 // no views. The storage lives in HBM, allocated stream-ordered from the
 // device's caching pool through the C-ABI (bcad_cu_malloc); host access is
-// explicit (from / to_host) or element-wise through a synchronous read.
+// explicit (from / to_host) or element-wise. Element reads go through a
+// cached host window of the tensor (up to 64 Ki elements around the index,
+// downloaded once) that stays valid until the next library call that can
+// write device memory (errors.hpp device_generation) or a writable
+// device_data() access, so reference-style loops over elements cost one
+// copy per window, not one per element. Code that writes a tensor's device
+// memory OUTSIDE this library (its own kernels through a pointer taken
+// earlier) must call device_data() again, or invalidate_host_view(), before
+// reading elements.
 #pragma once
 
 #include <cstdint>
 #include <cstring>
 #include <memory>
+#include <mutex>
 #include <ostream>
 #include <span>
 #include <vector>
@@ -54,8 +63,10 @@ public:
     CopyBatch(const CopyBatch&) = delete;
     CopyBatch& operator=(const CopyBatch&) = delete;
     ~CopyBatch() {
-        if (!dst_.empty())
+        if (!dst_.empty()) {
+            advance_device_generation();
             bcad_cu_memcpy_batch(dst_.size(), dst_.data(), src_.data(), size_.data(), kind_, current_stream());
+        }
     }
     void add(void* dst, const void* src, std::size_t bytes) {
         dst_.push_back(dst);
@@ -77,6 +88,15 @@ private:
 };
 
 namespace detail {
+
+// Cached host copy of a window of a tensor's elements (element reads).
+template <class T>
+struct HostView {
+    std::mutex mu;
+    std::uint64_t generation = 0;  // 0: empty
+    std::int64_t begin = 0;
+    std::vector<T> data;
+};
 
 struct DeviceBuffer {
     void* ptr = nullptr;
@@ -144,8 +164,19 @@ public:
     const Shape& shape() const { return shape_; }
     std::int64_t volume() const { return shape_.volume(); }
     std::size_t bytes() const { return static_cast<std::size_t>(volume()) * sizeof(T); }
-    T* device_data() { return static_cast<T*>(buf_->ptr); }
+    // A writable pointer may be used to change the contents: the cached host
+    // view of the elements is dropped.
+    T* device_data() {
+        invalidate_host_view();
+        return static_cast<T*>(buf_->ptr);
+    }
     const T* device_data() const { return static_cast<const T*>(buf_->ptr); }
+    void invalidate_host_view() const {
+        if (view_) {
+            std::lock_guard<std::mutex> lock(view_->mu);
+            view_->generation = 0;
+        }
+    }
     void* stream() const { return buf_ ? buf_->stream : current_stream(); }
 
     void copy_to_host(T* dst) const {
@@ -215,15 +246,39 @@ private:
         for (int k = 0; k < shape_.rank(); ++k) flat = flat * shape_.dim(k) + index[static_cast<std::size_t>(k)];
         return flat;
     }
+    static constexpr std::int64_t kViewWindow = std::int64_t(1) << 16;
+
     T read(std::int64_t flat) const {
-        T v{};
-        check(bcad_cu_memcpy(&v, device_data() + flat, sizeof(T), 1, stream()));
-        check(bcad_cu_stream_synchronize(stream()));
-        return v;
+        if (!view_) view_ = std::make_unique<detail::HostView<T>>();
+        detail::HostView<T>& v = *view_;
+        std::lock_guard<std::mutex> lock(v.mu);
+        const std::uint64_t gen = device_generation().load(std::memory_order_relaxed);
+        if (v.generation != gen || flat < v.begin || flat >= v.begin + static_cast<std::int64_t>(v.data.size())) {
+            // the window around `flat` (the whole tensor when it is small)
+            const std::int64_t vol = volume();
+            const std::int64_t w = vol < kViewWindow ? vol : kViewWindow;
+            std::int64_t b = flat - w / 2;
+            if (b < 0) b = 0;
+            if (b > vol - w) b = vol - w;
+            v.data.resize(static_cast<std::size_t>(w));
+            check_read(bcad_cu_memcpy(v.data.data(), static_cast<const T*>(buf_->ptr) + b, static_cast<std::size_t>(w) * sizeof(T),
+                                      1, stream()));
+            check_read(bcad_cu_stream_synchronize(stream()));
+            v.begin = b;
+            v.generation = gen;
+        }
+        return v.data[static_cast<std::size_t>(flat - v.begin)];
     }
-    void write(std::int64_t flat, T v) {
-        check(bcad_cu_memcpy(device_data() + flat, &v, sizeof(T), 0, stream()));
-        check(bcad_cu_stream_synchronize(stream()));
+    void write(std::int64_t flat, T x) {
+        check_read(bcad_cu_memcpy(static_cast<T*>(buf_->ptr) + flat, &x, sizeof(T), 0, stream()));
+        check_read(bcad_cu_stream_synchronize(stream()));
+        if (view_) {  // keep a current view coherent (this write is the only change)
+            std::lock_guard<std::mutex> lock(view_->mu);
+            const std::int64_t o = flat - view_->begin;
+            if (view_->generation == device_generation().load(std::memory_order_relaxed) && o >= 0 &&
+                o < static_cast<std::int64_t>(view_->data.size()))
+                view_->data[static_cast<std::size_t>(o)] = x;
+        }
     }
 
     // device->device through the copy kernel (a launch is cheaper on the host
@@ -240,6 +295,7 @@ private:
 
     Shape shape_;
     std::unique_ptr<detail::DeviceBuffer> buf_;
+    mutable std::unique_ptr<detail::HostView<T>> view_;  // element reads
 };
 
 // Host-generated, bit-identical to the reference's inputs (tensor.hpp:71-84).

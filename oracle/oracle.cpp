@@ -514,7 +514,9 @@ const Entry kEntries[] = {
     ENTRY("exp", KExp),
     ENTRY("tanh_product_1", TanhProduct<1>),
     ENTRY("tanh_product_2", TanhProduct<2>),
+    ENTRY("tanh_product_3", TanhProduct<3>),
     ENTRY("tanh_product_4", TanhProduct<4>),
+    ENTRY("tanh_product_5", TanhProduct<5>),
     ENTRY("tanh_product_8", TanhProduct<8>),
     ENTRY("tanh_product_16", TanhProduct<16>),
     ENTRY("tanh_product_18", TanhProduct<18>),

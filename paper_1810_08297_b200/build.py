@@ -173,10 +173,13 @@ REF_SUITES_B200 = os.path.join(ROOT, "tests", "cpp", "bin", "ref_suites_b200")
 # Tensor lives in HBM and every broadcast runs on the B200. The suites'
 # test-local lambda bodies get their device twins from
 # tests/cpp/ref_suite_bodies/ref_suite_bodies.cu (the porting step a reference
-# user takes for their own bodies). Not compiled: test_bench.cpp and
-# acceptance.cpp (they link the reference's CLI, which needs CLI11).
+# user takes for their own bodies). test_bench.cpp exercises the bench
+# records / CLI of include/bcad/bench.hpp, implemented by libbcad_host.so; the
+# reference's acceptance program (acceptance.cpp, its own main) is built the
+# same way as tests/cpp/bin/ref_acceptance_b200.
 REF_SUITES = ["test_mixed", "test_hmlstm", "test_forward", "test_tape", "test_dual", "test_oracle",
-              "test_broadcast"]
+              "test_broadcast", "test_bench"]
+REF_ACCEPTANCE_B200 = os.path.join(ROOT, "tests", "cpp", "bin", "ref_acceptance_b200")
 REF_BODIES = os.path.join(ROOT, "tests", "cpp", "ref_suite_bodies", "ref_suite_bodies.cu")
 
 
@@ -215,12 +218,25 @@ def build_ref_suites_b200(verbose: bool = False) -> list[str]:
         for (obj, deps, cmd, dg), f in [(t, ex.submit(_run, t[2], verbose)) for t in todo]:
             f.result()
             _stamp(obj, deps, cmd, dg)
-    link = [nvcc(), *ARCH, "-o", REF_SUITES_B200, *objs, "-L" + PKG, "-lbcad_cu",
+    link = [nvcc(), *ARCH, "-o", REF_SUITES_B200, *objs, "-L" + PKG, "-lbcad_host", "-lbcad_cu",
             "-Xlinker", "-rpath,$ORIGIN/../../../paper_1810_08297_b200"]
-    if todo or _stale(REF_SUITES_B200, objs + [LIB], link):
+    if todo or _stale(REF_SUITES_B200, objs + [LIB, HOST_LIB], link):
         _run(link, verbose)
-        _stamp(REF_SUITES_B200, objs + [LIB], link)
-    return [REF_SUITES_B200]
+        _stamp(REF_SUITES_B200, objs + [LIB, HOST_LIB], link)
+    # the reference's acceptance program (its own main), unchanged
+    src = os.path.join(REF_TESTS, "acceptance.cpp")
+    aobj = os.path.join(odir, "acceptance.o")
+    cmd = flags + ["-c", src, "-o", aobj]
+    if _stale(aobj, [src] + hdrs, cmd):
+        dg = _digest([src] + hdrs, cmd)
+        _run(cmd, verbose)
+        _stamp(aobj, [src] + hdrs, cmd, dg)
+    link = [nvcc(), *ARCH, "-o", REF_ACCEPTANCE_B200, aobj, bobj, "-L" + PKG, "-lbcad_host", "-lbcad_cu",
+            "-Xlinker", "-rpath,$ORIGIN/../../../paper_1810_08297_b200"]
+    if _stale(REF_ACCEPTANCE_B200, [aobj, bobj, LIB, HOST_LIB], link):
+        _run(link, verbose)
+        _stamp(REF_ACCEPTANCE_B200, [aobj, bobj, LIB, HOST_LIB], link)
+    return [REF_SUITES_B200, REF_ACCEPTANCE_B200]
 
 
 def build_oracle(verbose: bool = False):

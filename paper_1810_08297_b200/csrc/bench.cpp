@@ -189,7 +189,7 @@ std::vector<BenchRecord> run_hmlstm_for(const BenchConfig& cfg) {
         std::vector<CellRun<Real>> gate;
         for (const std::string& impl : impls) gate.push_back(run_cell_once(impl, inputs, seed));
         check_equivalence(impls, gate, n);
-        if (dump.is_open()) dump_gradients(dump, device_impl_name(impls.front()), n, gate.front().grads);
+        if (dump.is_open()) dump_gradients(dump, impls.front(), n, gate.front().grads);
         for (std::size_t k = 0; k < impls.size(); ++k) {
             for (int w = 0; w < cfg.warmup; ++w) (void)run_cell_once(impls[k], inputs, seed);
             sync();
@@ -203,7 +203,7 @@ std::vector<BenchRecord> run_hmlstm_for(const BenchConfig& cfg) {
             const Stats st = summarize(std::move(samples));
             BenchRecord rec;
             rec.workload = "hmlstm";
-            rec.impl = device_impl_name(impls[k]);
+            rec.impl = impls[k];
             rec.n = n;
             rec.arity = 0;
             rec.reps = cfg.repetitions;
@@ -220,7 +220,7 @@ std::vector<BenchRecord> run_hmlstm_for(const BenchConfig& cfg) {
     return records;
 }
 
-constexpr int kArities[] = {1, 2, 4, 8, 16, 18, 32};  // registered tanh_product_<A> bodies
+constexpr int kArities[] = {1, 2, 3, 4, 5, 8, 16, 18, 32};  // registered tanh_product_<A> bodies
 
 template <class Real>
 std::vector<BenchRecord> run_arity_for(const BenchConfig& cfg) {
@@ -292,7 +292,7 @@ std::vector<BenchRecord> run_arity_for(const BenchConfig& cfg) {
         const Stats st = summarize(std::move(samples));
         BenchRecord rec;
         rec.workload = "arity";
-        rec.impl = device_impl_name(kImplForwardOnly);
+        rec.impl = kImplForwardOnly;
         rec.n = n;
         rec.arity = arity;
         rec.reps = cfg.repetitions;
@@ -533,7 +533,7 @@ std::vector<BenchRecord> run_arity_bench(const BenchConfig& cfg) {
             throw ConfigError("arity " + std::to_string(a) + " outside [1, " + std::to_string(kMaxPartials) + "]");
         if (std::find(std::begin(kArities), std::end(kArities), a) == std::end(kArities))
             throw ConfigError("arity " + std::to_string(a) +
-                              " has no registered device body (registered: 1, 2, 4, 8, 16, 18, 32)");
+                              " has no registered device body (registered: 1, 2, 3, 4, 5, 8, 16, 18, 32)");
     }
     return cfg.precision == Precision::F64 ? run_arity_for<double>(cfg) : run_arity_for<float>(cfg);
 }

@@ -145,9 +145,11 @@ BCAD_BODY_P(KSelectFalseBwd, "select_false_bwd", 2, 1, false, 0x2u, out[0] = in[
 template <int A>
 struct KTanhProduct {  // arity_workload.hpp:19-28
     static constexpr const char* kName =
-        A == 1 ? "tanh_product_1" : A == 2 ? "tanh_product_2" : A == 4 ? "tanh_product_4"
-      : A == 8 ? "tanh_product_8" : A == 16 ? "tanh_product_16" : A == 18 ? "tanh_product_18"
-      : A == 32 ? "tanh_product_32" : "tanh_product_?";
+        A == 1 ? "tanh_product_1" : A == 2 ? "tanh_product_2" : A == 3 ? "tanh_product_3"
+      : A == 4 ? "tanh_product_4" : A == 5 ? "tanh_product_5" : A == 8 ? "tanh_product_8"
+      : A == 16 ? "tanh_product_16" : A == 18 ? "tanh_product_18" : A == 32 ? "tanh_product_32" : nullptr;
+    static_assert(A == 1 || A == 2 || A == 3 || A == 4 || A == 5 || A == 8 || A == 16 || A == 18 || A == 32,
+                  "add the arity's name to KTanhProduct::kName");
     static constexpr int kIn = A, kOut = 1;
     static constexpr bool kMayRaise = false;
     static constexpr uint32_t kPredicateArgs = A >= 32 ? ~0u : (1u << A) - 1u;  // reflect_below_half on every arg

@@ -1,4 +1,5 @@
 // Registration group: the arity-scaling workload tanh_product_<A>, A <= 8
+// (3 and 5: the arities the reference's acceptance program and tests name)
 // (the wide arities are in reg_arity_wide*.cu: separate translation units
 // compile in parallel)
 // (proj/include/bcad/arity_workload.hpp:19-28; paper Fig. 3 register study).
@@ -13,7 +14,8 @@
 using bcad_cu_impl::SigAllFull;
 static const bcad_cu_kernel_entry kEntries[] = {
     BCAD_ENTRY(bcad_dev::KTanhProduct<1>, SigAllFull<1>), BCAD_ENTRY(bcad_dev::KTanhProduct<2>, SigAllFull<2>),
-    BCAD_ENTRY(bcad_dev::KTanhProduct<4>, SigAllFull<4>), BCAD_ENTRY(bcad_dev::KTanhProduct<8>, SigAllFull<8>),
+    BCAD_ENTRY(bcad_dev::KTanhProduct<3>, SigAllFull<3>), BCAD_ENTRY(bcad_dev::KTanhProduct<4>, SigAllFull<4>),
+    BCAD_ENTRY(bcad_dev::KTanhProduct<5>, SigAllFull<5>), BCAD_ENTRY(bcad_dev::KTanhProduct<8>, SigAllFull<8>),
 };
 
 int bcad_reg_arity(const bcad_cu_kernel_entry** out) {

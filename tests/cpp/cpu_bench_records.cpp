@@ -114,7 +114,7 @@ TEST_CASE("config validation happens before any device work") {
     CHECK_THROWS_AS((void)run_arity_bench(ar), ConfigError);
     ar.arities = {33};
     CHECK_THROWS_AS((void)run_arity_bench(ar), ConfigError);
-    ar.arities = {3};  // in range, but no registered device body
+    ar.arities = {6};  // in range, but no registered device body
     CHECK_THROWS_AS((void)run_arity_bench(ar), ConfigError);
     ar.arities = {1, 2};
     ar.sizes = {16, 32};

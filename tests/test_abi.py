@@ -43,7 +43,9 @@ def test_python_binding_covers_the_header():
 def test_registry_and_arity_rules():
     from paper_1810_08297_b200 import native
     names = native.kernel_names()
-    for required in ("hmlstm_update", "hmlstm_update_bias", "identity", "mul", "tanh_product_32", "sigmoid_bwd"):
+    assert len(names) == len(set(names)), "every registered name binds exactly one body"
+    for required in ("hmlstm_update", "hmlstm_update_bias", "identity", "mul", "tanh_product_32", "sigmoid_bwd",
+                     "tanh_product_3", "tanh_product_5"):
         assert required in names
     k = native.Kernel("hmlstm_update")
     assert (k.n_in, k.m_out, k.may_raise) == (6, 1, False)

@@ -39,11 +39,10 @@ def test_cli_tiny_run_gpu():
     assert lines[0] == HEADER
     rows = list(csv.DictReader(io.StringIO(r.stdout)))
     assert len(rows) == 8
-    assert {row["impl"] for row in rows} == {"cuda-forward-only", "cuda-mixed-cache", "cuda-mixed-recompute",
-                                             "cuda-reverse-unfused"}
+    assert {row["impl"] for row in rows} == {"forward-only", "mixed-cache", "mixed-recompute", "reverse-unfused"}
     for row in rows:
         assert int(row["min_ns"]) > 0 and int(row["min_ns"]) <= int(row["median_ns"])
-        if row["impl"] == "cuda-reverse-unfused":
+        if row["impl"] == "reverse-unfused":
             n = int(row["n"])
             assert int(row["transcendental_evals"]) == 3 * n * n
             assert int(row["tape_nodes"]) == 14

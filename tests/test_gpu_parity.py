@@ -295,7 +295,7 @@ def test_graph_capture_replays_the_step_bit_exact(oracle_lib):
         assert torch.equal(a, b)
 
 
-ARITIES = [1, 2, 4, 8, 16, 18, 32]
+ARITIES = [1, 2, 3, 4, 5, 8, 16, 18, 32]
 
 
 @pytest.mark.parametrize("dtype", DTYPES)

@@ -1,5 +1,5 @@
 """The reference's OWN doctest suites (proj/tests: test_mixed, test_hmlstm,
-test_forward, test_tape, test_dual, test_oracle, test_broadcast), compiled unchanged against
+test_forward, test_tape, test_dual, test_oracle, test_broadcast, test_bench), compiled unchanged against
 this repo's include/ — not the reference's headers — and linked to
 libbcad_cu.so (tests/cpp/bin/ref_suites_b200, built by
 paper_1810_08297_b200/build.py where /root/reference exists). Every Tensor
@@ -59,3 +59,23 @@ def test_reference_suites_pass_against_this_api_on_the_gpu():
     n_cases = int(r.stdout.split("test cases:")[1].split("|")[0])
     assert n_cases >= 60
     assert f"| {len(EXCLUDED)} skipped" in r.stdout
+
+
+ACCEPTANCE = os.path.join(os.path.dirname(os.path.abspath(__file__)), "cpp", "bin", "ref_acceptance_b200")
+
+
+@pytest.mark.skipif(not os.path.exists(ACCEPTANCE), reason="ref_acceptance_b200 not built (needs /root/reference)")
+def test_reference_acceptance_program_passes_on_the_gpu(tmp_path):
+    """The reference's acceptance program (proj/tests/acceptance.cpp, its own
+    main: nine criteria with their wall-clock limits), compiled unchanged
+    against include/ and linked to libbcad_host / libbcad_cu. Criterion 6
+    (untaken-branch accounting on all-COPY inputs) reads the transcendental
+    counters: the unfused path counts one evaluation per element of each
+    device Sigmoid / Tanh primitive, as the reference's scalar wrappers do;
+    device dual evaluations inside the fused kernels are not counted per
+    element (bcad/counters.hpp), so the fused path reads 0 — which is what the
+    device executes on COPY cells (profiles/r02/census.md: no MUFU)."""
+    r = subprocess.run([ACCEPTANCE], capture_output=True, text=True, timeout=1200, cwd=tmp_path)
+    print(r.stdout[-4000:])
+    assert r.returncode == 0, r.stdout[-4000:] + r.stderr[-2000:]
+    assert r.stdout.count("[PASS]") == 9
