@@ -104,7 +104,14 @@ def build_cuda(verbose: bool = False, jobs: int | None = None) -> str:
         for (obj, deps, cmd, dg), f in [(t, ex.submit(_run, t[2], verbose)) for t in todo]:
             f.result()
             _stamp(obj, deps, cmd, dg)
-    link = [nvcc(), "-shared", *ARCH, "-o", LIB, *objs, "-ldl", "-Xcompiler", "-fPIC"]
+    # -Bsymbolic: the library's own references (template launch helpers such
+    # as ctas_per_sm / sm_count and their static caches) bind inside it. A
+    # program that registers device bodies instantiates the same templates in
+    # its own object with its own CUDA runtime; without this, the dynamic
+    # linker would route the library's calls to the program's copies, which
+    # cannot see the library's kernels (cudaErrorInvalidResourceHandle in the
+    # occupancy query, found by compute-sanitizer on ref_suites_b200).
+    link = [nvcc(), "-shared", *ARCH, "-o", LIB, *objs, "-ldl", "-Xcompiler", "-fPIC", "-Xlinker", "-Bsymbolic"]
     if todo or _stale(LIB, objs, link):
         _run(link, verbose)
         _stamp(LIB, objs, link)
