@@ -66,14 +66,16 @@ def _check(results, ins, seed, dtype, B, H, tag):
                        extra=eps * np.abs(got.astype(np.float64)))
 
 
-@pytest.mark.parametrize("dtype,B,H", [(np.float32, 2048, 512), (np.float64, 1022, 256)])
-def test_two_ranks_one_process_fused_allreduce(oracle_lib, dtype, B, H):
+@pytest.mark.parametrize("dtype,B,H,world", [(np.float32, 2048, 512, 2), (np.float64, 1022, 256, 2),
+                                             (np.float32, 2050, 384, 4), (np.float32, 4096, 256, 8)])
+def test_ranks_in_one_process_fused_allreduce(oracle_lib, dtype, B, H, world):
+    """world ranks on world streams of one process (ragged row shards when B
+    is not a multiple of world); 8 = the peer group's maximum."""
     import torch
     from paper_1810_08297_b200 import native
     from paper_1810_08297_b200 import partition as P
     ins = O.hmlstm_inputs(oracle_lib, B, H, dtype, "bias")
     seed = np.random.default_rng(11).uniform(-1, 1, (B, H)).astype(dtype)
-    world = 2
     streams = [torch.cuda.Stream() for _ in range(world)]
     st = [_rank_state(torch, native, P, ins, seed, world, r, streams[r]) for r in range(world)]
     torch.cuda.synchronize()
