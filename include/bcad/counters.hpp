@@ -5,19 +5,22 @@
 // broadcast with the output volume (broadcast.hpp:123, forward.hpp:148): each
 // device forward, and each RecomputeReverse pullback (which re-derives every
 // cell's diagonals), visits every output cell exactly once.
-// Transcendental evaluations are counted for HOST scalar evaluations only:
-// BroadcastKernel::eval on reals or duals (the finite-difference / Jacobian
-// oracles and the body check at kernel construction) calls the counting
-// wrappers of bcad/dual.hpp exactly as the reference's bodies do. On the
-// device a per-evaluation counter would sit in the hot loop: the device's
-// transcendental census is measured with ncu instead
-// (smsp__inst_executed_pipe_xu, profiles/r02/census.md).
+// Transcendental evaluations (exp, log, sin, cos, tanh, sigmoid on reals and
+// duals) are counted where they execute: host scalar evaluations
+// (BroadcastKernel::eval with a host body, the finite-difference / Jacobian
+// oracles) through the counting wrappers of bcad/dual.hpp, and device kernels
+// through a per-thread tally flushed once per warp (bcad_cu_eval_counters).
+// The device census is armed by the first counter_totals() call, so programs
+// that never read the counters never pay for it; counts before that first
+// read are not included (the reference's tests read before and after).
 #pragma once
 
 #include <cstdint>
 #include <memory>
 #include <mutex>
 #include <vector>
+
+#include "bcad_cu.h"
 
 namespace bcad {
 
@@ -50,10 +53,40 @@ inline EvalCounters& local_counters() {
 
 }  // namespace detail
 
-inline void count_transcendental(std::uint64_t n = 1) { detail::local_counters().transcendental_evals += n; }
-inline void count_element_visits(std::uint64_t n) { detail::local_counters().kernel_element_visits += n; }
+namespace detail {
+inline int& count_pause_depth() {
+    static thread_local int d = 0;
+    return d;
+}
+}  // namespace detail
+
+inline void count_transcendental(std::uint64_t n = 1) {
+    if (detail::count_pause_depth() == 0) detail::local_counters().transcendental_evals += n;
+}
+inline void count_element_visits(std::uint64_t n) {
+    if (detail::count_pause_depth() == 0) detail::local_counters().kernel_element_visits += n;
+}
+
+// Pauses both censuses on this thread (host wrappers and the device launches
+// this thread makes): the library's own probe evaluations, which the
+// reference never performs, stay out of the totals.
+class CountPause {
+public:
+    CountPause() {
+        ++detail::count_pause_depth();
+        bcad_cu_count_pause(1);
+    }
+    ~CountPause() {
+        bcad_cu_count_pause(0);
+        --detail::count_pause_depth();
+    }
+    CountPause(const CountPause&) = delete;
+    CountPause& operator=(const CountPause&) = delete;
+};
 
 inline EvalCounters counter_totals() {
+    unsigned long long dev = 0;  // the device census (arms it on first use; synchronises)
+    const bool have_dev = bcad_cu_eval_counters(&dev) == BCAD_CU_OK;
     detail::CounterRegistry& r = detail::counter_registry();
     std::lock_guard<std::mutex> lock(r.mu);
     EvalCounters t;
@@ -61,6 +94,7 @@ inline EvalCounters counter_totals() {
         t.transcendental_evals += s->transcendental_evals;
         t.kernel_element_visits += s->kernel_element_visits;
     }
+    if (have_dev) t.transcendental_evals += dev;
     return t;
 }
 

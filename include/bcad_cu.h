@@ -166,6 +166,17 @@ int bcad_cu_pullback(bcad_cu_kernel k, int dtype, int n_in, const bcad_cu_shape*
 int bcad_cu_scatter_add(int dtype, void* acc, const bcad_cu_shape* acc_shape, const void* contrib,
                         const bcad_cu_shape* contrib_shape, int zero_first, void* stream);
 
+/* Transcendental evaluations (exp, log, sin, cos, tanh, sigmoid on reals or
+ * duals) executed by the device kernels so far, summed over devices
+ * (reference counters.hpp EvalCounters::transcendental_evals). The first call
+ * arms the census: launches made before it are not counted, launches after it
+ * add one atomic per warp. Synchronises every device that has counted. */
+int bcad_cu_eval_counters(unsigned long long* transcendental_evals);
+/* pause != 0: launches from this host thread stop counting until a matching
+ * bcad_cu_count_pause(0) (nested). Used for the library's own probe launches
+ * (the body check of BroadcastKernel), which the reference never runs. */
+int bcad_cu_count_pause(int pause);
+
 /* ptr[0..count) = value (dtype elements). */
 int bcad_cu_fill(int dtype, void* ptr, int64_t count, double value, void* stream);
 

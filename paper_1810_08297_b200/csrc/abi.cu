@@ -6,6 +6,7 @@
 
 #include <cstdint>
 #include <cstring>
+#include <atomic>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -106,6 +107,65 @@ private:
     int dev_ = 0;
     unsigned long long* word_ = nullptr;
 };
+
+// ---------------------------------------------- transcendental counters
+// Device census of transcendental evaluations (the reference's
+// EvalCounters::transcendental_evals). Armed by the first
+// bcad_cu_eval_counters call: from then on every body-evaluating launch on a
+// thread that has not paused counting adds its per-thread tallies into the
+// current device's kCountSlots slots (kernels.cuh count_flush). Programs that
+// never read the counters never arm them and launch with a null slot pointer.
+struct CountState {
+    std::mutex mu;
+    std::atomic<bool> armed{false};
+    unsigned long long* slots[kMaxDevices] = {};
+    bool dev_armed[kMaxDevices] = {};  // every registered unit's module armed on this device
+};
+CountState& count_state() {
+    static CountState c;
+    return c;
+}
+thread_local int t_count_pause = 0;
+
+int count_slots_alloc(int dev, unsigned long long** out) {
+    CountState& c = count_state();
+    std::lock_guard<std::mutex> lock(c.mu);
+    if (!c.slots[dev]) {
+        void* p = nullptr;
+        CU_TRY(cudaMalloc(&p, kCountSlots * sizeof(unsigned long long)), "cudaMalloc(counter slots)");
+        CU_TRY(cudaMemset(p, 0, kCountSlots * sizeof(unsigned long long)), "cudaMemset(counter slots)");
+        c.slots[dev] = static_cast<unsigned long long*>(p);
+    }
+    *out = c.slots[dev];
+    return BCAD_CU_OK;
+}
+
+// The slots a launch should count into (null: not armed, or paused on this
+// thread). Allocated when armed, so a launch under graph capture never
+// allocates.
+unsigned long long* count_slots_for_launch() {
+    CountState& c = count_state();
+    if (!c.armed.load(std::memory_order_acquire) || t_count_pause > 0) return nullptr;
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDevices) return nullptr;
+    std::lock_guard<std::mutex> lock(c.mu);
+    return c.dev_armed[dev] ? c.slots[dev] : nullptr;
+}
+
+// Sets every registered translation unit's c_count_armed on the current
+// device (each unit is one module with its own copy).
+int arm_units(const std::vector<const bcad_cu_kernel_entry*>& entries) {
+    std::vector<int (*)(int)> done;
+    for (const bcad_cu_kernel_entry* e : entries) {
+        if (!e->arm_counts) continue;
+        bool seen = false;
+        for (auto f : done) seen |= f == e->arm_counts;
+        if (seen) continue;
+        done.push_back(e->arm_counts);
+        if (e->arm_counts(1) != 0) return fail(BCAD_CU_ERR_CUDA, "cannot arm the transcendental census");
+    }
+    return BCAD_CU_OK;
+}
 
 // A may-raise launch decodes its error word synchronously, which a stream
 // under CUDA-graph capture cannot do: refuse explicitly instead.
@@ -331,6 +391,8 @@ int bcad_cu_register_kernel(const bcad_cu_kernel_entry* entry) {
             return fail(BCAD_CU_ERR_CONFIG, std::string("a device body is already registered under the name '") +
                                                 entry->name + "'; registering a second body under it is refused");
     registry().all.push_back(entry);
+    // a unit loaded after the census was armed counts from now on (current device)
+    if (count_state().armed.load(std::memory_order_acquire) && entry->arm_counts) (void)entry->arm_counts(1);
     return BCAD_CU_OK;
 }
 
@@ -379,6 +441,55 @@ int bcad_cu_broadcast_shape(int n, const bcad_cu_shape* shapes, bcad_cu_shape* o
     return BCAD_CU_OK;
 }
 
+int bcad_cu_eval_counters(unsigned long long* transcendental_evals) {
+    if (!transcendental_evals) return fail(BCAD_CU_ERR_CONFIG, "null output");
+    int dev = 0;
+    CU_TRY(cudaGetDevice(&dev), "cudaGetDevice");
+    if (dev < 0 || dev >= kMaxDevices) return fail(BCAD_CU_ERR_CUDA, "device ordinal out of range");
+    unsigned long long* cur = nullptr;
+    if (const int rc = count_slots_alloc(dev, &cur)) return rc;
+    bool need_arm = false;
+    {
+        std::lock_guard<std::mutex> lock(count_state().mu);
+        need_arm = !count_state().dev_armed[dev];
+    }
+    if (need_arm) {
+        std::vector<const bcad_cu_kernel_entry*> entries;
+        {
+            std::lock_guard<std::mutex> lock(registry().mu);
+            entries = registry().all;
+        }
+        if (const int rc = arm_units(entries)) return rc;
+        std::lock_guard<std::mutex> lock(count_state().mu);
+        count_state().dev_armed[dev] = true;
+    }
+    count_state().armed.store(true, std::memory_order_release);
+    unsigned long long total = 0;
+    std::vector<unsigned long long> h(kCountSlots);
+    for (int d = 0; d < kMaxDevices; ++d) {
+        unsigned long long* slots = nullptr;
+        {
+            std::lock_guard<std::mutex> lock(count_state().mu);
+            slots = count_state().slots[d];
+        }
+        if (!slots) continue;
+        CU_TRY(cudaSetDevice(d), "cudaSetDevice");
+        CU_TRY(cudaDeviceSynchronize(), "cudaDeviceSynchronize");
+        CU_TRY(cudaMemcpy(h.data(), slots, kCountSlots * sizeof(unsigned long long), cudaMemcpyDeviceToHost),
+               "cudaMemcpy(counter slots)");
+        for (unsigned long long v : h) total += v;
+    }
+    CU_TRY(cudaSetDevice(dev), "cudaSetDevice");
+    *transcendental_evals = total;
+    return BCAD_CU_OK;
+}
+
+int bcad_cu_count_pause(int pause) {
+    t_count_pause += pause ? 1 : -1;
+    if (t_count_pause < 0) t_count_pause = 0;
+    return BCAD_CU_OK;
+}
+
 int bcad_cu_forward(bcad_cu_kernel k, int dtype, int n_in, const void* const* in, const bcad_cu_shape* in_shapes,
                     int m_out, void* const* primal_out, void* const* partials_out, void* stream) {
     int rc = arity_check(k, n_in, m_out);
@@ -399,6 +510,7 @@ int bcad_cu_forward(bcad_cu_kernel k, int dtype, int n_in, const void* const* in
     }
     unsigned long long* word = ew.get();
     FwdArgs a{dtype, in, primal_out, partials_out, s, word, &plan};
+    a.tcount = count_slots_for_launch();
     if ((rc = k->fwd(a, &err))) return fail(rc, err);
     if (check) return check_error_word(word, s, plan);
     return BCAD_CU_OK;
@@ -491,6 +603,7 @@ int pullback_impl(bcad_cu_kernel k, int dtype, int n_in, const bcad_cu_shape* in
     unsigned long long* word = ew.get();
     PullArgs a{dtype, out_adj, partials, in, in_adj, accumulate, workspace, workspace_bytes, s, word, &plan};
     a.peer = peer;
+    a.tcount = count_slots_for_launch();
     if ((rc = k->pull(a, &err))) return fail(rc, err);
     if (check) return check_error_word(word, s, plan);
     return BCAD_CU_OK;

@@ -112,28 +112,6 @@ CellRun<Real> run_cell_once(const std::string& impl, const CellInputs<Real>& in,
     return r;
 }
 
-// Body evaluations' transcendentals, from the branch classes of the rows
-// (hmlstm.hpp:49-54): UPDATE sigmoid, sigmoid, tanh; FLUSH sigmoid, tanh;
-// COPY none.
-template <class Real>
-std::uint64_t body_transcendentals(const CellInputs<Real>& in) {
-    const std::vector<Real> z1 = in.z1.to_host(), z2 = in.z2.to_host();
-    const auto n = static_cast<std::uint64_t>(z1.size());
-    std::uint64_t per_column = 0;
-    for (std::size_t r = 0; r < z1.size(); ++r) {
-        if (z1[r] == Real(0) && z2[r] == Real(1)) per_column += 3;
-        else if (!(z1[r] == Real(0) && z2[r] == Real(0))) per_column += 2;
-    }
-    return per_column * n;
-}
-
-template <class Real>
-std::uint64_t transcendentals(const std::string& impl, const CellInputs<Real>& in, std::int64_t n) {
-    if (impl == kImplReverseUnfused) return 3 * static_cast<std::uint64_t>(n) * static_cast<std::uint64_t>(n);
-    const std::uint64_t once = body_transcendentals(in);
-    return impl == kImplMixedRecompute ? 2 * once : once;  // real primal pass + reverse-time recomputation
-}
-
 template <class Real>
 bool close_tensors(const Tensor<Real>& a, const Tensor<Real>& b, double rtol, double atol) {
     if (!(a.shape() == b.shape())) return false;
@@ -187,7 +165,12 @@ std::vector<BenchRecord> run_hmlstm_for(const BenchConfig& cfg) {
         const Tensor<Real> seed(Shape{n, n}, Real(1));
         // gate: nothing is timed unless every implementation agrees
         std::vector<CellRun<Real>> gate;
-        for (const std::string& impl : impls) gate.push_back(run_cell_once(impl, inputs, seed));
+        std::vector<std::uint64_t> evals;  // measured: the device census around each gate run
+        for (const std::string& impl : impls) {
+            const std::uint64_t before = counter_totals().transcendental_evals;
+            gate.push_back(run_cell_once(impl, inputs, seed));
+            evals.push_back(counter_totals().transcendental_evals - before);
+        }
         check_equivalence(impls, gate, n);
         if (dump.is_open()) dump_gradients(dump, impls.front(), n, gate.front().grads);
         for (std::size_t k = 0; k < impls.size(); ++k) {
@@ -212,7 +195,7 @@ std::vector<BenchRecord> run_hmlstm_for(const BenchConfig& cfg) {
             rec.mean_ns = st.mean_ns;
             rec.tape_nodes = gate[k].tape_nodes;
             rec.peak_cached_bytes = gate[k].peak_cached_bytes;
-            rec.transcendental_evals = transcendentals(impls[k], inputs, n);
+            rec.transcendental_evals = evals[k];
             rec.rng_seed = cfg.rng_seed;
             records.push_back(std::move(rec));
         }
@@ -237,7 +220,9 @@ std::vector<BenchRecord> run_arity_for(const BenchConfig& cfg) {
         for (int j = 0; j < arity; ++j) inputs.push_back(random_pm1<Real>(Shape{n, n}, rng));
         std::vector<const Tensor<Real>*> ptrs;
         for (const Tensor<Real>& t : inputs) ptrs.push_back(&t);
+        const std::uint64_t evals_before = counter_totals().transcendental_evals;
         ForwardBroadcastResult<Real> fwd = broadcast_diag_jacobian<Real>(kernel, ptrs, true);
+        const std::uint64_t evals = counter_totals().transcendental_evals - evals_before;  // measured
         if (fwd.jacobian.inputs != arity) throw Error("partial-vector width does not match the kernel arity");
 
         // spot checks against central differences of the device body at one
@@ -301,7 +286,7 @@ std::vector<BenchRecord> run_arity_for(const BenchConfig& cfg) {
         rec.mean_ns = st.mean_ns;
         rec.tape_nodes = 0;
         rec.peak_cached_bytes = (1 + static_cast<std::uint64_t>(arity)) * static_cast<std::uint64_t>(vol) * sizeof(Real);
-        rec.transcendental_evals = static_cast<std::uint64_t>(arity) * static_cast<std::uint64_t>(vol);  // one tanh per input
+        rec.transcendental_evals = evals;
         rec.rng_seed = cfg.rng_seed;
         records.push_back(std::move(rec));
     }

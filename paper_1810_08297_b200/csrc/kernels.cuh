@@ -114,6 +114,25 @@ __device__ __forceinline__ Pack<T, V> ld_arg(const T* base, int cls, int64_t r, 
     return a;
 }
 
+// Transcendental census (dual.cuh s_tcount): zero this thread's tally at
+// kernel entry; at exit, when counting is armed, add the warp's tallies with
+// one atomic into a slot spread by block index (kCountSlots).
+__device__ __forceinline__ void count_begin() { s_tcount[threadIdx.x] = 0; }
+// Host side: arms / disarms this translation unit's kernels on the current
+// device (registered with every kernel entry of the unit, BCAD_ENTRY).
+[[maybe_unused]] static int arm_counts_tu(int on) {
+    const uint32_t v = on ? 1u : 0u;
+    return cudaMemcpyToSymbol(c_count_armed, &v, sizeof v) == cudaSuccess ? 0 : 1;
+}
+__device__ __forceinline__ void count_flush(unsigned long long* slots) {
+    if (slots == nullptr) return;
+    const unsigned mask = __activemask();
+    const unsigned c = __reduce_add_sync(mask, s_tcount[threadIdx.x]);
+    if (int(threadIdx.x & 31) == __ffs(int(mask)) - 1 && c != 0)
+        atomicAdd(slots + ((blockIdx.x + blockIdx.y * 977u) & unsigned(bcad_cu_impl::kCountSlots - 1)),
+                  static_cast<unsigned long long>(c));
+}
+
 // Device error word: (status << 56) | flat output index; the lowest failing
 // cell wins (atomicMin), matching the reference's per-cell annotation.
 __device__ __forceinline__ void report_error(unsigned long long* word, int64_t flat) {
@@ -276,6 +295,7 @@ struct Fwd2DParams {
     int txv_shift, ty, rpt;
     int64_t tile_rows;
     unsigned long long* err;
+    unsigned long long* tcount;  // transcendental counter slots (null: counting not armed)
 };
 
 // K1. kReal: evaluate the real body (primal only). Otherwise the dual body,
@@ -306,6 +326,7 @@ __global__ void __launch_bounds__(kThreads, fwd_min_blocks<Body>()) fwd2d_kernel
     pdl_wait();
     pdl_trigger();
     if constexpr (Body::kMayRaise && !kReal) s_err_flag[threadIdx.x] = 0;
+    count_begin();
     const int tx = threadIdx.x & ((1 << p.txv_shift) - 1);
     const int ty = threadIdx.x >> p.txv_shift;
     const int vc = (blockIdx.x << p.txv_shift) + tx;
@@ -387,6 +408,7 @@ __global__ void __launch_bounds__(kThreads, fwd_min_blocks<Body>()) fwd2d_kernel
         }
         r = rn;
     }
+    count_flush(p.tcount);
 }
 
 // ------------------------------------------------------------- K2 params
@@ -415,6 +437,7 @@ struct Pull2DParams {
     unsigned int* tickets;
     int col_to_ws;        // column sums always leave fp64 partials (fused peer allreduce)
     unsigned long long* err;
+    unsigned long long* tcount;  // transcendental counter slots (null: counting not armed)
 };
 
 template <class T>
@@ -560,6 +583,7 @@ __global__ void __launch_bounds__(kThreads, kPipe ? 2 : (kRecompute ? kRecompute
     pdl_wait();
     pdl_trigger();  // lets the finisher (if any) be scheduled; it waits for this grid to complete
     if constexpr (Body::kMayRaise && kRecompute) s_err_flag[threadIdx.x] = 0;
+    if constexpr (kRecompute) count_begin();
 
     const int tid = threadIdx.x;
     const int txv = 1 << p.txv_shift;
@@ -772,6 +796,7 @@ __global__ void __launch_bounds__(kThreads, kPipe ? 2 : (kRecompute ? kRecompute
             if (rp < p.rows) prefetch_row(rp);
         }
     }
+    if constexpr (kRecompute) count_flush(p.tcount);
     if constexpr (!kAnyRow && !kAnyCol && !kAnyScal) return;
     else {
         __syncthreads();
@@ -1014,6 +1039,7 @@ struct GenParams {
     uint32_t seg_col_mask;
     int64_t seg_block[N + 1];
     unsigned long long* err;
+    unsigned long long* tcount;  // transcendental counter slots (null: counting not armed)
 };
 
 template <int N, int M, class T>
@@ -1044,6 +1070,7 @@ template <class Body, class T, bool kReal>
 __global__ void __launch_bounds__(kThreads) fwd_generic_kernel(const __grid_constant__ GenParams<Body::kIn, Body::kOut, T> p) {
     constexpr int N = Body::kIn, M = Body::kOut;
     if constexpr (Body::kMayRaise && !kReal) s_err_flag[threadIdx.x] = 0;
+    count_begin();
     for (int64_t cell = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; cell < p.vol;
          cell += int64_t(gridDim.x) * blockDim.x) {
         int64_t off[N];
@@ -1073,6 +1100,7 @@ __global__ void __launch_bounds__(kThreads) fwd_generic_kernel(const __grid_cons
             }
         }
     }
+    count_flush(p.tcount);
 }
 
 // Generic forward, V cells per thread along the output's last axis (when
@@ -1084,6 +1112,7 @@ template <class Body, class T, int V, bool kReal>
 __global__ void __launch_bounds__(kThreads) fwd_generic_vec_kernel(const __grid_constant__ GenParams<Body::kIn, Body::kOut, T> p) {
     constexpr int N = Body::kIn, M = Body::kOut;
     if constexpr (Body::kMayRaise && !kReal) s_err_flag[threadIdx.x] = 0;
+    count_begin();
     const int last = p.out_rank - 1;
     const int64_t nv = p.vol / V;
     for (int64_t v = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; v < nv; v += int64_t(gridDim.x) * blockDim.x) {
@@ -1129,6 +1158,7 @@ __global__ void __launch_bounds__(kThreads) fwd_generic_vec_kernel(const __grid_
             }
         }
     }
+    count_flush(p.tcount);
 }
 
 // Generic pullback of the arguments of the output's full shape (p.adj set
@@ -1140,6 +1170,7 @@ template <class Body, class T, int V, bool kRecompute>
 __global__ void __launch_bounds__(kThreads) pull_generic_full_kernel(const __grid_constant__ GenParams<Body::kIn, Body::kOut, T> p) {
     constexpr int N = Body::kIn, M = Body::kOut;
     if constexpr (Body::kMayRaise && kRecompute) s_err_flag[threadIdx.x] = 0;
+    if constexpr (kRecompute) count_begin();
     const int last = p.out_rank - 1;
     const int64_t nv = p.vol / V;
     for (int64_t v = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; v < nv; v += int64_t(gridDim.x) * blockDim.x) {
@@ -1187,6 +1218,7 @@ __global__ void __launch_bounds__(kThreads) pull_generic_full_kernel(const __gri
             st_vec<T, V>(p.adj[j] + cell, out);
         }
     }
+    if constexpr (kRecompute) count_flush(p.tcount);
 }
 
 // Generic pullback. kWarp = false: one thread per element e of each input j
@@ -1198,6 +1230,7 @@ template <class Body, class T, bool kRecompute, bool kWarp>
 __global__ void __launch_bounds__(kThreads) pull_generic_kernel(const __grid_constant__ GenParams<Body::kIn, Body::kOut, T> p) {
     constexpr int N = Body::kIn, M = Body::kOut;
     if constexpr (Body::kMayRaise && kRecompute) s_err_flag[threadIdx.x] = 0;
+    if constexpr (kRecompute) count_begin();
     const int64_t total = p.adj_offset[N];
     const int lane = threadIdx.x & 31;
     const int64_t first = kWarp ? (blockIdx.x * int64_t(blockDim.x) + threadIdx.x) / 32
@@ -1298,6 +1331,7 @@ __global__ void __launch_bounds__(kThreads) pull_generic_kernel(const __grid_con
             else p.adj[j][e] = acc ? T(double(p.adj[j][e]) + sum) : T(sum);
         }
     }
+    if constexpr (kRecompute) count_flush(p.tcount);
 }
 
 // Generic pullback, arguments reduced over many output cells, cut into
@@ -1347,6 +1381,7 @@ template <class Body, class T, bool kRecompute>
 __global__ void __launch_bounds__(kThreads) pull_generic_seg_kernel(const __grid_constant__ GenParams<Body::kIn, Body::kOut, T> p) {
     constexpr int N = Body::kIn;
     if constexpr (Body::kMayRaise && kRecompute) s_err_flag[threadIdx.x] = 0;
+    if constexpr (kRecompute) count_begin();
     __shared__ double part[kThreads];
     const int64_t b = blockIdx.x;
     int j = 0;
@@ -1433,6 +1468,7 @@ __global__ void __launch_bounds__(kThreads) pull_generic_seg_kernel(const __grid
             advance();
         }
         p.seg_ws[p.seg_offset[j] + e * S + seg] = sum;
+        if constexpr (kRecompute) count_flush(p.tcount);
         return;
     }
     {
@@ -1484,6 +1520,7 @@ __global__ void __launch_bounds__(kThreads) pull_generic_seg_kernel(const __grid
             advance();
         }
     }
+    if constexpr (kRecompute) count_flush(p.tcount);
     part[threadIdx.x] = sum;
     __syncthreads();
     for (int stride = kThreads / 2; stride > 0; stride >>= 1) {

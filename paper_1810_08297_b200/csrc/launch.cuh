@@ -170,6 +170,7 @@ int launch_fwd2d(const FwdArgs& a, std::string* err) {
     p.rows = plan.rows;
     p.cols = plan.cols;
     p.err = a.err;
+    p.tcount = a.tcount;
     bool dense = true;  // every output pointer present: no per-store checks
     for (int i = 0; i < M; ++i) {
         dense = dense && p.primal[i];
@@ -224,6 +225,7 @@ int launch_fwd_t(const FwdArgs& a, std::string* err) {
         for (int j = 0; j < N; ++j) g.partials[i * N + j] = a.partials ? static_cast<T*>(a.partials[i * N + j]) : nullptr;
     }
     g.err = a.err;
+    g.tcount = a.tcount;
     if constexpr (generic_vec_width<Body, T>() > 1) {
         constexpr int GV = generic_vec_width<Body, T>();
         bool gvec = generic_vec_ok(plan, GV);
@@ -322,6 +324,7 @@ int launch_pull2d(const PullArgs& a, std::string* err) {
     p.ws_col = reinterpret_cast<double*>(ws + L.ws_col);
     p.ws_scalar = reinterpret_cast<double*>(ws + L.ws_scalar);
     p.err = a.err;
+    p.tcount = a.tcount;
     int64_t fin_blocks = bcad_dev::pull_finish_blocks(plan.rows, plan.cols, p.n_row_tiles, p.n_col_tiles, nr, nc, ns);
     // cross-CTA reductions combined inside K2 (completion tickets) unless the
     // tiling asks for the separate K2f launch
@@ -430,6 +433,7 @@ int launch_pull_t(const PullArgs& a, std::string* err) {
         for (int j = 0; j < N; ++j) g.D[i * N + j] = recompute ? nullptr : static_cast<const T*>(a.partials[i * N + j]);
     }
     g.err = a.err;
+    g.tcount = a.tcount;
     bcad_dev::GenParams<N, M, T> gw = g, gs = g, gf = g;
     bool any_full = false;
     // arguments reduced over many cells per element: segmented (needs the
@@ -555,7 +559,7 @@ using SigPredRow = typename SigPredRowT<N, PRED>::type;
     bcad_cu_kernel_entry {                                                                             \
         Body::kName, Body::kIn, Body::kOut, Body::kMayRaise,                                           \
             &bcad_cu_impl::launch_fwd_any<Body __VA_OPT__(, ) __VA_ARGS__>,                             \
-            &bcad_cu_impl::launch_pull_any<Body __VA_OPT__(, ) __VA_ARGS__>                             \
+            &bcad_cu_impl::launch_pull_any<Body __VA_OPT__(, ) __VA_ARGS__>, &bcad_dev::arm_counts_tu   \
     }
 
 // A registered body whose forward also gets signature S but whose pullback
@@ -564,5 +568,5 @@ using SigPredRow = typename SigPredRowT<N, PRED>::type;
 #define BCAD_ENTRY_FWD_SIG(Body, S)                                                                    \
     bcad_cu_kernel_entry {                                                                             \
         Body::kName, Body::kIn, Body::kOut, Body::kMayRaise, &bcad_cu_impl::launch_fwd_any<Body, S>,    \
-            &bcad_cu_impl::launch_pull_any<Body>                                                       \
+            &bcad_cu_impl::launch_pull_any<Body>, &bcad_dev::arm_counts_tu                             \
     }

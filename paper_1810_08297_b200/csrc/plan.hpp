@@ -27,6 +27,9 @@ constexpr int kMaxRank = BCAD_CU_MAX_RANK;
 constexpr int kMaxIn = BCAD_CU_MAX_INPUTS;
 constexpr int kMaxOut = BCAD_CU_MAX_OUTPUTS;
 constexpr int kThreads = 256;
+// Device transcendental-evaluation counter slots (one atomic per warp into
+// slot blockIdx % kCountSlots; the host sums them, abi.cu)
+constexpr int kCountSlots = 1024;
 
 enum ArgClass : int { kFull = 0, kRow = 1, kCol = 2, kScalar = 3 };
 

@@ -21,6 +21,7 @@ struct FwdArgs {
     unsigned long long* err;
     const Plan* plan;
     const Tiling* tiling = nullptr;  // tuning override (tests / scripts/lab); null = choose_tiling
+    unsigned long long* tcount = nullptr;  // transcendental counter slots (null: counting not armed)
 };
 
 struct PullArgs {
@@ -37,6 +38,7 @@ struct PullArgs {
     const Plan* plan;
     const Tiling* tiling = nullptr;  // tuning override (tests / scripts/lab); null = choose_tiling
     const PeerParams* peer = nullptr;  // fused allreduce of the (1,H)-class adjoints over a peer group
+    unsigned long long* tcount = nullptr;  // transcendental counter slots (null: counting not armed)
 };
 
 size_t pull_ws_any(const Plan& plan, int dtype);
@@ -49,6 +51,9 @@ struct bcad_cu_kernel_entry {
     bool may_raise;
     int (*fwd)(const bcad_cu_impl::FwdArgs&, std::string*);
     int (*pull)(const bcad_cu_impl::PullArgs&, std::string*);
+    // arms (1) / disarms (0) the transcendental census of the translation
+    // unit that instantiated fwd / pull, on the current device
+    int (*arm_counts)(int on) = nullptr;
 };
 
 // One registration group per translation unit (compiled in parallel).

@@ -128,6 +128,8 @@ PROTOS = {
     "bcad_cu_pullback": (I, [VP, I, I, VP, I, VP, VP, VP, VP, VP, VP, SZ, VP]),
     "bcad_cu_scatter_add": (I, [I, VP, VP, VP, VP, I, VP]),
     "bcad_cu_fill": (I, [I, VP, I64, C.c_double, VP]),
+    "bcad_cu_eval_counters": (I, [C.POINTER(C.c_ulonglong)]),
+    "bcad_cu_count_pause": (I, [I]),
     "bcad_cu_device_count": (I, [C.POINTER(I)]),
     "bcad_cu_set_device": (I, [I]),
     "bcad_cu_get_device": (I, [C.POINTER(I)]),
@@ -300,6 +302,14 @@ def scatter_add(acc, contrib, zero_first=False, stream=None):
 
 def fill(t, value: float, stream=None):
     check(LIB.bcad_cu_fill(_dtype_code(t), _dptr(t), t.numel(), float(value), _stream_ptr(stream)))
+
+
+def transcendental_evals() -> int:
+    """Transcendental evaluations executed by the device kernels since the
+    census was armed (the first call arms it; bcad_cu_eval_counters)."""
+    v = C.c_ulonglong(0)
+    check(LIB.bcad_cu_eval_counters(C.byref(v)))
+    return int(v.value)
 
 
 def pullback_launches(kernel: Kernel, shapes, dtype_code: int) -> int:

@@ -21,13 +21,6 @@ pytestmark = pytest.mark.gpu
 BIN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "cpp", "bin", "ref_suites_b200")
 
 EXCLUDED = {
-    # The reference counts every transcendental evaluation and element visit
-    # in per-thread host counters (counters.hpp:10-33, bumped inside dual.hpp's
-    # rules and the broadcast loop). The device kernels do not count per
-    # element (a counter update per cell would serialise them); the device
-    # census is measured with ncu instead (profiles/r02/census.md).
-    "untaken-branch accounting: all-COPY inputs": "per-element host counters",
-    "recompute policy pays the forward differentiation twice": "per-element host counters",
     # A body that captures a host Dual of another differentiation and mixes it
     # in (TagMismatch on the CPU): device bodies are compiled pure functors and
     # cannot capture host state, so the situation cannot arise.
@@ -68,13 +61,12 @@ ACCEPTANCE = os.path.join(os.path.dirname(os.path.abspath(__file__)), "cpp", "bi
 def test_reference_acceptance_program_passes_on_the_gpu(tmp_path):
     """The reference's acceptance program (proj/tests/acceptance.cpp, its own
     main: nine criteria with their wall-clock limits), compiled unchanged
-    against include/ and linked to libbcad_host / libbcad_cu. Criterion 6
-    (untaken-branch accounting on all-COPY inputs) reads the transcendental
-    counters: the unfused path counts one evaluation per element of each
-    device Sigmoid / Tanh primitive, as the reference's scalar wrappers do;
-    device dual evaluations inside the fused kernels are not counted per
-    element (bcad/counters.hpp), so the fused path reads 0 — which is what the
-    device executes on COPY cells (profiles/r02/census.md: no MUFU)."""
+    against include/ and linked to libbcad_host / libbcad_cu. Criteria 6, 8
+    and 9 read the transcendental counters, which here are the device census
+    (bcad/counters.hpp: per-thread tallies in the kernels, armed by the first
+    counter_totals() call): 0 for the fused kernels on all-COPY inputs, 3 per
+    cell for the unfused primitives, A per cell for tanh_product_A, and the
+    RecomputeReverse policy exactly twice the cached one."""
     r = subprocess.run([ACCEPTANCE], capture_output=True, text=True, timeout=1200, cwd=tmp_path)
     print(r.stdout[-4000:])
     assert r.returncode == 0, r.stdout[-4000:] + r.stderr[-2000:]
