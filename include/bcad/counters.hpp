@@ -9,10 +9,11 @@
 // duals) are counted where they execute: host scalar evaluations
 // (BroadcastKernel::eval with a host body, the finite-difference / Jacobian
 // oracles) through the counting wrappers of bcad/dual.hpp, and device kernels
-// through a per-thread tally flushed once per warp (bcad_cu_eval_counters).
-// The device census is armed by the first counter_totals() call, so programs
-// that never read the counters never pay for it; counts before that first
-// read are not included (the reference's tests read before and after).
+// through a census launch that follows each body-evaluating launch and re-runs
+// the body per cell on counting scalars (bcad_cu_eval_counters). The device
+// census is armed by the first counter_totals() call, so programs that never
+// read the counters never pay for it; launches before that first read are not
+// counted (the reference's tests read before and after).
 #pragma once
 
 #include <cstdint>

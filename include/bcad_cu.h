@@ -169,8 +169,10 @@ int bcad_cu_scatter_add(int dtype, void* acc, const bcad_cu_shape* acc_shape, co
 /* Transcendental evaluations (exp, log, sin, cos, tanh, sigmoid on reals or
  * duals) executed by the device kernels so far, summed over devices
  * (reference counters.hpp EvalCounters::transcendental_evals). The first call
- * arms the census: launches made before it are not counted, launches after it
- * add one atomic per warp. Synchronises every device that has counted. */
+ * arms the census: launches made before it are not counted; after it, every
+ * body-evaluating launch is followed by a census launch that re-runs the body
+ * per cell on counting scalars (the production kernels carry no counting
+ * code). Synchronises every device that has counted. */
 int bcad_cu_eval_counters(unsigned long long* transcendental_evals);
 /* pause != 0: launches from this host thread stop counting until a matching
  * bcad_cu_count_pause(0) (nested). Used for the library's own probe launches

@@ -112,14 +112,13 @@ private:
 // Device census of transcendental evaluations (the reference's
 // EvalCounters::transcendental_evals). Armed by the first
 // bcad_cu_eval_counters call: from then on every body-evaluating launch on a
-// thread that has not paused counting adds its per-thread tallies into the
-// current device's kCountSlots slots (kernels.cuh count_flush). Programs that
-// never read the counters never arm them and launch with a null slot pointer.
+// thread that has not paused counting is followed by a census launch
+// (launch.cuh launch_census) that adds into the current device's kCountSlots
+// slots. Programs that never read the counters never arm them.
 struct CountState {
     std::mutex mu;
     std::atomic<bool> armed{false};
     unsigned long long* slots[kMaxDevices] = {};
-    bool dev_armed[kMaxDevices] = {};  // every registered unit's module armed on this device
 };
 CountState& count_state() {
     static CountState c;
@@ -149,22 +148,7 @@ unsigned long long* count_slots_for_launch() {
     int dev = 0;
     if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDevices) return nullptr;
     std::lock_guard<std::mutex> lock(c.mu);
-    return c.dev_armed[dev] ? c.slots[dev] : nullptr;
-}
-
-// Sets every registered translation unit's c_count_armed on the current
-// device (each unit is one module with its own copy).
-int arm_units(const std::vector<const bcad_cu_kernel_entry*>& entries) {
-    std::vector<int (*)(int)> done;
-    for (const bcad_cu_kernel_entry* e : entries) {
-        if (!e->arm_counts) continue;
-        bool seen = false;
-        for (auto f : done) seen |= f == e->arm_counts;
-        if (seen) continue;
-        done.push_back(e->arm_counts);
-        if (e->arm_counts(1) != 0) return fail(BCAD_CU_ERR_CUDA, "cannot arm the transcendental census");
-    }
-    return BCAD_CU_OK;
+    return c.slots[dev];
 }
 
 // A may-raise launch decodes its error word synchronously, which a stream
@@ -391,8 +375,6 @@ int bcad_cu_register_kernel(const bcad_cu_kernel_entry* entry) {
             return fail(BCAD_CU_ERR_CONFIG, std::string("a device body is already registered under the name '") +
                                                 entry->name + "'; registering a second body under it is refused");
     registry().all.push_back(entry);
-    // a unit loaded after the census was armed counts from now on (current device)
-    if (count_state().armed.load(std::memory_order_acquire) && entry->arm_counts) (void)entry->arm_counts(1);
     return BCAD_CU_OK;
 }
 
@@ -448,21 +430,6 @@ int bcad_cu_eval_counters(unsigned long long* transcendental_evals) {
     if (dev < 0 || dev >= kMaxDevices) return fail(BCAD_CU_ERR_CUDA, "device ordinal out of range");
     unsigned long long* cur = nullptr;
     if (const int rc = count_slots_alloc(dev, &cur)) return rc;
-    bool need_arm = false;
-    {
-        std::lock_guard<std::mutex> lock(count_state().mu);
-        need_arm = !count_state().dev_armed[dev];
-    }
-    if (need_arm) {
-        std::vector<const bcad_cu_kernel_entry*> entries;
-        {
-            std::lock_guard<std::mutex> lock(registry().mu);
-            entries = registry().all;
-        }
-        if (const int rc = arm_units(entries)) return rc;
-        std::lock_guard<std::mutex> lock(count_state().mu);
-        count_state().dev_armed[dev] = true;
-    }
     count_state().armed.store(true, std::memory_order_release);
     unsigned long long total = 0;
     std::vector<unsigned long long> h(kCountSlots);

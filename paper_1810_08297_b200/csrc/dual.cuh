@@ -36,25 +36,11 @@ __shared__ uint8_t s_err_flag[kMaxThreadsPerCta];
 
 // Transcendental-evaluation census (the reference's EvalCounters,
 // counters.hpp:20-22, bumped by dual.hpp:55-60 and 280-320 for exp, log, sin,
-// cos, tanh and sigmoid on reals and duals): a per-thread shared-memory tally
-// that every body-evaluating kernel zeroes at entry and adds, one atomic per
-// warp, into the library's counter slots at exit when counting is armed
-// (kernels.cuh count_begin / count_flush). A lane-vector dual counts one
-// evaluation per cell it carries.
-// The tally is kept only while the census is armed: c_count_armed is set per
-// device in every translation unit's module by the library
-// (kernels.cuh arm_counts_tu, through the registry entries), so a disarmed
-// kernel pays one uniform constant-bank test per evaluation and no
-// shared-memory traffic.
+// cos, tanh and sigmoid): the production kernels carry no counting code. When
+// the census is armed, each forward / RecomputeReverse pullback launch is
+// followed by one census launch that re-runs the body per cell on CountReal
+// scalars (census.cuh), which tally into this per-thread slot.
 __shared__ uint32_t s_tcount[kMaxThreadsPerCta];
-static __constant__ uint32_t c_count_armed = 0;
-BCAD_HD void count_tr(uint32_t n) {
-#ifdef __CUDA_ARCH__
-    if (c_count_armed) s_tcount[threadIdx.x] += n;
-#else
-    (void)n;
-#endif
-}
 
 BCAD_HD void raise_status(uint32_t code) {
 #ifdef __CUDA_ARCH__
@@ -98,18 +84,18 @@ BCAD_HD F raw_sigmoid(F x) {
 
 // Real-body primitives (dual.hpp:55-63): what the generic kernel bodies call
 // when instantiated on plain reals (the primal-only / broadcast_apply path).
-BCAD_HD float sigmoid(float x) { count_tr(1); return raw_sigmoid(x); }
-BCAD_HD double sigmoid(double x) { count_tr(1); return raw_sigmoid(x); }
-BCAD_HD float tanh(float x) { count_tr(1); return d_tanh(x); }
-BCAD_HD double tanh(double x) { count_tr(1); return d_tanh(x); }
-BCAD_HD float exp(float x) { count_tr(1); return d_exp(x); }
-BCAD_HD double exp(double x) { count_tr(1); return d_exp(x); }
-BCAD_HD float log(float x) { count_tr(1); return d_log(x); }
-BCAD_HD double log(double x) { count_tr(1); return d_log(x); }
-BCAD_HD float sin(float x) { count_tr(1); return d_sin(x); }
-BCAD_HD double sin(double x) { count_tr(1); return d_sin(x); }
-BCAD_HD float cos(float x) { count_tr(1); return d_cos(x); }
-BCAD_HD double cos(double x) { count_tr(1); return d_cos(x); }
+BCAD_HD float sigmoid(float x) { return raw_sigmoid(x); }
+BCAD_HD double sigmoid(double x) { return raw_sigmoid(x); }
+BCAD_HD float tanh(float x) { return d_tanh(x); }
+BCAD_HD double tanh(double x) { return d_tanh(x); }
+BCAD_HD float exp(float x) { return d_exp(x); }
+BCAD_HD double exp(double x) { return d_exp(x); }
+BCAD_HD float log(float x) { return d_log(x); }
+BCAD_HD double log(double x) { return d_log(x); }
+BCAD_HD float sin(float x) { return d_sin(x); }
+BCAD_HD double sin(double x) { return d_sin(x); }
+BCAD_HD float cos(float x) { return d_cos(x); }
+BCAD_HD double cos(double x) { return d_cos(x); }
 BCAD_HD float sqrt(float x) { return d_sqrt(x); }
 BCAD_HD double sqrt(double x) { return d_sqrt(x); }
 BCAD_HD float abs(float x) { return ::fabsf(x); }
@@ -284,30 +270,24 @@ BCAD_HD Dual<T, N> chain(const Dual<T, N>& a, T p, T scale) {
 
 // Unary rules (dual.hpp:280-342).
 template <class T, int N> BCAD_HD Dual<T, N> exp(const Dual<T, N>& a) {
-    count_tr(1);
     const T p = d_exp(a.v);
     return chain(a, p, p);
 }
 template <class T, int N> BCAD_HD Dual<T, N> log(const Dual<T, N>& a) {
     if (!(a.v > T(0))) raise_status(kDevDomainError);
-    count_tr(1);
     return chain(a, d_log(a.v), T(1) / a.v);
 }
 template <class T, int N> BCAD_HD Dual<T, N> sin(const Dual<T, N>& a) {
-    count_tr(1);
     return chain(a, d_sin(a.v), d_cos(a.v));
 }
 template <class T, int N> BCAD_HD Dual<T, N> cos(const Dual<T, N>& a) {
-    count_tr(1);
     return chain(a, d_cos(a.v), -d_sin(a.v));
 }
 template <class T, int N> BCAD_HD Dual<T, N> tanh(const Dual<T, N>& a) {
-    count_tr(1);
     const T t = d_tanh(a.v);
     return chain(a, t, T(1) - t * t);
 }
 template <class T, int N> BCAD_HD Dual<T, N> sigmoid(const Dual<T, N>& a) {
-    count_tr(1);
     const T s = raw_sigmoid(a.v);
     return chain(a, s, s * (T(1) - s));
 }
@@ -493,11 +473,9 @@ BCAD_HD VDual<T, N, V> vchain(const VDual<T, N, V>& a, F&& prim_and_scale) {
     return r;
 }
 template <class T, int N, int V> BCAD_HD VDual<T, N, V> exp(const VDual<T, N, V>& a) {
-    count_tr(V);
     return vchain(a, [](T x, T& p, T& s) { p = d_exp(x); s = p; });
 }
 template <class T, int N, int V> BCAD_HD VDual<T, N, V> log(const VDual<T, N, V>& a) {
-    count_tr(V);
     return vchain(a, [](T x, T& p, T& s) {
         if (!(x > T(0))) raise_status(kDevDomainError);
         p = d_log(x);
@@ -505,19 +483,15 @@ template <class T, int N, int V> BCAD_HD VDual<T, N, V> log(const VDual<T, N, V>
     });
 }
 template <class T, int N, int V> BCAD_HD VDual<T, N, V> sin(const VDual<T, N, V>& a) {
-    count_tr(V);
     return vchain(a, [](T x, T& p, T& s) { p = d_sin(x); s = d_cos(x); });
 }
 template <class T, int N, int V> BCAD_HD VDual<T, N, V> cos(const VDual<T, N, V>& a) {
-    count_tr(V);
     return vchain(a, [](T x, T& p, T& s) { p = d_cos(x); s = -d_sin(x); });
 }
 template <class T, int N, int V> BCAD_HD VDual<T, N, V> tanh(const VDual<T, N, V>& a) {
-    count_tr(V);
     return vchain(a, [](T x, T& p, T& s) { p = d_tanh(x); s = T(1) - p * p; });
 }
 template <class T, int N, int V> BCAD_HD VDual<T, N, V> sigmoid(const VDual<T, N, V>& a) {
-    count_tr(V);
     return vchain(a, [](T x, T& p, T& s) { p = raw_sigmoid(x); s = p * (T(1) - p); });
 }
 template <class T, int N, int V> BCAD_HD VDual<T, N, V> sqrt(const VDual<T, N, V>& a) {

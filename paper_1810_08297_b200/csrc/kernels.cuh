@@ -23,6 +23,7 @@
 #pragma once
 
 #include <cstdint>
+#include <type_traits>
 #include <cuda_runtime.h>
 
 #include "dual.cuh"
@@ -114,16 +115,11 @@ __device__ __forceinline__ Pack<T, V> ld_arg(const T* base, int cls, int64_t r, 
     return a;
 }
 
-// Transcendental census (dual.cuh s_tcount): zero this thread's tally at
-// kernel entry; at exit, when counting is armed, add the warp's tallies with
-// one atomic into a slot spread by block index (kCountSlots).
+// Transcendental census (census.cuh; dual.cuh s_tcount): zero this thread's
+// tally at kernel entry; at exit add the warp's tallies with one atomic into
+// a slot spread by block index (kCountSlots).
 __device__ __forceinline__ void count_begin() { s_tcount[threadIdx.x] = 0; }
-// Host side: arms / disarms this translation unit's kernels on the current
-// device (registered with every kernel entry of the unit, BCAD_ENTRY).
-[[maybe_unused]] static int arm_counts_tu(int on) {
-    const uint32_t v = on ? 1u : 0u;
-    return cudaMemcpyToSymbol(c_count_armed, &v, sizeof v) == cudaSuccess ? 0 : 1;
-}
+
 __device__ __forceinline__ void count_flush(unsigned long long* slots) {
     if (slots == nullptr) return;
     const unsigned mask = __activemask();
@@ -295,7 +291,6 @@ struct Fwd2DParams {
     int txv_shift, ty, rpt;
     int64_t tile_rows;
     unsigned long long* err;
-    unsigned long long* tcount;  // transcendental counter slots (null: counting not armed)
 };
 
 // K1. kReal: evaluate the real body (primal only). Otherwise the dual body,
@@ -326,7 +321,6 @@ __global__ void __launch_bounds__(kThreads, fwd_min_blocks<Body>()) fwd2d_kernel
     pdl_wait();
     pdl_trigger();
     if constexpr (Body::kMayRaise && !kReal) s_err_flag[threadIdx.x] = 0;
-    count_begin();
     const int tx = threadIdx.x & ((1 << p.txv_shift) - 1);
     const int ty = threadIdx.x >> p.txv_shift;
     const int vc = (blockIdx.x << p.txv_shift) + tx;
@@ -408,7 +402,6 @@ __global__ void __launch_bounds__(kThreads, fwd_min_blocks<Body>()) fwd2d_kernel
         }
         r = rn;
     }
-    count_flush(p.tcount);
 }
 
 // ------------------------------------------------------------- K2 params
@@ -437,7 +430,6 @@ struct Pull2DParams {
     unsigned int* tickets;
     int col_to_ws;        // column sums always leave fp64 partials (fused peer allreduce)
     unsigned long long* err;
-    unsigned long long* tcount;  // transcendental counter slots (null: counting not armed)
 };
 
 template <class T>
@@ -583,7 +575,6 @@ __global__ void __launch_bounds__(kThreads, kPipe ? 2 : (kRecompute ? kRecompute
     pdl_wait();
     pdl_trigger();  // lets the finisher (if any) be scheduled; it waits for this grid to complete
     if constexpr (Body::kMayRaise && kRecompute) s_err_flag[threadIdx.x] = 0;
-    if constexpr (kRecompute) count_begin();
 
     const int tid = threadIdx.x;
     const int txv = 1 << p.txv_shift;
@@ -796,7 +787,6 @@ __global__ void __launch_bounds__(kThreads, kPipe ? 2 : (kRecompute ? kRecompute
             if (rp < p.rows) prefetch_row(rp);
         }
     }
-    if constexpr (kRecompute) count_flush(p.tcount);
     if constexpr (!kAnyRow && !kAnyCol && !kAnyScal) return;
     else {
         __syncthreads();
@@ -1039,7 +1029,7 @@ struct GenParams {
     uint32_t seg_col_mask;
     int64_t seg_block[N + 1];
     unsigned long long* err;
-    unsigned long long* tcount;  // transcendental counter slots (null: counting not armed)
+    unsigned long long* tcount;  // census kernel: transcendental counter slots
 };
 
 template <int N, int M, class T>
@@ -1070,7 +1060,6 @@ template <class Body, class T, bool kReal>
 __global__ void __launch_bounds__(kThreads) fwd_generic_kernel(const __grid_constant__ GenParams<Body::kIn, Body::kOut, T> p) {
     constexpr int N = Body::kIn, M = Body::kOut;
     if constexpr (Body::kMayRaise && !kReal) s_err_flag[threadIdx.x] = 0;
-    count_begin();
     for (int64_t cell = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; cell < p.vol;
          cell += int64_t(gridDim.x) * blockDim.x) {
         int64_t off[N];
@@ -1100,7 +1089,6 @@ __global__ void __launch_bounds__(kThreads) fwd_generic_kernel(const __grid_cons
             }
         }
     }
-    count_flush(p.tcount);
 }
 
 // Generic forward, V cells per thread along the output's last axis (when
@@ -1112,7 +1100,6 @@ template <class Body, class T, int V, bool kReal>
 __global__ void __launch_bounds__(kThreads) fwd_generic_vec_kernel(const __grid_constant__ GenParams<Body::kIn, Body::kOut, T> p) {
     constexpr int N = Body::kIn, M = Body::kOut;
     if constexpr (Body::kMayRaise && !kReal) s_err_flag[threadIdx.x] = 0;
-    count_begin();
     const int last = p.out_rank - 1;
     const int64_t nv = p.vol / V;
     for (int64_t v = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; v < nv; v += int64_t(gridDim.x) * blockDim.x) {
@@ -1158,7 +1145,6 @@ __global__ void __launch_bounds__(kThreads) fwd_generic_vec_kernel(const __grid_
             }
         }
     }
-    count_flush(p.tcount);
 }
 
 // Generic pullback of the arguments of the output's full shape (p.adj set
@@ -1170,7 +1156,6 @@ template <class Body, class T, int V, bool kRecompute>
 __global__ void __launch_bounds__(kThreads) pull_generic_full_kernel(const __grid_constant__ GenParams<Body::kIn, Body::kOut, T> p) {
     constexpr int N = Body::kIn, M = Body::kOut;
     if constexpr (Body::kMayRaise && kRecompute) s_err_flag[threadIdx.x] = 0;
-    if constexpr (kRecompute) count_begin();
     const int last = p.out_rank - 1;
     const int64_t nv = p.vol / V;
     for (int64_t v = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; v < nv; v += int64_t(gridDim.x) * blockDim.x) {
@@ -1218,7 +1203,6 @@ __global__ void __launch_bounds__(kThreads) pull_generic_full_kernel(const __gri
             st_vec<T, V>(p.adj[j] + cell, out);
         }
     }
-    if constexpr (kRecompute) count_flush(p.tcount);
 }
 
 // Generic pullback. kWarp = false: one thread per element e of each input j
@@ -1230,7 +1214,6 @@ template <class Body, class T, bool kRecompute, bool kWarp>
 __global__ void __launch_bounds__(kThreads) pull_generic_kernel(const __grid_constant__ GenParams<Body::kIn, Body::kOut, T> p) {
     constexpr int N = Body::kIn, M = Body::kOut;
     if constexpr (Body::kMayRaise && kRecompute) s_err_flag[threadIdx.x] = 0;
-    if constexpr (kRecompute) count_begin();
     const int64_t total = p.adj_offset[N];
     const int lane = threadIdx.x & 31;
     const int64_t first = kWarp ? (blockIdx.x * int64_t(blockDim.x) + threadIdx.x) / 32
@@ -1331,7 +1314,6 @@ __global__ void __launch_bounds__(kThreads) pull_generic_kernel(const __grid_con
             else p.adj[j][e] = acc ? T(double(p.adj[j][e]) + sum) : T(sum);
         }
     }
-    if constexpr (kRecompute) count_flush(p.tcount);
 }
 
 // Generic pullback, arguments reduced over many output cells, cut into
@@ -1381,7 +1363,6 @@ template <class Body, class T, bool kRecompute>
 __global__ void __launch_bounds__(kThreads) pull_generic_seg_kernel(const __grid_constant__ GenParams<Body::kIn, Body::kOut, T> p) {
     constexpr int N = Body::kIn;
     if constexpr (Body::kMayRaise && kRecompute) s_err_flag[threadIdx.x] = 0;
-    if constexpr (kRecompute) count_begin();
     __shared__ double part[kThreads];
     const int64_t b = blockIdx.x;
     int j = 0;
@@ -1468,8 +1449,7 @@ __global__ void __launch_bounds__(kThreads) pull_generic_seg_kernel(const __grid
             advance();
         }
         p.seg_ws[p.seg_offset[j] + e * S + seg] = sum;
-        if constexpr (kRecompute) count_flush(p.tcount);
-        return;
+            return;
     }
     {
         // threads stride the segment by kThreads cells: the odometer advances
@@ -1520,7 +1500,6 @@ __global__ void __launch_bounds__(kThreads) pull_generic_seg_kernel(const __grid
             advance();
         }
     }
-    if constexpr (kRecompute) count_flush(p.tcount);
     part[threadIdx.x] = sum;
     __syncthreads();
     for (int stride = kThreads / 2; stride > 0; stride >>= 1) {
@@ -1547,6 +1526,75 @@ __global__ void __launch_bounds__(kThreads) pull_generic_seg_finish(const __grid
     for (int k = 0; k < S; ++k) sum += p.seg_ws[p.seg_offset[j] + e * S + k];
     const bool acc = (p.acc_mask >> j) & 1u;
     p.adj[j][e] = acc ? T(double(p.adj[j][e]) + sum) : T(sum);
+}
+
+// ------------------------------------------------- transcendental census
+// Tally<T>: a real that counts its exp / log / sin / cos / tanh / sigmoid
+// evaluations (the reference's counting wrappers, dual.hpp:55-60, 280-320)
+// into this thread's s_tcount slot. Primal values are computed exactly as the
+// production kernels compute them (same d_* calls, same operation order under
+// --fmad=false), so every branch a body takes on Tally is the branch the
+// production kernel took on that cell.
+template <class T>
+struct Tally {
+    T v;
+    BCAD_HD Tally() : v(T(0)) {}
+    BCAD_HD Tally(T x) : v(x) {}  // NOLINT: bodies mix reals and literals
+    template <class U, class = std::enable_if_t<std::is_arithmetic_v<U> && !std::is_same_v<U, T>>>
+    BCAD_HD Tally(U x) : v(T(x)) {}  // NOLINT
+};
+__device__ __forceinline__ void tally_one() { s_tcount[threadIdx.x] += 1u; }
+#define BCAD_TALLY_BIN(OP)                                                                                    \
+    template <class T> BCAD_HD Tally<T> operator OP(const Tally<T>& a, const Tally<T>& b) { return Tally<T>(a.v OP b.v); } \
+    template <class T> BCAD_HD Tally<T> operator OP(const Tally<T>& a, double b) { return Tally<T>(a.v OP T(b)); }       \
+    template <class T> BCAD_HD Tally<T> operator OP(double a, const Tally<T>& b) { return Tally<T>(T(a) OP b.v); }
+BCAD_TALLY_BIN(+)
+BCAD_TALLY_BIN(-)
+BCAD_TALLY_BIN(*)
+BCAD_TALLY_BIN(/)
+#undef BCAD_TALLY_BIN
+#define BCAD_TALLY_CMP(OP)                                                                                    \
+    template <class T> BCAD_HD bool operator OP(const Tally<T>& a, const Tally<T>& b) { return a.v OP b.v; }            \
+    template <class T> BCAD_HD bool operator OP(const Tally<T>& a, double b) { return a.v OP T(b); }                    \
+    template <class T> BCAD_HD bool operator OP(double a, const Tally<T>& b) { return T(a) OP b.v; }
+BCAD_TALLY_CMP(<)
+BCAD_TALLY_CMP(>)
+BCAD_TALLY_CMP(<=)
+BCAD_TALLY_CMP(>=)
+BCAD_TALLY_CMP(==)
+BCAD_TALLY_CMP(!=)
+#undef BCAD_TALLY_CMP
+template <class T> BCAD_HD Tally<T> operator-(const Tally<T>& a) { return Tally<T>(-a.v); }
+template <class T> __device__ Tally<T> sigmoid(const Tally<T>& a) { tally_one(); return Tally<T>(raw_sigmoid(a.v)); }
+template <class T> __device__ Tally<T> tanh(const Tally<T>& a) { tally_one(); return Tally<T>(d_tanh(a.v)); }
+template <class T> __device__ Tally<T> exp(const Tally<T>& a) { tally_one(); return Tally<T>(d_exp(a.v)); }
+template <class T> __device__ Tally<T> log(const Tally<T>& a) { tally_one(); return Tally<T>(d_log(a.v)); }
+template <class T> __device__ Tally<T> sin(const Tally<T>& a) { tally_one(); return Tally<T>(d_sin(a.v)); }
+template <class T> __device__ Tally<T> cos(const Tally<T>& a) { tally_one(); return Tally<T>(d_cos(a.v)); }
+template <class T> __device__ Tally<T> sqrt(const Tally<T>& a) { return Tally<T>(d_sqrt(a.v)); }
+template <class T> __device__ Tally<T> abs(const Tally<T>& a) { return Tally<T>(a.v < T(0) ? -a.v : a.v); }
+template <class T> __device__ Tally<T> pow(const Tally<T>& a, double c) { return Tally<T>(d_pow(a.v, T(c))); }
+template <class T> struct scalar_of<Tally<T>> { using type = T; };
+
+// One census pass over the output cells of a launch that just ran: the body
+// on Tally scalars per cell (kSelect: the branch-free select form, which the
+// production kernels use when the boundary bits vary per cell), tallies
+// flushed once per warp. Only launched while the census is armed.
+template <class Body, class T, bool kSelect>
+__global__ void __launch_bounds__(kThreads) census_kernel(const __grid_constant__ GenParams<Body::kIn, Body::kOut, T> p) {
+    constexpr int N = Body::kIn, M = Body::kOut;
+    count_begin();
+    for (int64_t cell = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; cell < p.vol;
+         cell += int64_t(gridDim.x) * blockDim.x) {
+        int64_t off[N];
+        decode_offsets<N, M, T>(p, cell, off);
+        Tally<T> xi[N], yo[M];
+#pragma unroll
+        for (int j = 0; j < N; ++j) xi[j] = Tally<T>(p.in[j][off[j]]);
+        if constexpr (kSelect) Body::template body_select<Tally<T>>(xi, yo);
+        else Body::template body<Tally<T>>(xi, yo);
+    }
+    count_flush(p.tcount);
 }
 
 }  // namespace bcad_dev

@@ -108,6 +108,29 @@ void fill_generic(bcad_dev::GenParams<N, M, T>& g, const Plan& plan) {
     }
 }
 
+// The transcendental census (kernels.cuh census_kernel): one launch after a
+// body-evaluating launch, only while counting is armed (FwdArgs / PullArgs
+// tcount non-null). kSelect mirrors the production kernel's choice of the
+// branch-free select form (static signature whose predicates vary per cell).
+template <class Body, class S>
+constexpr bool census_select() {
+    if constexpr (S::kStatic) return Body::kSelectForm && !bcad_dev::vec_eval_ok<Body, S>();
+    else return false;
+}
+template <class Body, class T>
+int launch_census(const Plan& plan, const void* const* in, unsigned long long* tcount, bool select, cudaStream_t s,
+                  std::string* err) {
+    constexpr int N = Body::kIn, M = Body::kOut;
+    bcad_dev::GenParams<N, M, T> g{};
+    fill_generic(g, plan);
+    for (int j = 0; j < N; ++j) g.in[j] = static_cast<const T*>(in[j]);
+    g.tcount = tcount;
+    const int grid = generic_grid(plan.vol);
+    if (select) bcad_dev::census_kernel<Body, T, true><<<grid, kThreads, 0, s>>>(g);
+    else bcad_dev::census_kernel<Body, T, false><<<grid, kThreads, 0, s>>>(g);
+    return cuda_status(cudaGetLastError(), err);
+}
+
 // ---------------------------------------------------------------- forward
 // K1's cells per thread: one 128-bit vector, unless the body caps it
 // (Body::kMaxVec) because its dual state per cell is wide enough that V
@@ -170,7 +193,6 @@ int launch_fwd2d(const FwdArgs& a, std::string* err) {
     p.rows = plan.rows;
     p.cols = plan.cols;
     p.err = a.err;
-    p.tcount = a.tcount;
     bool dense = true;  // every output pointer present: no per-store checks
     for (int i = 0; i < M; ++i) {
         dense = dense && p.primal[i];
@@ -196,7 +218,9 @@ int launch_fwd2d(const FwdArgs& a, std::string* err) {
         p.rpt = t.rpt;
         p.tile_rows = t.tile_rows;
         const dim3 grid(unsigned(t.n_col_tiles), unsigned(t.n_row_tiles));
-        return cuda_status(launch_pdl(kern, grid, 0, a.stream, p), err);
+        if (const int rc = cuda_status(launch_pdl(kern, grid, 0, a.stream, p), err)) return rc;
+        if (a.tcount) return launch_census<Body, T>(plan, a.in, a.tcount, census_select<Body, S>(), a.stream, err);
+        return int(BCAD_CU_OK);
     });
 }
 
@@ -225,7 +249,6 @@ int launch_fwd_t(const FwdArgs& a, std::string* err) {
         for (int j = 0; j < N; ++j) g.partials[i * N + j] = a.partials ? static_cast<T*>(a.partials[i * N + j]) : nullptr;
     }
     g.err = a.err;
-    g.tcount = a.tcount;
     if constexpr (generic_vec_width<Body, T>() > 1) {
         constexpr int GV = generic_vec_width<Body, T>();
         bool gvec = generic_vec_ok(plan, GV);
@@ -240,13 +263,15 @@ int launch_fwd_t(const FwdArgs& a, std::string* err) {
             const int grid = generic_grid(plan.vol / GV);
             if (real) bcad_dev::fwd_generic_vec_kernel<Body, T, GV, true><<<grid, kThreads, 0, a.stream>>>(g);
             else bcad_dev::fwd_generic_vec_kernel<Body, T, GV, false><<<grid, kThreads, 0, a.stream>>>(g);
-            return cuda_status(cudaGetLastError(), err);
+            if (const int rc = cuda_status(cudaGetLastError(), err)) return rc;
+            return a.tcount ? launch_census<Body, T>(plan, a.in, a.tcount, false, a.stream, err) : BCAD_CU_OK;
         }
     }
     const int grid = generic_grid(plan.vol);
     if (real) bcad_dev::fwd_generic_kernel<Body, T, true><<<grid, kThreads, 0, a.stream>>>(g);
     else bcad_dev::fwd_generic_kernel<Body, T, false><<<grid, kThreads, 0, a.stream>>>(g);
-    return cuda_status(cudaGetLastError(), err);
+    if (const int rc = cuda_status(cudaGetLastError(), err)) return rc;
+    return a.tcount ? launch_census<Body, T>(plan, a.in, a.tcount, false, a.stream, err) : BCAD_CU_OK;
 }
 
 // --------------------------------------------------------------- pullback
@@ -324,7 +349,6 @@ int launch_pull2d(const PullArgs& a, std::string* err) {
     p.ws_col = reinterpret_cast<double*>(ws + L.ws_col);
     p.ws_scalar = reinterpret_cast<double*>(ws + L.ws_scalar);
     p.err = a.err;
-    p.tcount = a.tcount;
     int64_t fin_blocks = bcad_dev::pull_finish_blocks(plan.rows, plan.cols, p.n_row_tiles, p.n_col_tiles, nr, nc, ns);
     // cross-CTA reductions combined inside K2 (completion tickets) unless the
     // tiling asks for the separate K2f launch
@@ -374,6 +398,8 @@ int launch_pull2d(const PullArgs& a, std::string* err) {
         }
         int rc = cuda_status(launch_pdl(kern, grid, smem, a.stream, p), err);
         if (rc) return rc;
+        if (recompute && a.tcount)  // K2r re-evaluated every cell's body
+            if ((rc = launch_census<Body, T>(plan, a.in, a.tcount, census_select<Body, S>(), a.stream, err))) return rc;
         if (ar_blocks > 0) {
             cudaLaunchConfig_t cfg = {};
             cfg.gridDim = dim3(unsigned(ar_blocks));
@@ -433,7 +459,6 @@ int launch_pull_t(const PullArgs& a, std::string* err) {
         for (int j = 0; j < N; ++j) g.D[i * N + j] = recompute ? nullptr : static_cast<const T*>(a.partials[i * N + j]);
     }
     g.err = a.err;
-    g.tcount = a.tcount;
     bcad_dev::GenParams<N, M, T> gw = g, gs = g, gf = g;
     bool any_full = false;
     // arguments reduced over many cells per element: segmented (needs the
@@ -511,6 +536,14 @@ int launch_pull_t(const PullArgs& a, std::string* err) {
         else bcad_dev::pull_generic_kernel<Body, T, false, true><<<grid, kThreads, 0, a.stream>>>(gw);
         if (const int rc = cuda_status(cudaGetLastError(), err)) return rc;
     }
+    if (recompute && a.tcount) {
+        // the generic RecomputeReverse kernels re-evaluate every cell once for
+        // the full-shape arguments together and once per reduced argument
+        int passes = any_full ? 1 : 0;
+        for (int j = 0; j < N; ++j) passes += a.in_adj[j] && plan.arg_vol[j] != plan.vol;
+        for (int k = 0; k < passes; ++k)
+            if (const int rc = launch_census<Body, T>(plan, a.in, a.tcount, false, a.stream, err)) return rc;
+    }
     return BCAD_CU_OK;
 }
 
@@ -559,7 +592,7 @@ using SigPredRow = typename SigPredRowT<N, PRED>::type;
     bcad_cu_kernel_entry {                                                                             \
         Body::kName, Body::kIn, Body::kOut, Body::kMayRaise,                                           \
             &bcad_cu_impl::launch_fwd_any<Body __VA_OPT__(, ) __VA_ARGS__>,                             \
-            &bcad_cu_impl::launch_pull_any<Body __VA_OPT__(, ) __VA_ARGS__>, &bcad_dev::arm_counts_tu   \
+            &bcad_cu_impl::launch_pull_any<Body __VA_OPT__(, ) __VA_ARGS__>                             \
     }
 
 // A registered body whose forward also gets signature S but whose pullback
@@ -568,5 +601,5 @@ using SigPredRow = typename SigPredRowT<N, PRED>::type;
 #define BCAD_ENTRY_FWD_SIG(Body, S)                                                                    \
     bcad_cu_kernel_entry {                                                                             \
         Body::kName, Body::kIn, Body::kOut, Body::kMayRaise, &bcad_cu_impl::launch_fwd_any<Body, S>,    \
-            &bcad_cu_impl::launch_pull_any<Body>, &bcad_dev::arm_counts_tu                             \
+            &bcad_cu_impl::launch_pull_any<Body>                                                       \
     }

@@ -51,9 +51,6 @@ struct bcad_cu_kernel_entry {
     bool may_raise;
     int (*fwd)(const bcad_cu_impl::FwdArgs&, std::string*);
     int (*pull)(const bcad_cu_impl::PullArgs&, std::string*);
-    // arms (1) / disarms (0) the transcendental census of the translation
-    // unit that instantiated fwd / pull, on the current device
-    int (*arm_counts)(int on) = nullptr;
 };
 
 // One registration group per translation unit (compiled in parallel).

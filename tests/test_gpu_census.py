@@ -1,4 +1,4 @@
-"""Device transcendental census (bcad_cu_eval_counters; dual.cuh count_tr):
+"""Device transcendental census (bcad_cu_eval_counters; kernels.cuh census_kernel):
 the kernels count exp / log / sin / cos / tanh / sigmoid evaluations like the
 reference's counting wrappers (dual.hpp:55-60, 280-320) — per cell and per
 branch taken: UPDATE 3, FLUSH 2, COPY 0 for cell_update_scalar
