@@ -45,9 +45,9 @@ struct Registry {
     std::mutex mu;
     std::vector<const bcad_cu_kernel_entry*> all;
     Registry() {
-        int (*groups[])(const bcad_cu_kernel_entry**) = {&bcad_reg_hmlstm, &bcad_reg_pool,       &bcad_reg_probe,
-                                                         &bcad_reg_prims,  &bcad_reg_arity,      &bcad_reg_arity_wide,
-                                                         &bcad_reg_arity_wide32};
+        int (*groups[])(const bcad_cu_kernel_entry**) = {&bcad_reg_hmlstm,       &bcad_reg_pool,  &bcad_reg_pool_b,
+                                                         &bcad_reg_probe,        &bcad_reg_prims, &bcad_reg_arity,
+                                                         &bcad_reg_arity_wide,   &bcad_reg_arity_wide32};
         for (auto g : groups) {
             const bcad_cu_kernel_entry* e = nullptr;
             const int n = g(&e);

@@ -126,8 +126,13 @@ int launch_census(const Plan& plan, const void* const* in, unsigned long long* t
     for (int j = 0; j < N; ++j) g.in[j] = static_cast<const T*>(in[j]);
     g.tcount = tcount;
     const int grid = generic_grid(plan.vol);
-    if (select) bcad_dev::census_kernel<Body, T, true><<<grid, kThreads, 0, s>>>(g);
-    else bcad_dev::census_kernel<Body, T, false><<<grid, kThreads, 0, s>>>(g);
+    bool launched = false;
+    if constexpr (Body::kSelectForm)  // only bodies with a select form instantiate it
+        if (select) {
+            bcad_dev::census_kernel<Body, T, true><<<grid, kThreads, 0, s>>>(g);
+            launched = true;
+        }
+    if (!launched) bcad_dev::census_kernel<Body, T, false><<<grid, kThreads, 0, s>>>(g);
     return cuda_status(cudaGetLastError(), err);
 }
 

@@ -56,6 +56,7 @@ struct bcad_cu_kernel_entry {
 // One registration group per translation unit (compiled in parallel).
 int bcad_reg_hmlstm(const bcad_cu_kernel_entry** out);
 int bcad_reg_pool(const bcad_cu_kernel_entry** out);
+int bcad_reg_pool_b(const bcad_cu_kernel_entry** out);
 int bcad_reg_probe(const bcad_cu_kernel_entry** out);
 int bcad_reg_arity(const bcad_cu_kernel_entry** out);
 int bcad_reg_arity_wide(const bcad_cu_kernel_entry** out);
